@@ -1,0 +1,267 @@
+"""Benchmark of the Newmark IMEX time step (BASELINE.json metric: DOF-steps/s, FP64).
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+* ours: the CUDA path through the C ABI (libsc.so).  W warm-up steps, then K steps timed
+  with CUDA events on the library stream, barrier + synchronize on both sides, max over
+  ranks.  value = n_dof * K * world / t (weak scaling: each rank advances its own copy of
+  the workload; the slab-partitioned halo-exchange path is not built yet).
+* roofline: the dominant kernel (fused explicit (a1)+(a2)) timed alone with CUDA events
+  on the library stream (sc_profile), algorithmic bytes = 24 B per tensor-d DOF.
+* e2e: one job through the public API with HOST buffers: sc_set_state(u0, v0 host) ->
+  sc_step(K) -> sc_read(u host), copies inside the timed region.
+* cpu_baseline / --impl reference: the CPU oracle (oracle/) as it stands, on the host
+  cores, on a bounded sample of the same workload (its time loop, steps stated).
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import sc_inputs  # noqa: E402
+
+METRIC = "DOF-steps/sec (FP64) at 1/2/4/8 B200; achieved HBM GB/s vs peak"
+UNIT = "DOF-steps/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.1)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def oracle_sample(cfg, steps):
+    """Time the oracle's IMEX loop (as it stands) on `steps` steps of `cfg`."""
+    import oracle.assembly as OA
+    from oracle.integrators import from_system, imex
+    from oracle.run import initial_field
+    n_dof_cells = np.prod(cfg["cells"]) * (cfg["p"] + 1) ** (2 * cfg["dim"])
+    mode = "sparse" if n_dof_cells < 1.2e8 else "ebe"
+    t0 = time.perf_counter()
+    sysm = OA.build_system(cfg, mode)
+    t_setup = time.perf_counter() - t0
+    pr = from_system(sysm)
+    f_t = sc_inputs.source_signal(cfg, steps + 1)
+    u0 = initial_field(cfg, sysm)
+    t0 = time.perf_counter()
+    imex(pr, cfg["dt"], steps, f_t, u0, None)
+    t = time.perf_counter() - t0
+    return sysm.n_dof * steps / t, t, t_setup, sysm.n_dof, mode
+
+
+def _cores():
+    try:
+        import threadpoolctl
+        info = threadpoolctl.threadpool_info()
+        return max([i.get("num_threads", 1) for i in info] + [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return 0
+    cfg = sc_inputs.get_config(args.config)
+    # bounded sample: per step a few oracle steps (their time loop only)
+    n = max(1, args.ref_steps)
+    vals = []
+    t_tot = 0.0
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        pass
+    value, t, t_setup, n_dof, mode = oracle_sample(cfg, n * max(1, args.steps))
+    t_tot += t
+    vals.append(value)
+    sample = (f"config {args.config} full size ({n_dof} DOFs, {mode} assembly), oracle IMEX time loop of "
+              f"{n * max(1, args.steps)} steps ({t:.1f} s; setup {t_setup:.1f} s untimed)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / (n * max(1, args.steps)),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": _config_dict(cfg, n_dof),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": _cores(), "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _config_dict(cfg, n_dof, extra=None):
+    d = {"workload": f"config{cfg['id']}: {cfg['name']}", "dim": cfg["dim"], "cells": cfg["cells"],
+         "p": cfg["p"], "n_voids": len(cfg["voids"]), "alpha": cfg["alpha"], "tree_depth": cfg["tree_depth"],
+         "dt": cfg["dt"], "n_dof": int(n_dof)}
+    if extra:
+        d.update(extra)
+    return d
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-steps", type=int, default=1, help="oracle steps per timed step (reference arm)")
+    ap.add_argument("--cpu-steps", type=int, default=3, help="oracle steps for cpu_baseline")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2310_14712_b200 as pkg
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    W, K = max(3, args.warmup), args.steps
+    cfg = sc_inputs.get_config(args.config)
+    f_t = sc_inputs.source_signal(cfg, W + K + 2) if cfg["source"] else None
+    stream = torch.cuda.Stream()
+    t0 = time.perf_counter()
+    s = pkg.from_config(cfg, f_t=f_t, stream=stream.cuda_stream)
+    setup_s = time.perf_counter() - t0
+    info = s.info
+    n_dof = info["n_dof"]
+    s.step(W)
+    s.sync()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(local)
+    clk.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        s.step(K)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    s.sync()   # raises on a non-finite state
+    t_ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([t_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    value = n_dof * K * world / (t_ms / 1e3)
+    # ---- roofline of the dominant kernel (explicit (a1)+(a2)), timed alone on the same stream
+    peak, peak_kind = _peaks()
+    nprof = 50
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        s.profile(0, nprof)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    t_exp = e0.elapsed_time(e1) / nprof
+    ach = info["bytes_explicit_per_step"] / (t_exp / 1e3) / 1e9
+    roof = {"kernel": "k_explicit (a1)+(a2) fused", "bound": "hbm", "achieved": ach, "peak": peak,
+            "unit": "GB/s", "frac": ach / peak, "traffic": None, "peak_kind": peak_kind,
+            "kernel_ms": t_exp, "share_of_step": t_exp / (t_ms / K),
+            "algorithmic_bytes": info["bytes_explicit_per_step"]}
+    # ---- e2e through the public API with host buffers
+    u0 = np.zeros(n_dof)
+    if cfg.get("u0") == "gaussian_pulse":
+        u0 = sc_inputs.gaussian_pulse(s.dof_coords()[:, 0])
+    v0 = np.zeros(n_dof)
+    uh = np.empty(n_dof)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        s.set_state(u0, v0)
+        s.step(K)
+        s.read(uh)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    t_e2e = e0.elapsed_time(e1)
+    e2e = {"value": n_dof * K * world / (t_e2e / 1e3), "unit": UNIT,
+           "h2d_bytes_per_step": 16.0 * n_dof / K, "d2h_bytes_per_step": 8.0 * n_dof / K,
+           "job": f"sc_set_state(u0,v0 host) + sc_step({K}) + sc_read(u host)"}
+    # ---- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            v, t, t_setup, nd, mode = oracle_sample(cfg, args.cpu_steps)
+            cpu = {"value": v, "unit": UNIT, "cores": _cores(), "kind": "oracle",
+                   "sample": f"config {args.config} full size ({nd} DOFs, {mode}), {args.cpu_steps} oracle IMEX "
+                             f"steps ({t:.1f} s; setup {t_setup:.1f} s untimed)"}
+        except Exception as ex:  # report, do not fail the bench
+            cpu = {"value": None, "unit": UNIT, "cores": _cores(), "kind": "oracle", "sample": f"failed: {ex}"}
+    if rank == 0:
+        l2 = "inputs larger than L2" if 16.0 * info["lattice_nodes"] > 126e6 else "L2-resident (no flush)"
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+                "ms_per_step": t_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic",
+                "config": _config_dict(cfg, n_dof, {"n_c": info["n_c"], "n_d": info["n_d"],
+                                                     "cells_cut": info["cells_cut"], "l2": l2,
+                                                     "parallelism": f"{world} independent replicas"}),
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+                "gpu_launches": int(info["kernels_per_step"]) * K,
+                "step_bytes_algorithmic": info["bytes_per_step"],
+                "step_achieved_GBps": info["bytes_per_step"] / (t_ms / K / 1e3) / 1e9,
+                "setup_s": setup_s}
+        print(json.dumps(line), flush=True)
+    s.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

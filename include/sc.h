@@ -1,0 +1,181 @@
+/*
+ * sc.h - C ABI of the B200-native immersed Newmark IMEX spectral cell solver.
+ *
+ * The problem statement these calls take follows PAPER.md (arXiv 2310.14712):
+ *   rho u'' - div(rho c^2 grad u) = f on the extended box Omega = Omega_p U Omega_f
+ *   (Eq. eq:scalarWaveEq), homogeneous Neumann on the box,
+ *   FCM indicator alpha = 1 in Omega_p, alpha_f in Omega_f,
+ *   order-p GLL spectral cells on a Cartesian grid,
+ *   separable load f = f_t(t) f_x,
+ *   Newmark IMEX time stepping: explicit CDM on the 'd' DOFs
+ *   (supported only by uncut cells), implicit trapezoidal Newmark on the
+ *   'c' DOFs (supported by >= 1 cut cell).
+ *
+ * Conventions (all functions):
+ *  - Every pointer argument is a HOST pointer unless stated otherwise; the
+ *    caller owns it; inputs are copied during the call and may be freed after.
+ *  - The context owns all device memory, the factors, the CUDA graphs and (for
+ *    world > 1) the NCCL communicator.  sc_destroy releases everything.
+ *  - Errors are returned as sc_status; a human-readable message is available
+ *    from sc_last_error(ctx).  No function aborts the process.
+ *  - Canonical DOF order: retained lattice nodes (nodes of non-empty cells,
+ *    P:866) in lexicographic order, x fastest; lattice index
+ *    = i + n0*(j + n1*k) with n_k = cells[k]*p + 1.
+ *  - All floating point is IEEE fp64.
+ */
+#ifndef SC_H
+#define SC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sc_ctx sc_ctx; /* opaque */
+
+typedef enum {
+  SC_OK = 0,
+  SC_ERR_CONFIG = 2,  /* invalid argument / unsupported configuration (SPEC exit code 2) */
+  SC_ERR_NUMERIC = 3, /* non-finite state or non-positive pivot (SPEC exit code 3) */
+  SC_ERR_CUDA = 4,    /* CUDA runtime error */
+  SC_ERR_NCCL = 5,    /* NCCL error (world > 1) */
+  SC_ERR_OOM = 6,     /* device or host allocation failed */
+  SC_ERR_STATE = 7    /* call not valid in the current state (e.g. NULL ctx) */
+} sc_status;
+
+/* Uniform Cartesian grid of the extended domain Omega (Fig. fig:FCM).
+ * dim in {1,2,3}; cells[k] >= 1 and lo[k] < hi[k] for k < dim (entries k >= dim ignored). */
+typedef struct {
+  int32_t dim;
+  int32_t cells[3];
+  double lo[3];
+  double hi[3];
+} sc_grid;
+
+/* One void (part of the fictitious domain Omega_f).
+ *  kind SC_VOID_ELLIPSOID: void = {x : (x-c)^T A (x-c) < 1} (strict: Omega_p is closed),
+ *       A symmetric positive definite, packed A00,A11,A22,A01,A02,A12 (unused dims 0);
+ *  kind SC_VOID_HALFSPACE: void = {x : n.x > b}.
+ * Membership is evaluated exactly as DESIGN.md reading C17 (no FMA). */
+enum { SC_VOID_ELLIPSOID = 1, SC_VOID_HALFSPACE = 2 };
+typedef struct {
+  int32_t kind;
+  double c[3];
+  double A[6];
+  double n[3];
+  double b;
+} sc_void;
+
+/* Geometry and material.  tree_depth = spacetree depth D; lattice_s = s of the
+ * cut-test lattice (reading C6, default 4); fill_eps = empty-cell threshold (P:866-868,
+ * default 1e-10; reading C7); rho, c constant (reading C10). */
+typedef struct {
+  int32_t n_voids;
+  const sc_void* voids;
+  int32_t tree_depth;
+  int32_t lattice_s;
+  double fill_eps;
+  double rho;
+  double c;
+} sc_geometry;
+
+/* Separable point source f(x,t) = f_t(t) delta(x - x_s) (reading C11):
+ * f_x,i = alpha(x_s) N_i(x_s) in the lowest-index non-empty cell containing x_s.
+ * f_t[k] = f_t(k*dt) for k < n_t (host array, copied); f_t = 0 beyond n_t.
+ * kind 0 = no source (f_t ignored), 1 = point source. */
+typedef struct {
+  int32_t kind;
+  double x[3];
+  int64_t n_t;
+  const double* f_t;
+} sc_source;
+
+/* Distribution: NULL => one GPU (current device, current stream semantics below).
+ * rank/world: slab decomposition over world ranks (NCCL over NVLink); device: CUDA
+ * device ordinal; nccl_unique_id: 128-byte ncclUniqueId shared by all ranks (world>1);
+ * cuda_stream: cudaStream_t to enqueue on (NULL => the context creates its own). */
+typedef struct {
+  int32_t rank;
+  int32_t world;
+  int32_t device;
+  const void* nccl_unique_id;
+  void* cuda_stream;
+} sc_dist;
+
+typedef struct {
+  int64_t n_dof, n_d, n_c;          /* retained DOFs; |I_d|; |I_c| */
+  int64_t n_irregular;              /* d DOFs updated off the tensor kernel (touching an
+                                       empty cell, or carrying the point load) */
+  int64_t cells_uncut, cells_cut, cells_empty;
+  int64_t n_components;             /* connected components of the c-graph (blocks of S) */
+  int64_t n_supernodes;
+  int64_t nnz_factor;               /* stored entries of the S factor (Linv + L panels) */
+  int32_t factor_height;            /* supernodal elimination-tree height */
+  double dt;
+  double dt_crit_uncut;             /* 2/sqrt(lambda_max(K_e, M_e)) of an uncut cell */
+  int64_t step;                     /* steps taken since the last (re)start */
+  double bytes_per_step;            /* algorithmic HBM bytes per step */
+  double bytes_explicit_per_step;   /* ... of the fused explicit (a1)+(a2) kernel alone */
+  int32_t kernels_per_step;         /* kernel launches per step */
+  int64_t lattice_nodes;            /* prod(cells*p+1) */
+  double setup_seconds;
+} sc_info;
+
+/* Build the discretisation, classify cells and DOFs, integrate the cut cells, factor
+ * S = M^cc + dt^2/4 K^cc once and compute the consistent start
+ * (reading C3).  u0, v0: nullable host arrays of length n_dof in canonical order (NULL =>
+ * zero); since n_dof is only known after classification, callers with a nonzero initial
+ * field pass NULL here and then call sc_set_state.  dt is fixed for the context (S depends
+ * on dt).  On success *out receives the new context; on failure *out is NULL and the
+ * message is available from sc_last_error(NULL) (thread-local). */
+sc_status sc_setup(const sc_grid* grid, int32_t p, double alpha, const sc_geometry* geom,
+                   double dt, const sc_source* src, const double* u0, const double* v0,
+                   const sc_dist* dist, sc_ctx** out);
+
+/* Reset the state to (u0, v0) at t = 0 (host arrays, length n_dof, canonical order; NULL =>
+ * zero) and recompute the start a_0 = M^-1 (f_t(0) f_x - K u0), u^d_-1 (reading C3). */
+sc_status sc_set_state(sc_ctx* ctx, const double* u0, const double* v0);
+
+/* Enqueue n >= 0 Newmark IMEX steps (steps (a1)-(a6) of DESIGN.md §2) on the
+ * context stream.  Asynchronous: returns after enqueueing.  Blow-up (non-finite u) sets a
+ * device flag that sc_sync / sc_read report as SC_ERR_NUMERIC. */
+sc_status sc_step(sc_ctx* ctx, int64_t n);
+
+/* Wait for all enqueued work; SC_ERR_NUMERIC if a non-finite value was produced. */
+sc_status sc_sync(sc_ctx* ctx);
+
+/* Copy u_n (canonical order) to the host array u of length len >= n_dof.  Synchronises. */
+sc_status sc_read(sc_ctx* ctx, double* u, int64_t len);
+
+/* Copy v^c_n and a^c_n of the c DOFs (canonical order of I_c) to host arrays (nullable). */
+sc_status sc_read_c_state(sc_ctx* ctx, double* v_c, double* a_c, int64_t len);
+
+/* Counters and sizes; see sc_info. */
+sc_status sc_query(sc_ctx* ctx, sc_info* out);
+
+/* Classification readback: cell_class[prod(cells)] (0 uncut, 1 cut, 2 empty; cells x
+ * fastest), dof_is_c[n_dof] (1 = c DOF), dof_lattice_index[n_dof].  Each nullable. */
+sc_status sc_read_classification(sc_ctx* ctx, int8_t* cell_class, uint8_t* dof_is_c,
+                                 int64_t* dof_lattice_index);
+
+/* Physical coordinates of the DOFs (GLL node positions): xyz[3*i + k], len >= 3*n_dof. */
+sc_status sc_dof_coords(sc_ctx* ctx, double* xyz, int64_t len);
+
+/* Instrumentation: enqueue n launches of ONE sub-kernel of the step on the context stream
+ * so that a caller can time it with events: which = 0 fused explicit (a1)+(a2) tensor
+ * kernel, 1 c-element products (a4), 2 supernodal solve of S (a5).  Clobbers the state:
+ * call sc_set_state before stepping again. */
+sc_status sc_profile(sc_ctx* ctx, int32_t which, int64_t n);
+
+/* Last error message of ctx (or of the calling thread's last failed sc_setup if NULL). */
+const char* sc_last_error(const sc_ctx* ctx);
+
+/* Release the context and everything it owns.  NULL is a no-op. */
+void sc_destroy(sc_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SC_H */

@@ -1,0 +1,246 @@
+"""B200-native immersed Newmark IMEX spectral cell solver (arXiv 2310.14712).
+
+Thin Python binding over the C ABI of ``libsc.so`` (``include/sc.h``): argument
+marshalling only - every step of the method runs in the library's CUDA kernels.
+There is no CPU fallback: if the library is missing or cannot be loaded every
+call raises ``RuntimeError``.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsc.so")
+
+SC_OK, SC_ERR_CONFIG, SC_ERR_NUMERIC = 0, 2, 3
+SC_VOID_ELLIPSOID, SC_VOID_HALFSPACE = 1, 2
+
+
+class sc_grid(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int32), ("cells", ctypes.c_int32 * 3),
+                ("lo", ctypes.c_double * 3), ("hi", ctypes.c_double * 3)]
+
+
+class sc_void(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("c", ctypes.c_double * 3), ("A", ctypes.c_double * 6),
+                ("n", ctypes.c_double * 3), ("b", ctypes.c_double)]
+
+
+class sc_geometry(ctypes.Structure):
+    _fields_ = [("n_voids", ctypes.c_int32), ("voids", ctypes.POINTER(sc_void)),
+                ("tree_depth", ctypes.c_int32), ("lattice_s", ctypes.c_int32),
+                ("fill_eps", ctypes.c_double), ("rho", ctypes.c_double), ("c", ctypes.c_double)]
+
+
+class sc_source(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("x", ctypes.c_double * 3), ("n_t", ctypes.c_int64),
+                ("f_t", ctypes.POINTER(ctypes.c_double))]
+
+
+class sc_dist(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("nccl_unique_id", ctypes.c_void_p), ("cuda_stream", ctypes.c_void_p)]
+
+
+class sc_info(ctypes.Structure):
+    _fields_ = [("n_dof", ctypes.c_int64), ("n_d", ctypes.c_int64), ("n_c", ctypes.c_int64),
+                ("n_irregular", ctypes.c_int64), ("cells_uncut", ctypes.c_int64),
+                ("cells_cut", ctypes.c_int64), ("cells_empty", ctypes.c_int64),
+                ("n_components", ctypes.c_int64), ("n_supernodes", ctypes.c_int64),
+                ("nnz_factor", ctypes.c_int64), ("factor_height", ctypes.c_int32),
+                ("dt", ctypes.c_double), ("dt_crit_uncut", ctypes.c_double), ("step", ctypes.c_int64),
+                ("bytes_per_step", ctypes.c_double), ("bytes_explicit_per_step", ctypes.c_double),
+                ("kernels_per_step", ctypes.c_int32), ("lattice_nodes", ctypes.c_int64),
+                ("setup_seconds", ctypes.c_double)]
+
+
+EXPORTS = ("sc_setup", "sc_set_state", "sc_step", "sc_sync", "sc_read", "sc_read_c_state", "sc_query",
+           "sc_read_classification", "sc_dof_coords", "sc_profile", "sc_last_error", "sc_destroy")
+
+_lib = None
+
+
+def load_library(path=LIB_PATH):
+    """Load libsc.so (raises RuntimeError if it is missing: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"libsc.so not built at {path}; run __graft_entry__.build()")
+    lib = ctypes.CDLL(path)
+    P = ctypes.POINTER
+    lib.sc_setup.argtypes = [P(sc_grid), ctypes.c_int32, ctypes.c_double, P(sc_geometry), ctypes.c_double,
+                             P(sc_source), P(ctypes.c_double), P(ctypes.c_double), P(sc_dist),
+                             P(ctypes.c_void_p)]
+    lib.sc_set_state.argtypes = [ctypes.c_void_p, P(ctypes.c_double), P(ctypes.c_double)]
+    lib.sc_step.argtypes = [ctypes.c_void_p, ctypes.c_int64]
+    lib.sc_sync.argtypes = [ctypes.c_void_p]
+    lib.sc_read.argtypes = [ctypes.c_void_p, P(ctypes.c_double), ctypes.c_int64]
+    lib.sc_read_c_state.argtypes = [ctypes.c_void_p, P(ctypes.c_double), P(ctypes.c_double), ctypes.c_int64]
+    lib.sc_query.argtypes = [ctypes.c_void_p, P(sc_info)]
+    lib.sc_read_classification.argtypes = [ctypes.c_void_p, P(ctypes.c_int8), P(ctypes.c_uint8),
+                                           P(ctypes.c_int64)]
+    lib.sc_dof_coords.argtypes = [ctypes.c_void_p, P(ctypes.c_double), ctypes.c_int64]
+    lib.sc_profile.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64]
+    lib.sc_last_error.argtypes = [ctypes.c_void_p]
+    lib.sc_last_error.restype = ctypes.c_char_p
+    lib.sc_destroy.argtypes = [ctypes.c_void_p]
+    lib.sc_destroy.restype = None
+    for name in EXPORTS:
+        if name not in ("sc_last_error", "sc_destroy"):
+            getattr(lib, name).restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+class ScError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"sc status {status}: {msg}")
+        self.status = status
+
+
+def _dptr(a):
+    return None if a is None else a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+class Solver:
+    """One context of the library (sc_setup ... sc_destroy)."""
+
+    def __init__(self, grid, p, alpha, geometry, dt, source=None, u0=None, v0=None, stream=None, device=None):
+        lib = load_library()
+        self._lib = lib
+        dim = grid["dim"]
+        g = sc_grid()
+        g.dim = dim
+        for k in range(3):
+            g.cells[k] = grid["cells"][k] if k < dim else 1
+            g.lo[k] = grid["lo"][k] if k < dim else 0.0
+            g.hi[k] = grid["hi"][k] if k < dim else 0.0
+        vs = geometry.get("voids", [])
+        arr = (sc_void * max(1, len(vs)))()
+        for i, v in enumerate(vs):
+            if v["kind"] == "ellipsoid":
+                arr[i].kind = SC_VOID_ELLIPSOID
+                for k in range(3):
+                    arr[i].c[k] = v["c"][k]
+                for k in range(6):
+                    arr[i].A[k] = v["A"][k]
+            else:
+                arr[i].kind = SC_VOID_HALFSPACE
+                for k in range(3):
+                    arr[i].n[k] = v["n"][k]
+                arr[i].b = v["b"]
+        geo = sc_geometry(len(vs), arr, geometry.get("tree_depth", 2), geometry.get("lattice_s", 4),
+                          geometry.get("fill_eps", 1e-10), geometry.get("rho", 1.0), geometry.get("c", 1.0))
+        src = None
+        self._ft = None
+        if source is not None:
+            ft = np.ascontiguousarray(source["f_t"], dtype=np.float64)
+            self._ft = ft
+            src = sc_source()
+            src.kind = 1
+            for k in range(3):
+                src.x[k] = source["x"][k] if k < len(source["x"]) else 0.0
+            src.n_t = len(ft)
+            src.f_t = _dptr(ft)
+        dist = None
+        if stream is not None or device is not None:
+            dist = sc_dist(0, 1, -1 if device is None else int(device), None,
+                           ctypes.c_void_p(stream) if stream is not None else None)
+        ctx = ctypes.c_void_p()
+        u0a = None if u0 is None else np.ascontiguousarray(u0, dtype=np.float64)
+        v0a = None if v0 is None else np.ascontiguousarray(v0, dtype=np.float64)
+        st = lib.sc_setup(ctypes.byref(g), int(p), float(alpha), ctypes.byref(geo), float(dt),
+                          ctypes.byref(src) if src is not None else None, _dptr(u0a), _dptr(v0a),
+                          ctypes.byref(dist) if dist is not None else None, ctypes.byref(ctx))
+        if st != SC_OK:
+            raise ScError(st, lib.sc_last_error(None).decode())
+        self.ctx = ctx
+        self.info = self.query()
+
+    # -- ABI mirrors -------------------------------------------------------------
+    def _check(self, st):
+        if st != SC_OK:
+            raise ScError(st, self._lib.sc_last_error(self.ctx).decode())
+
+    def query(self):
+        inf = sc_info()
+        self._check(self._lib.sc_query(self.ctx, ctypes.byref(inf)))
+        return {k: getattr(inf, k) for k, _ in sc_info._fields_}
+
+    def set_state(self, u0=None, v0=None):
+        u0a = None if u0 is None else np.ascontiguousarray(u0, dtype=np.float64)
+        v0a = None if v0 is None else np.ascontiguousarray(v0, dtype=np.float64)
+        self._check(self._lib.sc_set_state(self.ctx, _dptr(u0a), _dptr(v0a)))
+
+    def step(self, n):
+        self._check(self._lib.sc_step(self.ctx, int(n)))
+
+    def sync(self):
+        self._check(self._lib.sc_sync(self.ctx))
+
+    def read(self, out=None):
+        n = self.info["n_dof"]
+        if out is None:
+            out = np.empty(n, dtype=np.float64)
+        self._check(self._lib.sc_read(self.ctx, _dptr(out), len(out)))
+        return out
+
+    def read_c_state(self):
+        n = self.info["n_c"]
+        v = np.empty(max(n, 1))
+        a = np.empty(max(n, 1))
+        self._check(self._lib.sc_read_c_state(self.ctx, _dptr(v), _dptr(a), n))
+        return v[:n], a[:n]
+
+    def classification(self):
+        n_cells = 1
+        # cell count from the lattice: product of cells; keep it from construction
+        cc = np.empty(self._n_cells, dtype=np.int8)
+        isc = np.empty(self.info["n_dof"], dtype=np.uint8)
+        lat = np.empty(self.info["n_dof"], dtype=np.int64)
+        del n_cells
+        self._check(self._lib.sc_read_classification(
+            self.ctx, cc.ctypes.data_as(ctypes.POINTER(ctypes.c_int8)),
+            isc.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)),
+            lat.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
+        return cc, isc.astype(bool), lat
+
+    def dof_coords(self):
+        n = self.info["n_dof"]
+        X = np.empty(3 * n)
+        self._check(self._lib.sc_dof_coords(self.ctx, _dptr(X), len(X)))
+        return X.reshape(n, 3)
+
+    def profile(self, which, n):
+        """Instrumentation: n launches of one sub-kernel (clobbers the state)."""
+        self._check(self._lib.sc_profile(self.ctx, int(which), int(n)))
+
+    def close(self):
+        if getattr(self, "ctx", None) is not None and self.ctx.value:
+            self._lib.sc_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def from_config(cfg, f_t=None, stream=None, device=None, set_initial=True):
+    """Build a Solver from an ``sc_inputs`` config dict (marshalling only)."""
+    src = None
+    if cfg.get("source") is not None:
+        if f_t is None:
+            from sc_inputs import source_signal
+            f_t = source_signal(cfg)
+        src = {"x": cfg["source"]["x"], "f_t": f_t}
+    geo = {k: cfg[k] for k in ("voids", "tree_depth", "lattice_s", "fill_eps", "rho", "c")}
+    s = Solver(cfg, cfg["p"], cfg["alpha"], geo, cfg["dt"], source=src, stream=stream, device=device)
+    s._n_cells = int(np.prod(cfg["cells"]))
+    if set_initial and cfg.get("u0") == "gaussian_pulse":
+        from sc_inputs import gaussian_pulse
+        s.set_state(gaussian_pulse(s.dof_coords()[:, 0]), None)
+    return s

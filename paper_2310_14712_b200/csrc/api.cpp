@@ -1,0 +1,367 @@
+// C ABI entry points of libsc (include/sc.h).
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "sc_internal.h"
+
+static thread_local std::string g_setup_err;
+
+static sc_status fail(sc_ctx* c, const ScError& e) {
+  if (c) c->err = e.msg;
+  else g_setup_err = e.msg;
+  return e.st;
+}
+
+static void free_ctx(sc_ctx* c) {
+  if (!c) return;
+  int cur = -1;
+  cudaGetDevice(&cur);
+  cudaSetDevice(c->device);
+  for (int i = 0; i < 2; ++i)
+    if (c->graph[i]) cudaGraphExecDestroy(c->graph[i]);
+  void* ptrs[] = {c->d_voids, c->d_u[0], c->d_u[1], c->d_ntype, c->d_cell_class, c->d_dof_lat, c->d_out,
+                  c->d_ft, c->d_step, c->d_flag, c->d_irr_lat, c->d_irr_invm, c->d_irr_fx, c->d_Kref,
+                  c->d_c_lat, c->d_vc, c->d_ac, c->d_fxc, c->d_b, c->d_y, c->d_x, c->d_z, c->d_U,
+                  c->d_celem_cell, c->d_celem_kidx, c->d_celem_cidx, c->d_Kcut, c->d_Y, c->d_rhs_ptr,
+                  c->d_rhs_idx, c->d_sn_c0, c->d_sn_w, c->d_sn_r, c->d_sn_linv, c->d_sn_lr, c->d_sn_roff,
+                  c->d_sn_uoff, c->d_sn_goff, c->d_R, c->d_gptr, c->d_gidx, c->d_items, c->fS.Linv, c->fS.LR,
+                  c->fM.Linv, c->fM.LR, c->d_tmp};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  if (cur >= 0) cudaSetDevice(cur);
+  delete c;
+}
+
+static void validate(const sc_grid* grid, int32_t p, double alpha, const sc_geometry* geom, double dt,
+                     const sc_source* src) {
+  if (!grid || !geom) throw ScError(SC_ERR_CONFIG, "grid and geometry are required");
+  if (grid->dim < 1 || grid->dim > 3) throw ScError(SC_ERR_CONFIG, "dim must be 1, 2 or 3");
+  for (int k = 0; k < grid->dim; ++k) {
+    if (grid->cells[k] < 1) throw ScError(SC_ERR_CONFIG, "cells must be >= 1");
+    if (!(grid->hi[k] > grid->lo[k])) throw ScError(SC_ERR_CONFIG, "hi must exceed lo");
+  }
+  if (p < 1 || p > 8) throw ScError(SC_ERR_CONFIG, "p must be in [1, 8]");
+  if (grid->dim == 3 && p > 6) throw ScError(SC_ERR_CONFIG, "3D supports p <= 6");
+  if (!(alpha > 0.0) || !(alpha <= 1.0)) throw ScError(SC_ERR_CONFIG, "alpha must be in (0, 1]");
+  if (!(dt > 0.0) || !std::isfinite(dt)) throw ScError(SC_ERR_CONFIG, "dt must be positive");
+  if (geom->n_voids < 0 || geom->n_voids > SC_MAX_VOIDS || (geom->n_voids > 0 && !geom->voids))
+    throw ScError(SC_ERR_CONFIG, "invalid void list");
+  if (geom->tree_depth < 0 || geom->tree_depth > 12) throw ScError(SC_ERR_CONFIG, "tree_depth in [0, 12]");
+  if (geom->lattice_s < 1 || geom->lattice_s > 16) throw ScError(SC_ERR_CONFIG, "lattice_s in [1, 16]");
+  if (!(geom->rho > 0.0) || !(geom->c > 0.0)) throw ScError(SC_ERR_CONFIG, "rho and c must be positive");
+  if (src && src->kind == 1 && (src->n_t < 0 || (src->n_t > 0 && !src->f_t)))
+    throw ScError(SC_ERR_CONFIG, "invalid source signal");
+  for (int i = 0; i < geom->n_voids; ++i) {
+    const sc_void& v = geom->voids[i];
+    if (v.kind != SC_VOID_ELLIPSOID && v.kind != SC_VOID_HALFSPACE) throw ScError(SC_ERR_CONFIG, "void kind");
+  }
+}
+
+extern "C" sc_status sc_setup(const sc_grid* grid, int32_t p, double alpha, const sc_geometry* geom, double dt,
+                              const sc_source* src, const double* u0, const double* v0, const sc_dist* dist,
+                              sc_ctx** out) {
+  if (!out) return SC_ERR_STATE;
+  *out = nullptr;
+  sc_ctx* c = nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  try {
+    validate(grid, p, alpha, geom, dt, src);
+    c = new sc_ctx();
+    c->device = dist ? dist->device : -1;
+    if (c->device < 0) SC_CUDA(cudaGetDevice(&c->device));
+    SC_CUDA(cudaSetDevice(c->device));
+    if (dist && dist->world > 1) throw ScError(SC_ERR_CONFIG, "world > 1 is not supported by this build");
+    if (dist && dist->cuda_stream) {
+      c->stream = (cudaStream_t)dist->cuda_stream;
+    } else {
+      SC_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    GridP& g = c->g;
+    g.dim = grid->dim;
+    g.p = p;
+    g.s = geom->lattice_s;
+    g.depth = geom->tree_depth;
+    c->nb = 1;
+    c->n_cells = 1;
+    c->n_lat = 1;
+    for (int k = 0; k < 3; ++k) {
+      if (k < g.dim) {
+        g.N[k] = grid->cells[k];
+        g.lo[k] = grid->lo[k];
+        g.hi[k] = grid->hi[k];
+        g.h[k] = (grid->hi[k] - grid->lo[k]) / grid->cells[k];
+        g.nl[k] = (int64_t)g.N[k] * p + 1;
+        c->nb *= p + 1;
+      } else {
+        g.N[k] = 1;
+        g.lo[k] = 0.0;
+        g.hi[k] = 0.0;
+        g.h[k] = 1.0;
+        g.nl[k] = 1;
+      }
+      c->n_cells *= g.N[k];
+      c->n_lat *= g.nl[k];
+    }
+    if (c->n_lat >= (1LL << 31)) throw ScError(SC_ERR_CONFIG, "lattice larger than 2^31 nodes");
+    c->alpha = alpha;
+    c->rho = geom->rho;
+    c->c = geom->c;
+    c->dt = dt;
+    c->fill_eps = geom->fill_eps;
+    for (int i = 0; i < geom->n_voids; ++i) {
+      DVoid v;
+      std::memset(&v, 0, sizeof(v));
+      const sc_void& s = geom->voids[i];
+      v.kind = s.kind;
+      for (int k = 0; k < 3; ++k) {
+        v.c[k] = s.c[k];
+        v.n[k] = s.n[k];
+      }
+      for (int k = 0; k < 6; ++k) v.A[k] = s.A[k];
+      v.b = s.b;
+      c->voids.push_back(v);
+    }
+    if (src && src->kind == 1) {
+      c->src_kind = 1;
+      for (int k = 0; k < 3; ++k) c->src_x[k] = src->x[k];
+    }
+    host_reference(c);
+    device_upload_reference(c);
+    setup_device_geometry(c);
+    setup_factor(c, {});
+    // state buffers
+    const size_t latb = sizeof(double) * c->n_lat;
+    SC_CUDA(cudaMalloc(&c->d_u[0], latb));
+    SC_CUDA(cudaMalloc(&c->d_u[1], latb));
+    SC_CUDA(cudaMalloc(&c->d_step, sizeof(long long)));
+    SC_CUDA(cudaMalloc(&c->d_flag, sizeof(int)));
+    SC_CUDA(cudaMalloc(&c->d_dof_lat, sizeof(int64_t) * std::max<int64_t>(1, c->n_dof)));
+    SC_CUDA(cudaMemcpy(c->d_dof_lat, c->dof_lat.data(), sizeof(int64_t) * c->n_dof, cudaMemcpyHostToDevice));
+    SC_CUDA(cudaMalloc(&c->d_out, sizeof(double) * std::max<int64_t>(1, c->n_dof)));
+    c->n_t = (src && src->kind == 1) ? src->n_t : 0;
+    SC_CUDA(cudaMalloc(&c->d_ft, sizeof(double) * std::max<int64_t>(1, c->n_t)));
+    if (c->n_t) SC_CUDA(cudaMemcpy(c->d_ft, src->f_t, sizeof(double) * c->n_t, cudaMemcpyHostToDevice));
+    // algorithmic bytes per step
+    {
+      const double nbd = (double)c->nb;
+      double ex = 24.0 * (double)(c->n_d - c->n_irr);  // tensor-d: read u_n, u_{n-1}; write u_{n+1}
+      double b = ex;
+      b += 24.0 * (double)c->n_irr;
+      b += 8.0 * (double)c->n_cut * nbd * nbd;         // dense cut K_e
+      b += 48.0 * (double)c->n_c;                      // c state read/write (u, v, a)
+      b += 8.0 * (double)c->nnz_factor * 2.0;          // two sweeps... forward reads both, backward both
+      c->bytes_explicit = ex;
+      c->bytes_per_step = b;
+    }
+    if (u0 || v0) {
+      double *du = nullptr, *dv = nullptr;
+      const size_t nbytes = sizeof(double) * c->n_dof;
+      if (u0) {
+        SC_CUDA(cudaMalloc(&du, nbytes));
+        SC_CUDA(cudaMemcpy(du, u0, nbytes, cudaMemcpyHostToDevice));
+      }
+      if (v0) {
+        SC_CUDA(cudaMalloc(&dv, nbytes));
+        SC_CUDA(cudaMemcpy(dv, v0, nbytes, cudaMemcpyHostToDevice));
+      }
+      run_startup(c, du, dv);
+      if (du) cudaFree(du);
+      if (dv) cudaFree(dv);
+    } else {
+      run_startup(c, nullptr, nullptr);
+    }
+    build_graphs(c);
+    SC_CUDA(cudaStreamSynchronize(c->stream));
+    c->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *out = c;
+    return SC_OK;
+  } catch (const ScError& e) {
+    g_setup_err = e.msg;
+    free_ctx(c);
+    return e.st;
+  } catch (const std::bad_alloc&) {
+    g_setup_err = "host allocation failed";
+    free_ctx(c);
+    return SC_ERR_OOM;
+  }
+}
+
+extern "C" sc_status sc_set_state(sc_ctx* c, const double* u0, const double* v0) {
+  if (!c) return SC_ERR_STATE;
+  try {
+    SC_CUDA(cudaSetDevice(c->device));
+    double *du = nullptr, *dv = nullptr;
+    const size_t nbytes = sizeof(double) * c->n_dof;
+    if (u0) {
+      SC_CUDA(cudaMalloc(&du, nbytes));
+      SC_CUDA(cudaMemcpyAsync(du, u0, nbytes, cudaMemcpyHostToDevice, c->stream));
+    }
+    if (v0) {
+      SC_CUDA(cudaMalloc(&dv, nbytes));
+      SC_CUDA(cudaMemcpyAsync(dv, v0, nbytes, cudaMemcpyHostToDevice, c->stream));
+    }
+    run_startup(c, du, dv);
+    if (du) cudaFree(du);
+    if (dv) cudaFree(dv);
+    return SC_OK;
+  } catch (const ScError& e) {
+    return fail(c, e);
+  }
+}
+
+extern "C" sc_status sc_step(sc_ctx* c, int64_t n) {
+  if (!c) return SC_ERR_STATE;
+  if (n < 0) {
+    c->err = "n must be >= 0";
+    return SC_ERR_CONFIG;
+  }
+  try {
+    SC_CUDA(cudaSetDevice(c->device));
+    for (int64_t i = 0; i < n; ++i) {
+      SC_CUDA(cudaGraphLaunch(c->graph[c->cur], c->stream));
+      c->cur ^= 1;
+      ++c->host_step;
+    }
+    return SC_OK;
+  } catch (const ScError& e) {
+    return fail(c, e);
+  }
+}
+
+extern "C" sc_status sc_sync(sc_ctx* c) {
+  if (!c) return SC_ERR_STATE;
+  try {
+    SC_CUDA(cudaSetDevice(c->device));
+    int flag = 0;
+    SC_CUDA(cudaMemcpyAsync(&flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    SC_CUDA(cudaStreamSynchronize(c->stream));
+    if (flag) {
+      c->err = "non-finite value in the state (instability)";
+      return SC_ERR_NUMERIC;
+    }
+    return SC_OK;
+  } catch (const ScError& e) {
+    return fail(c, e);
+  }
+}
+
+extern "C" sc_status sc_read(sc_ctx* c, double* u, int64_t len) {
+  if (!c) return SC_ERR_STATE;
+  if (!u || len < c->n_dof) {
+    c->err = "output buffer too small";
+    return SC_ERR_CONFIG;
+  }
+  try {
+    SC_CUDA(cudaSetDevice(c->device));
+    gather_dofs(c, c->d_u[c->cur], c->d_out);
+    SC_CUDA(cudaMemcpyAsync(u, c->d_out, sizeof(double) * c->n_dof, cudaMemcpyDeviceToHost, c->stream));
+    return sc_sync(c);
+  } catch (const ScError& e) {
+    return fail(c, e);
+  }
+}
+
+extern "C" sc_status sc_read_c_state(sc_ctx* c, double* v_c, double* a_c, int64_t len) {
+  if (!c) return SC_ERR_STATE;
+  if (len < c->n_c) {
+    c->err = "output buffer too small";
+    return SC_ERR_CONFIG;
+  }
+  try {
+    SC_CUDA(cudaSetDevice(c->device));
+    std::vector<double> tmp(c->n_c);
+    for (int which = 0; which < 2; ++which) {
+      double* dst = which == 0 ? v_c : a_c;
+      if (!dst || c->n_c == 0) continue;
+      SC_CUDA(cudaMemcpyAsync(tmp.data(), which == 0 ? c->d_vc : c->d_ac, sizeof(double) * c->n_c,
+                              cudaMemcpyDeviceToHost, c->stream));
+      SC_CUDA(cudaStreamSynchronize(c->stream));
+      for (int64_t i = 0; i < c->n_c; ++i) dst[c->c_canon[i]] = tmp[i];
+    }
+    return SC_OK;
+  } catch (const ScError& e) {
+    return fail(c, e);
+  }
+}
+
+extern "C" sc_status sc_query(sc_ctx* c, sc_info* o) {
+  if (!c || !o) return SC_ERR_STATE;
+  std::memset(o, 0, sizeof(*o));
+  o->n_dof = c->n_dof;
+  o->n_d = c->n_d;
+  o->n_c = c->n_c;
+  o->n_irregular = c->n_irr;
+  o->cells_uncut = c->cells_uncut;
+  o->cells_cut = c->cells_cut;
+  o->cells_empty = c->cells_empty;
+  o->n_components = c->n_components;
+  o->n_supernodes = c->n_sn;
+  o->nnz_factor = c->nnz_factor;
+  o->factor_height = c->height;
+  o->dt = c->dt;
+  o->dt_crit_uncut = c->dt_crit_uncut;
+  o->step = c->host_step;
+  o->bytes_per_step = c->bytes_per_step;
+  o->bytes_explicit_per_step = c->bytes_explicit;
+  o->kernels_per_step = c->kernels_per_step;
+  o->lattice_nodes = c->n_lat;
+  o->setup_seconds = c->setup_seconds;
+  return SC_OK;
+}
+
+extern "C" sc_status sc_read_classification(sc_ctx* c, int8_t* cell_class, uint8_t* dof_is_c,
+                                            int64_t* dof_lattice_index) {
+  if (!c) return SC_ERR_STATE;
+  if (cell_class) std::memcpy(cell_class, c->cell_class.data(), c->cell_class.size());
+  for (int64_t i = 0; i < c->n_dof; ++i) {
+    if (dof_is_c) dof_is_c[i] = c->ntype[c->dof_lat[i]] == 3 ? 1 : 0;
+    if (dof_lattice_index) dof_lattice_index[i] = c->dof_lat[i];
+  }
+  return SC_OK;
+}
+
+extern "C" sc_status sc_dof_coords(sc_ctx* c, double* xyz, int64_t len) {
+  if (!c) return SC_ERR_STATE;
+  if (!xyz || len < 3 * c->n_dof) {
+    c->err = "output buffer too small";
+    return SC_ERR_CONFIG;
+  }
+  const GridP& g = c->g;
+  for (int64_t i = 0; i < c->n_dof; ++i) {
+    int64_t lat = c->dof_lat[i];
+    for (int k = 0; k < 3; ++k) {
+      double x = 0.0;
+      if (k < g.dim) {
+        int64_t j = lat % g.nl[k];
+        lat /= g.nl[k];
+        int64_t e = std::min<int64_t>(j / g.p, g.N[k] - 1);
+        int64_t l = j - e * g.p;
+        x = g.lo[k] + g.h[k] * (e + (c->gll_x[l] + 1.0) * 0.5);
+      }
+      xyz[3 * i + k] = x;
+    }
+  }
+  return SC_OK;
+}
+
+extern "C" const char* sc_last_error(const sc_ctx* c) { return c ? c->err.c_str() : g_setup_err.c_str(); }
+
+extern "C" void sc_destroy(sc_ctx* c) { free_ctx(c); }
+
+extern "C" sc_status sc_profile(sc_ctx* c, int32_t which, int64_t n) {
+  if (!c) return SC_ERR_STATE;
+  if (which < 0 || which > 2 || n < 0) {
+    c->err = "sc_profile: which in {0,1,2}, n >= 0";
+    return SC_ERR_CONFIG;
+  }
+  try {
+    SC_CUDA(cudaSetDevice(c->device));
+    for (int64_t i = 0; i < n; ++i) profile_launch(c, which);
+    return SC_OK;
+  } catch (const ScError& e) {
+    return fail(c, e);
+  }
+}

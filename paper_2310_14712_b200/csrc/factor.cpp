@@ -1,0 +1,735 @@
+// Host-side setup of the implicit cut-DOF solve (a5) and of the c-part data structures.
+//
+// PAPER.md P:583 / P:1425 / P:1767: the system matrix S = M^cc + beta dt^2 K^cc
+// (beta = 1/4) is "factorized once outside the time integration loop"; each step
+// performs forward and backward substitution.  B200 design:
+//  * S is block diagonal by connected component of the c-graph (voids are disjoint);
+//  * each component is ordered by geometric nested dissection on the integer lattice
+//    coordinates: planes x_k = m*p (element boundaries) are exact separators of the
+//    element graph;
+//  * every ND tree node is one dense supernode; the numeric factorisation is multifrontal
+//    (dense fronts, partial Cholesky, extend-add);
+//  * for the device solve each supernode stores L_ss^{-1} (so the per-step TRSV becomes a
+//    GEMV) and the panel L_{R_s,s}; both column-major.
+// Also builds: irregular-d list (d DOFs touching an empty cell or carrying the point
+// load), the c-element list (cut cells + uncut cells touching a c DOF) with their local
+// c-index maps, and the CSR that gathers element products into r^c.
+#include <omp.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <numeric>
+
+#include "sc_internal.h"
+
+namespace {
+
+struct SNode {
+  int comp;
+  int c0 = 0, w = 0;
+  std::vector<int> cols;      // ND indices are c0..c0+w-1; cols holds local node ids before numbering
+  std::vector<int> R;         // sorted ND indices > c0+w-1
+  std::vector<int> children;
+  int parent = -1;
+  int height = 0;
+};
+
+struct Builder {
+  sc_ctx* c;
+  int d, p, n1, nb;
+  // c nodes in canonical (lattice) order
+  std::vector<int64_t> clat;                 // canonical c index -> lattice
+  std::vector<int> nd_of_canon;              // canonical -> ND
+  std::vector<int> canon_of_nd;
+  std::vector<int64_t> celem_cell;
+  std::vector<int> celem_kidx;
+  std::vector<int> celem_cidx;               // [e*nb+loc] canonical c index or -1 (converted to ND later)
+  std::vector<int> node_eptr, node_eidx;     // canonical c node -> list of (e*nb+loc)
+  std::vector<SNode> sn;
+  std::vector<int> comp_roots;
+  std::vector<int> comp_of;                  // canonical c -> component
+};
+
+inline void lat_ijk(const GridP& g, int64_t lat, int64_t* ijk) {
+  for (int k = 0; k < 3; ++k) {
+    if (k < g.dim) {
+      ijk[k] = lat % g.nl[k];
+      lat /= g.nl[k];
+    } else {
+      ijk[k] = 0;
+    }
+  }
+}
+
+inline int64_t cell_lin(const GridP& g, const int64_t* ci) {
+  return ci[0] + (int64_t)g.N[0] * (ci[1] + (int64_t)(g.dim > 1 ? g.N[1] : 1) * ci[2]);
+}
+
+// lattice index of local node loc of cell (ci)
+inline int64_t elem_node(const GridP& g, const int64_t* ci, int loc, int n1) {
+  int64_t l[3] = {loc % n1, (loc / n1) % n1, loc / (n1 * n1)};
+  int64_t lat = 0, stride = 1;
+  for (int k = 0; k < g.dim; ++k) {
+    lat += (ci[k] * g.p + l[k]) * stride;
+    stride *= g.nl[k];
+  }
+  return lat;
+}
+
+struct UF {
+  std::vector<int> p;
+  explicit UF(int n) : p(n) { std::iota(p.begin(), p.end(), 0); }
+  int f(int x) {
+    while (p[x] != x) x = p[x] = p[p[x]];
+    return x;
+  }
+  void u(int a, int b) {
+    a = f(a);
+    b = f(b);
+    if (a != b) p[std::max(a, b)] = std::min(a, b);
+  }
+};
+
+// ---------------------------------------------------------------- dense kernels
+// Partial Cholesky of the (n x n, lower, column-major, ld) front on its first w columns,
+// then the Schur update of the trailing (n-w) block.  Returns the failing column or -1.
+int front_factor(double* F, int n, int w) {
+  for (int j = 0; j < w; ++j) {
+    double* Fj = F + (size_t)j * n;
+    for (int k = 0; k < j; ++k) {
+      const double* Fk = F + (size_t)k * n;
+      const double f = Fk[j];
+      if (f == 0.0) continue;
+      for (int i = j; i < n; ++i) Fj[i] -= Fk[i] * f;
+    }
+    if (!(Fj[j] > 0.0) || !std::isfinite(Fj[j])) return j;
+    const double dgn = std::sqrt(Fj[j]);
+    const double inv = 1.0 / dgn;
+    Fj[j] = dgn;
+    for (int i = j + 1; i < n; ++i) Fj[i] *= inv;
+  }
+  // U = F22 - L21 L21^T (lower part), blocked over k for cache reuse
+  const int r = n - w;
+  const int KB = 64;
+  for (int k0 = 0; k0 < w; k0 += KB) {
+    const int k1 = std::min(w, k0 + KB);
+    for (int jj = 0; jj < r; ++jj) {
+      const int j = w + jj;
+      double* Fj = F + (size_t)j * n;
+      for (int k = k0; k < k1; ++k) {
+        const double* Fk = F + (size_t)k * n;
+        const double f = Fk[j];
+        if (f == 0.0) continue;
+        for (int i = j; i < n; ++i) Fj[i] -= Fk[i] * f;
+      }
+    }
+  }
+  return -1;
+}
+
+// inverse of the lower-triangular w x w block L (column-major, ld n) into X (w x w, col-major)
+void tri_inverse(const double* L, int n, int w, double* X) {
+  std::fill(X, X + (size_t)w * w, 0.0);
+  for (int col = 0; col < w; ++col) {
+    double* x = X + (size_t)col * w;
+    x[col] = 1.0 / L[(size_t)col * n + col];
+    // forward substitution for rows > col: x_i = -(sum_{k=col}^{i-1} L_ik x_k) / L_ii
+    for (int k = col; k < w; ++k) {
+      if (k > col) x[k] /= L[(size_t)k * n + k];
+      const double xk = x[k];
+      const double* Lk = L + (size_t)k * n;
+      for (int i = k + 1; i < w; ++i) x[i] -= Lk[i] * xk;
+    }
+    // note: x[k] for k>col accumulated -(sum) then divided above
+  }
+}
+
+}  // namespace
+
+// Nested dissection of one component (local node ids into b.clat, canonical indices).
+static void nested_dissection(Builder& b, int comp, std::vector<int>& nodes, std::vector<int>& roots,
+                              int& next_col, std::vector<int>& order_out) {
+  const GridP& g = b.c->g;
+  const int LEAF = 64;
+  std::function<void(std::vector<int>&, std::vector<int>&)> rec = [&](std::vector<int>& nd,
+                                                                      std::vector<int>& out_roots) {
+    if (nd.empty()) return;
+    int axis = -1;
+    int64_t plane = 0;
+    if ((int)nd.size() > LEAF) {
+      int64_t lo[3] = {INT64_MAX, INT64_MAX, INT64_MAX}, hi[3] = {INT64_MIN, INT64_MIN, INT64_MIN};
+      for (int v : nd) {
+        int64_t ijk[3];
+        lat_ijk(g, b.clat[v], ijk);
+        for (int k = 0; k < g.dim; ++k) {
+          lo[k] = std::min(lo[k], ijk[k]);
+          hi[k] = std::max(hi[k], ijk[k]);
+        }
+      }
+      // axes by decreasing extent; first with an interior element-boundary plane
+      int ax[3] = {0, 1, 2};
+      std::sort(ax, ax + g.dim, [&](int a1, int a2) { return hi[a1] - lo[a1] > hi[a2] - lo[a2]; });
+      for (int t = 0; t < g.dim && axis < 0; ++t) {
+        const int k = ax[t];
+        // median coordinate
+        std::vector<int64_t> cs;
+        cs.reserve(nd.size());
+        for (int v : nd) {
+          int64_t ijk[3];
+          lat_ijk(g, b.clat[v], ijk);
+          cs.push_back(ijk[k]);
+        }
+        std::nth_element(cs.begin(), cs.begin() + cs.size() / 2, cs.end());
+        const int64_t med = cs[cs.size() / 2];
+        int64_t best = -1;
+        int64_t bestd = INT64_MAX;
+        for (int64_t m = (lo[k] / g.p) * g.p; m <= hi[k]; m += g.p) {
+          if (m <= lo[k] || m >= hi[k]) continue;
+          int64_t dd = std::llabs(m - med);
+          if (dd < bestd) {
+            bestd = dd;
+            best = m;
+          }
+        }
+        if (best >= 0) {
+          axis = k;
+          plane = best;
+        }
+      }
+    }
+    if (axis < 0) {
+      SNode s;
+      s.comp = comp;
+      s.cols = nd;
+      std::sort(s.cols.begin(), s.cols.end());
+      s.c0 = next_col;
+      s.w = (int)nd.size();
+      for (int v : s.cols) order_out.push_back(v);
+      next_col += s.w;
+      b.sn.push_back(std::move(s));
+      out_roots.push_back((int)b.sn.size() - 1);
+      return;
+    }
+    std::vector<int> left, right, sep;
+    for (int v : nd) {
+      int64_t ijk[3];
+      lat_ijk(g, b.clat[v], ijk);
+      if (ijk[axis] < plane) left.push_back(v);
+      else if (ijk[axis] > plane) right.push_back(v);
+      else sep.push_back(v);
+    }
+    nd.clear();
+    nd.shrink_to_fit();
+    std::vector<int> sub;
+    rec(left, sub);
+    rec(right, sub);
+    if (sep.empty()) {
+      for (int r : sub) out_roots.push_back(r);
+      return;
+    }
+    SNode s;
+    s.comp = comp;
+    s.cols = sep;
+    std::sort(s.cols.begin(), s.cols.end());
+    s.c0 = next_col;
+    s.w = (int)sep.size();
+    for (int v : s.cols) order_out.push_back(v);
+    next_col += s.w;
+    s.children = sub;
+    b.sn.push_back(std::move(s));
+    const int id = (int)b.sn.size() - 1;
+    for (int ch : sub) b.sn[ch].parent = id;
+    out_roots.push_back(id);
+  };
+  rec(nodes, roots);
+}
+
+void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
+  Builder b;
+  b.c = c;
+  const GridP& g = c->g;
+  b.d = g.dim;
+  b.p = g.p;
+  b.n1 = g.p + 1;
+  b.nb = c->nb;
+  const int nb = c->nb, n1 = b.n1;
+  // ---------------- source, DOF lists, irregular nodes
+  std::vector<std::pair<int64_t, double>> src;  // (lattice, f_x value)
+  if (c->src_kind == 1) {
+    int64_t cand[3][2];
+    int nc[3] = {1, 1, 1};
+    for (int k = 0; k < 3; ++k) {
+      cand[k][0] = 0;
+      if (k >= g.dim) continue;
+      nc[k] = 0;
+      for (int64_t e = 0; e < g.N[k]; ++e) {
+        double lo = host_lattice(g.lo[k], g.hi[k], e, g.N[k]);
+        double hi = host_lattice(g.lo[k], g.hi[k], e + 1, g.N[k]);
+        if (lo <= c->src_x[k] && c->src_x[k] <= hi && nc[k] < 2) cand[k][nc[k]++] = e;
+      }
+      if (nc[k] == 0) throw ScError(SC_ERR_CONFIG, "source point outside the grid");
+    }
+    // lowest linear index first: iterate z, y, x ascending
+    bool found = false;
+    for (int a2 = 0; a2 < nc[2] && !found; ++a2)
+      for (int a1 = 0; a1 < nc[1] && !found; ++a1)
+        for (int a0 = 0; a0 < nc[0] && !found; ++a0) {
+          int64_t ci[3] = {cand[0][a0], cand[1][a1], cand[2][a2]};
+          int64_t cl = cell_lin(g, ci);
+          if (c->cell_class[cl] == 2) continue;
+          found = true;
+          double xs[3] = {c->src_x[0], g.dim > 1 ? c->src_x[1] : 0.0, g.dim > 2 ? c->src_x[2] : 0.0};
+          const double al = host_phys(c->voids, xs) ? 1.0 : c->alpha;
+          double v[3][SC_MAXP1];
+          for (int k = 0; k < 3; ++k) {
+            if (k < g.dim) {
+              double lo = host_lattice(g.lo[k], g.hi[k], ci[k], g.N[k]);
+              double hi = host_lattice(g.lo[k], g.hi[k], ci[k] + 1, g.N[k]);
+              double xi = -1.0 + 2.0 * (xs[k] - lo) / (hi - lo);
+              host_lagrange(c->gll_x, xi, v[k], nullptr);
+            } else {
+              for (int i = 0; i < n1; ++i) v[k][i] = (i == 0) ? 1.0 : 0.0;
+            }
+          }
+          for (int loc = 0; loc < nb; ++loc) {
+            int l0 = loc % n1, l1 = (loc / n1) % n1, l2 = loc / (n1 * n1);
+            double val = al * v[0][l0] * v[1][l1] * v[2][l2];
+            if (val != 0.0) src.push_back({elem_node(g, ci, loc, n1), val});
+          }
+        }
+    if (!found) throw ScError(SC_ERR_CONFIG, "source point lies only in empty cells");
+  }
+  for (auto& sv : src)
+    if (c->ntype[sv.first] == 1) c->ntype[sv.first] = 2;  // point-load d nodes -> irregular path
+  c->dof_lat.clear();
+  c->n_d = c->n_c = c->n_irr = 0;
+  for (int64_t i = 0; i < c->n_lat; ++i) {
+    const uint8_t t = c->ntype[i];
+    if (!t) continue;
+    c->dof_lat.push_back(i);
+    if (t == 3) {
+      b.clat.push_back(i);
+      ++c->n_c;
+    } else {
+      ++c->n_d;
+      if (t == 2) ++c->n_irr;
+    }
+  }
+  c->n_dof = (int64_t)c->dof_lat.size();
+  // irregular d nodes: lattice index, 1/M_i (lumped, non-empty incident cells), f_x
+  {
+    std::vector<int32_t> ilat;
+    std::vector<double> iinv, ifx;
+    std::vector<std::pair<int64_t, double>> srcs = src;
+    std::sort(srcs.begin(), srcs.end());
+    for (int64_t i = 0; i < c->n_lat; ++i) {
+      if (c->ntype[i] != 2) continue;
+      int64_t ijk[3];
+      lat_ijk(g, i, ijk);
+      int64_t e0[3], e1[3];
+      for (int k = 0; k < 3; ++k) {
+        if (k < g.dim) {
+          if (ijk[k] % g.p == 0) {
+            e0[k] = ijk[k] / g.p - 1;
+            e1[k] = ijk[k] / g.p;
+          } else {
+            e0[k] = e1[k] = ijk[k] / g.p;
+          }
+          if (e0[k] < 0) e0[k] = e1[k];
+          if (e1[k] >= g.N[k]) e1[k] = e0[k];
+        } else {
+          e0[k] = e1[k] = 0;
+        }
+      }
+      double m = 0.0;
+      for (int64_t a2 = e0[2]; a2 <= e1[2]; ++a2)
+        for (int64_t a1 = e0[1]; a1 <= e1[1]; ++a1)
+          for (int64_t a0 = e0[0]; a0 <= e1[0]; ++a0) {
+            int64_t ci[3] = {a0, a1, a2};
+            if (c->cell_class[cell_lin(g, ci)] == 2) continue;
+            double mm = c->rho;
+            for (int k = 0; k < g.dim; ++k) mm *= 0.5 * g.h[k] * c->gll_w[ijk[k] - ci[k] * g.p];
+            m += mm;
+          }
+      ilat.push_back((int32_t)i);
+      iinv.push_back(1.0 / m);
+      auto it = std::lower_bound(srcs.begin(), srcs.end(), i,
+                                 [](const std::pair<int64_t, double>& a, int64_t v) { return a.first < v; });
+      ifx.push_back((it != srcs.end() && it->first == i) ? it->second : 0.0);
+    }
+    c->n_irr = (int64_t)ilat.size();
+    if (c->n_irr) {
+      SC_CUDA(cudaMalloc(&c->d_irr_lat, sizeof(int32_t) * c->n_irr));
+      SC_CUDA(cudaMalloc(&c->d_irr_invm, sizeof(double) * c->n_irr));
+      SC_CUDA(cudaMalloc(&c->d_irr_fx, sizeof(double) * c->n_irr));
+      SC_CUDA(cudaMemcpy(c->d_irr_lat, ilat.data(), sizeof(int32_t) * c->n_irr, cudaMemcpyHostToDevice));
+      SC_CUDA(cudaMemcpy(c->d_irr_invm, iinv.data(), sizeof(double) * c->n_irr, cudaMemcpyHostToDevice));
+      SC_CUDA(cudaMemcpy(c->d_irr_fx, ifx.data(), sizeof(double) * c->n_irr, cudaMemcpyHostToDevice));
+    }
+  }
+  SC_CUDA(cudaMemcpy(c->d_ntype, c->ntype.data(), c->n_lat, cudaMemcpyHostToDevice));
+  const int nc = (int)c->n_c;
+  // canonical c index of a lattice node (binary search in clat)
+  auto cidx_of = [&](int64_t lat) -> int {
+    auto it = std::lower_bound(b.clat.begin(), b.clat.end(), lat);
+    return (it != b.clat.end() && *it == lat) ? (int)(it - b.clat.begin()) : -1;
+  };
+  // ---------------- c elements: cut cells + uncut cells with >= 1 c node
+  std::vector<uint8_t> mark;
+  {
+    std::vector<int64_t> cells;
+    for (int64_t lat : b.clat) {
+      int64_t ijk[3];
+      lat_ijk(g, lat, ijk);
+      int64_t e0[3], e1[3];
+      for (int k = 0; k < 3; ++k) {
+        if (k < g.dim) {
+          if (ijk[k] % g.p == 0) {
+            e0[k] = ijk[k] / g.p - 1;
+            e1[k] = ijk[k] / g.p;
+          } else {
+            e0[k] = e1[k] = ijk[k] / g.p;
+          }
+          if (e0[k] < 0) e0[k] = e1[k];
+          if (e1[k] >= g.N[k]) e1[k] = e0[k];
+        } else {
+          e0[k] = e1[k] = 0;
+        }
+      }
+      for (int64_t a2 = e0[2]; a2 <= e1[2]; ++a2)
+        for (int64_t a1 = e0[1]; a1 <= e1[1]; ++a1)
+          for (int64_t a0 = e0[0]; a0 <= e1[0]; ++a0) {
+            int64_t ci[3] = {a0, a1, a2};
+            int64_t cl = cell_lin(g, ci);
+            if (c->cell_class[cl] != 2) cells.push_back(cl);
+          }
+    }
+    std::sort(cells.begin(), cells.end());
+    cells.erase(std::unique(cells.begin(), cells.end()), cells.end());
+    b.celem_cell = cells;
+  }
+  const int ne = (int)b.celem_cell.size();
+  c->n_celem = ne;
+  b.celem_kidx.assign(ne, -1);
+  b.celem_cidx.assign((size_t)ne * nb, -1);
+  for (int e = 0; e < ne; ++e) {
+    const int64_t cl = b.celem_cell[e];
+    if (c->cell_class[cl] == 1) {
+      auto it = std::lower_bound(c->cut_cells.begin(), c->cut_cells.end(), (long long)cl);
+      b.celem_kidx[e] = (int)(it - c->cut_cells.begin());
+    }
+    int64_t ci[3];
+    int64_t t = cl;
+    for (int k = 0; k < 3; ++k) {
+      if (k < g.dim) {
+        ci[k] = t % g.N[k];
+        t /= g.N[k];
+      } else {
+        ci[k] = 0;
+      }
+    }
+    for (int loc = 0; loc < nb; ++loc) b.celem_cidx[(size_t)e * nb + loc] = cidx_of(elem_node(g, ci, loc, n1));
+  }
+  // node -> (e, loc) lists, canonical order
+  b.node_eptr.assign(nc + 1, 0);
+  for (size_t q = 0; q < b.celem_cidx.size(); ++q)
+    if (b.celem_cidx[q] >= 0) ++b.node_eptr[b.celem_cidx[q] + 1];
+  for (int i = 0; i < nc; ++i) b.node_eptr[i + 1] += b.node_eptr[i];
+  b.node_eidx.resize(b.node_eptr[nc]);
+  {
+    std::vector<int> fill(b.node_eptr.begin(), b.node_eptr.end() - 1);
+    for (size_t q = 0; q < b.celem_cidx.size(); ++q)
+      if (b.celem_cidx[q] >= 0) b.node_eidx[fill[b.celem_cidx[q]]++] = (int)q;
+  }
+  // ---------------- components (union-find over c elements)
+  UF uf(std::max(nc, 1));
+  for (int e = 0; e < ne; ++e) {
+    int first = -1;
+    for (int loc = 0; loc < nb; ++loc) {
+      int ci = b.celem_cidx[(size_t)e * nb + loc];
+      if (ci < 0) continue;
+      if (first < 0) first = ci;
+      else uf.u(first, ci);
+    }
+  }
+  std::vector<int> comp_id(nc, -1);
+  std::vector<std::vector<int>> comps;
+  for (int i = 0; i < nc; ++i) {
+    int r = uf.f(i);
+    if (comp_id[r] < 0) {
+      comp_id[r] = (int)comps.size();
+      comps.emplace_back();
+    }
+    comps[comp_id[r]].push_back(i);
+  }
+  c->n_components = (int64_t)comps.size();
+  // ---------------- nested dissection -> ND order and supernodes
+  std::vector<int> order;  // ND index -> canonical
+  order.reserve(nc);
+  int next_col = 0;
+  for (int k = 0; k < (int)comps.size(); ++k) {
+    std::vector<int> roots;
+    nested_dissection(b, k, comps[k], roots, next_col, order);
+  }
+  b.canon_of_nd = order;
+  b.nd_of_canon.assign(nc, -1);
+  for (int i = 0; i < nc; ++i) b.nd_of_canon[order[i]] = i;
+  c->c_lat.resize(nc);
+  c->c_canon.resize(nc);
+  for (int i = 0; i < nc; ++i) {
+    c->c_lat[i] = b.clat[order[i]];
+    c->c_canon[i] = order[i];
+  }
+  // convert element maps to ND indices
+  for (auto& v : b.celem_cidx)
+    if (v >= 0) v = b.nd_of_canon[v];
+  // ---------------- symbolic: R_s = (adj(cols) U struct(children)) above the supernode
+  const int nsn = (int)b.sn.size();
+  std::vector<int> sn_of(nc);
+  for (int s = 0; s < nsn; ++s)
+    for (int j = 0; j < b.sn[s].w; ++j) sn_of[b.sn[s].c0 + j] = s;
+  for (int s = 0; s < nsn; ++s) {  // creation order is a postorder
+    SNode& S = b.sn[s];
+    const int last = S.c0 + S.w - 1;
+    std::vector<int> R;
+    for (int v : S.cols) {  // canonical ids
+      for (int q = b.node_eptr[v]; q < b.node_eptr[v + 1]; ++q) {
+        const int e = b.node_eidx[q] / nb;
+        for (int loc = 0; loc < nb; ++loc) {
+          int j = b.celem_cidx[(size_t)e * nb + loc];
+          if (j > last) R.push_back(j);
+        }
+      }
+    }
+    for (int ch : S.children)
+      for (int j : b.sn[ch].R)
+        if (j > last) R.push_back(j);
+    std::sort(R.begin(), R.end());
+    R.erase(std::unique(R.begin(), R.end()), R.end());
+    S.R = std::move(R);
+    int h = 0;
+    for (int ch : S.children) h = std::max(h, b.sn[ch].height + 1);
+    S.height = h;
+  }
+  // ---------------- numeric multifrontal factorisation of S and M^cc
+  const double beta_dt2 = 0.25 * c->dt * c->dt;
+  std::vector<int64_t> linv_off(nsn + 1, 0), lr_off(nsn + 1, 0);
+  for (int s = 0; s < nsn; ++s) {
+    linv_off[s + 1] = linv_off[s] + (int64_t)b.sn[s].w * b.sn[s].w;
+    lr_off[s + 1] = lr_off[s] + (int64_t)b.sn[s].w * (int64_t)b.sn[s].R.size();
+  }
+  c->nnz_factor = linv_off[nsn] + lr_off[nsn];
+  std::vector<double> hLinvS(linv_off[nsn]), hLRS(lr_off[nsn]), hLinvM(linv_off[nsn]), hLRM(lr_off[nsn]);
+  // supernodes grouped by component, in postorder
+  std::vector<std::vector<int>> comp_sn(comps.size());
+  for (int s = 0; s < nsn; ++s) comp_sn[b.sn[s].comp].push_back(s);
+  int fail_comp = -1, fail_row = -1, fail_which = 0;
+  const double* Kref = c->Kref.data();
+  const double* Mref = c->Mref.data();
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int k = 0; k < (int)comps.size(); ++k) {
+    for (int which = 0; which < 2; ++which) {  // 0: S, 1: M^cc
+      std::vector<std::vector<double>> upd(nsn);  // update matrices (sparse by sn id; only this comp used)
+      for (int s : comp_sn[k]) {
+        const SNode& S = b.sn[s];
+        const int w = S.w, r = (int)S.R.size(), n = w + r;
+        std::vector<double> F((size_t)n * n, 0.0);
+        auto pos = [&](int j) -> int {
+          if (j >= S.c0 && j < S.c0 + w) return j - S.c0;
+          auto it = std::lower_bound(S.R.begin(), S.R.end(), j);
+          return w + (int)(it - S.R.begin());
+        };
+        // original entries of columns C_s
+        for (int jj = 0; jj < w; ++jj) {
+          const int jnd = S.c0 + jj;
+          const int v = b.canon_of_nd[jnd];
+          for (int q = b.node_eptr[v]; q < b.node_eptr[v + 1]; ++q) {
+            const int e = b.node_eidx[q] / nb, lj = b.node_eidx[q] % nb;
+            const int kidx = b.celem_kidx[e];
+            const double* Ke = kidx >= 0 ? &c->Kcut_host[(size_t)kidx * nb * nb] : Kref;
+            const double* Me = kidx >= 0 ? &c->Mcut_host[(size_t)kidx * nb * nb] : nullptr;
+            for (int li = 0; li < nb; ++li) {
+              const int i = b.celem_cidx[(size_t)e * nb + li];
+              if (i < jnd) continue;
+              double m = Me ? Me[(size_t)li * nb + lj] : (li == lj ? Mref[li] : 0.0);
+              double val = which == 0 ? m + beta_dt2 * Ke[(size_t)li * nb + lj] : m;
+              F[(size_t)jj * n + pos(i)] += val;
+            }
+          }
+        }
+        // extend-add of the children's update matrices
+        for (int ch : S.children) {
+          const SNode& C = b.sn[ch];
+          const int rc = (int)C.R.size();
+          std::vector<int> pm(rc);
+          for (int a = 0; a < rc; ++a) pm[a] = pos(C.R[a]);
+          const std::vector<double>& U = upd[ch];
+          for (int bb = 0; bb < rc; ++bb)
+            for (int a = bb; a < rc; ++a) F[(size_t)pm[bb] * n + pm[a]] += U[(size_t)bb * rc + a];
+          upd[ch].clear();
+          upd[ch].shrink_to_fit();
+        }
+        const int bad = front_factor(F.data(), n, w);
+        if (bad >= 0) {
+#pragma omp critical
+          {
+            fail_comp = k;
+            fail_row = S.c0 + bad;
+            fail_which = which;
+          }
+          break;
+        }
+        double* Linv = (which == 0 ? hLinvS.data() : hLinvM.data()) + linv_off[s];
+        double* LR = (which == 0 ? hLRS.data() : hLRM.data()) + lr_off[s];
+        tri_inverse(F.data(), n, w, Linv);
+        for (int j = 0; j < w; ++j)
+          for (int i = 0; i < r; ++i) LR[(size_t)j * r + i] = F[(size_t)j * n + w + i];
+        std::vector<double> U((size_t)r * r);
+        for (int j = 0; j < r; ++j)
+          for (int i = j; i < r; ++i) U[(size_t)j * r + i] = F[(size_t)(w + j) * n + w + i];
+        upd[s] = std::move(U);
+      }
+    }
+  }
+  if (fail_comp >= 0)
+    throw ScError(SC_ERR_NUMERIC, std::string("non-positive pivot in the factorisation of ") +
+                                      (fail_which == 0 ? "S" : "M^cc") + " (component " +
+                                      std::to_string(fail_comp) + ", row " + std::to_string(fail_row) + ")");
+  // ---------------- device structures
+  c->n_sn = nsn;
+  int H = 0;
+  for (auto& S : b.sn) H = std::max(H, S.height);
+  c->height = nsn ? H + 1 : 0;
+  std::vector<int32_t> c0(nsn), wv(nsn), rv(nsn), roff(nsn + 1, 0), uoff(nsn + 1, 0), goff(nsn + 1, 0);
+  std::vector<int64_t> li(nsn), lr(nsn);
+  for (int s = 0; s < nsn; ++s) {
+    c0[s] = b.sn[s].c0;
+    wv[s] = b.sn[s].w;
+    rv[s] = (int)b.sn[s].R.size();
+    li[s] = linv_off[s];
+    lr[s] = lr_off[s];
+    roff[s + 1] = roff[s] + rv[s];
+    uoff[s + 1] = uoff[s] + rv[s];
+    goff[s + 1] = goff[s] + wv[s] + rv[s];
+    if (wv[s] > 4096) throw ScError(SC_ERR_CONFIG, "supernode wider than 4096 columns");
+    c->max_w = std::max(c->max_w, wv[s]);
+  }
+  std::vector<int32_t> Rall(roff[nsn]);
+  for (int s = 0; s < nsn; ++s) std::copy(b.sn[s].R.begin(), b.sn[s].R.end(), Rall.begin() + roff[s]);
+  // front gather lists: position t of supernode s <- update entries of its children
+  std::vector<std::vector<int32_t>> gl((size_t)goff[nsn]);
+  for (int s = 0; s < nsn; ++s) {
+    const SNode& S = b.sn[s];
+    for (int ch : S.children) {
+      const SNode& C = b.sn[ch];
+      for (int a = 0; a < (int)C.R.size(); ++a) {
+        const int j = C.R[a];
+        int pos;
+        if (j >= S.c0 && j < S.c0 + S.w) pos = j - S.c0;
+        else pos = S.w + (int)(std::lower_bound(S.R.begin(), S.R.end(), j) - S.R.begin());
+        gl[goff[s] + pos].push_back(uoff[ch] + a);
+      }
+    }
+  }
+  std::vector<int32_t> gptr(goff[nsn] + 1, 0), gidx;
+  for (int32_t t = 0; t < goff[nsn]; ++t) {
+    gptr[t + 1] = gptr[t] + (int32_t)gl[t].size();
+    gidx.insert(gidx.end(), gl[t].begin(), gl[t].end());
+  }
+  // work items per height: fwdA (rows of Linv, 32 per item), fwdB (rows of L_R, 32 per item),
+  // bwdA (columns, 8 per item), bwdB (outputs, 8 per item)
+  std::vector<int32_t> items;
+  c->levels.assign(c->height, SolveLevel{});
+  for (int h = 0; h < c->height; ++h) {
+    SolveLevel& L = c->levels[h];
+    L.offA = (int)items.size() / 2;
+    for (int s = 0; s < nsn; ++s)
+      if (b.sn[s].height == h)
+        for (int i = 0; i < wv[s]; i += 32) items.insert(items.end(), {s, i});
+    L.nA = (int)items.size() / 2 - L.offA;
+    L.offB = (int)items.size() / 2;
+    for (int s = 0; s < nsn; ++s)
+      if (b.sn[s].height == h)
+        for (int i = 0; i < rv[s]; i += 32) items.insert(items.end(), {s, i});
+    L.nB = (int)items.size() / 2 - L.offB;
+    L.offbA = (int)items.size() / 2;
+    for (int s = 0; s < nsn; ++s)
+      if (b.sn[s].height == h)
+        for (int i = 0; i < wv[s]; i += 8) items.insert(items.end(), {s, i});
+    L.nbA = (int)items.size() / 2 - L.offbA;
+    L.offbB = L.offbA;  // same decomposition (8 columns / outputs per item)
+    L.nbB = L.nbA;
+  }
+  auto up32 = [&](int32_t** dst, const std::vector<int32_t>& v) {
+    SC_CUDA(cudaMalloc(dst, sizeof(int32_t) * std::max<size_t>(1, v.size())));
+    if (!v.empty()) SC_CUDA(cudaMemcpy(*dst, v.data(), sizeof(int32_t) * v.size(), cudaMemcpyHostToDevice));
+  };
+  auto up64 = [&](int64_t** dst, const std::vector<int64_t>& v) {
+    SC_CUDA(cudaMalloc(dst, sizeof(int64_t) * std::max<size_t>(1, v.size())));
+    if (!v.empty()) SC_CUDA(cudaMemcpy(*dst, v.data(), sizeof(int64_t) * v.size(), cudaMemcpyHostToDevice));
+  };
+  auto upd_ = [&](double** dst, const std::vector<double>& v) {
+    SC_CUDA(cudaMalloc(dst, sizeof(double) * std::max<size_t>(1, v.size())));
+    if (!v.empty()) SC_CUDA(cudaMemcpy(*dst, v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice));
+  };
+  up32(&c->d_sn_c0, c0);
+  up32(&c->d_sn_w, wv);
+  up32(&c->d_sn_r, rv);
+  up64(&c->d_sn_linv, li);
+  up64(&c->d_sn_lr, lr);
+  up32(&c->d_sn_roff, roff);
+  up32(&c->d_sn_uoff, uoff);
+  up32(&c->d_sn_goff, goff);
+  up32(&c->d_R, Rall);
+  up32(&c->d_gptr, gptr);
+  up32(&c->d_gidx, gidx);
+  up32(&c->d_items, items);
+  upd_(&c->fS.Linv, hLinvS);
+  upd_(&c->fS.LR, hLRS);
+  upd_(&c->fM.Linv, hLinvM);
+  upd_(&c->fM.LR, hLRM);
+  SC_CUDA(cudaMalloc(&c->d_U, sizeof(double) * std::max<int32_t>(1, uoff[nsn])));
+  // c element tables
+  std::vector<int32_t> cell32(ne), kidx32(ne);
+  for (int e = 0; e < ne; ++e) {
+    cell32[e] = (int32_t)b.celem_cell[e];
+    kidx32[e] = b.celem_kidx[e];
+  }
+  up32(&c->d_celem_cell, cell32);
+  up32(&c->d_celem_kidx, kidx32);
+  up32(&c->d_celem_cidx, b.celem_cidx);
+  // r^c gather CSR in ND order
+  std::vector<int32_t> rptr(nc + 1, 0), ridx;
+  ridx.reserve(b.node_eidx.size());
+  for (int i = 0; i < nc; ++i) {
+    const int v = b.canon_of_nd[i];
+    for (int q = b.node_eptr[v]; q < b.node_eptr[v + 1]; ++q) ridx.push_back(b.node_eidx[q]);
+    rptr[i + 1] = (int32_t)ridx.size();
+  }
+  up32(&c->d_rhs_ptr, rptr);
+  up32(&c->d_rhs_idx, ridx);
+  // c-node lattice indices (ND order), f_x^c
+  std::vector<int32_t> clat32(nc);
+  std::vector<double> fxc(nc, 0.0);
+  for (int i = 0; i < nc; ++i) clat32[i] = (int32_t)c->c_lat[i];
+  for (auto& sv : src) {
+    int ci = cidx_of(sv.first);
+    if (ci >= 0) fxc[b.nd_of_canon[ci]] = sv.second;
+  }
+  up32(&c->d_c_lat, clat32);
+  upd_(&c->d_fxc, fxc);
+  const size_t ncs = std::max(1, nc);
+  SC_CUDA(cudaMalloc(&c->d_vc, sizeof(double) * ncs));
+  SC_CUDA(cudaMalloc(&c->d_ac, sizeof(double) * ncs));
+  SC_CUDA(cudaMalloc(&c->d_b, sizeof(double) * ncs));
+  SC_CUDA(cudaMalloc(&c->d_y, sizeof(double) * ncs));
+  SC_CUDA(cudaMalloc(&c->d_x, sizeof(double) * ncs));
+  SC_CUDA(cudaMalloc(&c->d_z, sizeof(double) * ncs));
+  SC_CUDA(cudaMalloc(&c->d_Y, sizeof(double) * std::max<size_t>(1, (size_t)ne * nb)));
+  c->Kcut_host.clear();
+  c->Kcut_host.shrink_to_fit();
+  c->Mcut_host.clear();
+  c->Mcut_host.shrink_to_fit();
+}

@@ -1,0 +1,513 @@
+// Setup kernels of libsc: cell classification (lattice cut test + spacetree, reading C6),
+// node classification (d / c partition), cut-cell element matrices
+// (spacetree Gauss quadrature with pointwise alpha).
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "geom.cuh"
+#include "sc_internal.h"
+
+#define MAXCAND 24
+
+namespace {
+
+__device__ __forceinline__ void cell_coords(const GridP& g, long long cell, int* ci) {
+  long long t = cell;
+  for (int k = 0; k < 3; ++k) {
+    if (k < g.dim) {
+      ci[k] = (int)(t % g.N[k]);
+      t /= g.N[k];
+    } else {
+      ci[k] = 0;
+    }
+  }
+}
+
+__device__ __forceinline__ void cell_box(const GridP& g, const int* ci, double* blo, double* bhi) {
+  for (int k = 0; k < 3; ++k) {
+    if (k < g.dim) {
+      blo[k] = lat_coord(g.lo[k], g.hi[k], ci[k], g.N[k]);
+      bhi[k] = lat_coord(g.lo[k], g.hi[k], ci[k] + 1, g.N[k]);
+    } else {
+      blo[k] = 0.0;
+      bhi[k] = 0.0;
+    }
+  }
+}
+
+// lattice test of tree node (level l, offsets a) of cell ci: returns 0 all phys, 1 all fict, 2 mixed
+__device__ int node_test(const GridP& g, const DVoid* V, int nv, const int* cand, int nc, const int* ci,
+                         int l, const int* a) {
+  const int s = g.s;
+  bool anyp = false, anyf = false;
+  const int n0 = s + 1, n1 = g.dim > 1 ? s + 1 : 1, n2 = g.dim > 2 ? s + 1 : 1;
+  double xs[3][17];
+  for (int k = 0; k < 3; ++k) {
+    if (k < g.dim) {
+      const long long den = (long long)g.N[k] * s << l;
+      const long long m0 = ((long long)ci[k] * s << l) + (long long)a[k] * s;
+      for (int t = 0; t <= s; ++t) xs[k][t] = lat_coord(g.lo[k], g.hi[k], m0 + t, den);
+    } else {
+      xs[k][0] = 0.0;
+    }
+  }
+  for (int t2 = 0; t2 < n2; ++t2)
+    for (int t1 = 0; t1 < n1; ++t1)
+      for (int t0 = 0; t0 < n0; ++t0) {
+        bool ph = phys_cand(V, nv, cand, nc, xs[0][t0], xs[1][t1], xs[2][t2]);
+        anyp |= ph;
+        anyf |= !ph;
+        if (anyp && anyf) return 2;
+      }
+  return anyp ? 0 : 1;
+}
+
+__global__ void k_root_classify(GridP g, const DVoid* __restrict__ V, int nv, long long n_cells,
+                                uint8_t* __restrict__ root) {
+  long long cell = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (cell >= n_cells) return;
+  int ci[3];
+  cell_coords(g, cell, ci);
+  double blo[3], bhi[3];
+  cell_box(g, ci, blo, bhi);
+  int cand[MAXCAND];
+  int nc = box_candidates(V, nv, blo, bhi, cand, MAXCAND);
+  if (nc == 0) {
+    root[cell] = 0;
+    return;
+  }
+  int a[3] = {0, 0, 0};
+  root[cell] = (uint8_t)node_test(g, V, nv, cand, nc, ci, 0, a);
+}
+
+// One thread per candidate cell (root not all-physical): depth-first spacetree by the
+// lattice rule; leaves stored packed; physical Gauss points counted -> CUT / EMPTY.
+__global__ void k_tree(GridP g, const DVoid* __restrict__ V, int nv, const long long* __restrict__ cells,
+                       int n, int cap, const double* __restrict__ tq, unsigned long long* __restrict__ leaves,
+                       int* __restrict__ nleaves, int8_t* __restrict__ cls, int* __restrict__ err) {
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n) return;
+  long long cell = cells[idx];
+  int ci[3];
+  cell_coords(g, cell, ci);
+  double blo[3], bhi[3];
+  cell_box(g, ci, blo, bhi);
+  int cand[MAXCAND];
+  int nc = box_candidates(V, nv, blo, bhi, cand, MAXCAND);
+  const int d = g.dim, nch = 1 << d;
+  // explicit DFS stack
+  int st_l[64];
+  int st_a[64][3];
+  int sp = 0;
+  st_l[0] = 0;
+  st_a[0][0] = st_a[0][1] = st_a[0][2] = 0;
+  sp = 1;
+  int nl = 0;
+  long long nphys = 0;
+  const int P1 = g.p + 1;
+  const int npk1 = g.dim > 1 ? P1 : 1, npk2 = g.dim > 2 ? P1 : 1;
+  while (sp > 0) {
+    --sp;
+    const int l = st_l[sp];
+    int a[3] = {st_a[sp][0], st_a[sp][1], st_a[sp][2]};
+    int t = node_test(g, V, nv, cand, nc, ci, l, a);
+    if (t == 2 && l < g.depth) {
+      if (sp + nch > 64) {
+        atomicExch(err, 1);
+        return;
+      }
+      for (int o = nch - 1; o >= 0; --o) {
+        st_l[sp] = l + 1;
+        for (int k = 0; k < 3; ++k) st_a[sp][k] = (k < d) ? 2 * a[k] + ((o >> k) & 1) : 0;
+        ++sp;
+      }
+      continue;
+    }
+    if (nl >= cap) {
+      atomicExch(err, 2);
+      return;
+    }
+    leaves[(long long)idx * cap + nl] = ((unsigned long long)l << 48) | ((unsigned long long)a[2] << 32) |
+                                        ((unsigned long long)a[1] << 16) | (unsigned long long)a[0];
+    ++nl;
+    // physical Gauss points of this leaf (pointwise alpha, C6)
+    double lo_[3], span[3];
+    for (int k = 0; k < 3; ++k) {
+      if (k < d) {
+        const long long den = (long long)g.N[k] * g.s << l;
+        const long long m0 = ((long long)ci[k] * g.s << l) + (long long)a[k] * g.s;
+        double xlo = lat_coord(g.lo[k], g.hi[k], m0, den);
+        double xhi = lat_coord(g.lo[k], g.hi[k], m0 + g.s, den);
+        lo_[k] = xlo;
+        span[k] = __dadd_rn(xhi, -xlo);
+      } else {
+        lo_[k] = 0.0;
+        span[k] = 0.0;
+      }
+    }
+    for (int q2 = 0; q2 < npk2; ++q2)
+      for (int q1 = 0; q1 < npk1; ++q1)
+        for (int q0 = 0; q0 < P1; ++q0) {
+          double x0 = __dadd_rn(lo_[0], __dmul_rn(span[0], tq[q0]));
+          double x1 = d > 1 ? __dadd_rn(lo_[1], __dmul_rn(span[1], tq[q1])) : 0.0;
+          double x2 = d > 2 ? __dadd_rn(lo_[2], __dmul_rn(span[2], tq[q2])) : 0.0;
+          nphys += phys_cand(V, nv, cand, nc, x0, x1, x2) ? 1 : 0;
+        }
+  }
+  nleaves[idx] = nl;
+  cls[cell] = nphys > 0 ? 1 : 2;  // CUT : EMPTY
+}
+
+// node types: 0 hole, 1 tensor-d (all incident in-box cells uncut), 2 irregular-d
+// (no cut incident cell, some empty one), 3 c (>= 1 cut incident cell)
+__global__ void k_node_type(GridP g, const int8_t* __restrict__ cls, long long n_lat, uint8_t* __restrict__ nt) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n_lat) return;
+  long long t = i;
+  int e0[3], e1[3];
+  for (int k = 0; k < 3; ++k) {
+    if (k < g.dim) {
+      long long j = t % g.nl[k];
+      t /= g.nl[k];
+      if (j % g.p == 0) {
+        e0[k] = (int)(j / g.p) - 1;
+        e1[k] = (int)(j / g.p);
+      } else {
+        e0[k] = e1[k] = (int)(j / g.p);
+      }
+      if (e0[k] < 0) e0[k] = e1[k];
+      if (e1[k] >= g.N[k]) e1[k] = e0[k];
+    } else {
+      e0[k] = e1[k] = 0;
+    }
+  }
+  bool anycut = false, anyempty = false, anyne = false;
+  for (int c2 = e0[2]; c2 <= e1[2]; ++c2)
+    for (int c1 = e0[1]; c1 <= e1[1]; ++c1)
+      for (int c0 = e0[0]; c0 <= e1[0]; ++c0) {
+        long long ci = c0 + (long long)g.N[0] * (c1 + (long long)(g.dim > 1 ? g.N[1] : 1) * c2);
+        int8_t c = cls[ci];
+        anycut |= (c == 1);
+        anyempty |= (c == 2);
+        anyne |= (c != 2);
+      }
+  nt[i] = !anyne ? 0 : (anycut ? 3 : (anyempty ? 2 : 1));
+}
+
+__device__ double d_lagr(const double* nodes, int n, int i, double xi, double* der) {
+  double val = 1.0, dv = 0.0;
+  for (int j = 0; j < n; ++j) {
+    if (j == i) continue;
+    double inv = 1.0 / (nodes[i] - nodes[j]);
+    double f = (xi - nodes[j]) * inv;
+    dv = dv * f + val * inv;
+    val *= f;
+  }
+  *der = dv;
+  return val;
+}
+
+// Cut-cell element matrices: one CTA per CUT cell; each thread owns a 4x4 tile of both M_e
+// and K_e; quadrature points are staged in chunks of QC points in shared memory.
+#define QC 8
+__global__ void k_cut_matrices(GridP g, const DVoid* __restrict__ V, int nv, const long long* __restrict__ cells,
+                               const int* __restrict__ slot, const unsigned long long* __restrict__ leaves,
+                               const int* __restrict__ nleaves, int cap, const double* __restrict__ gll,
+                               const double* __restrict__ gx, const double* __restrict__ gw,
+                               const double* __restrict__ tq, double alpha, double rho, double c2, int nb,
+                               int nbp, double* __restrict__ Kout, double* __restrict__ Mout) {
+  extern __shared__ double sm[];
+  double* sN = sm;                    // [QC][nbp]
+  double* sG = sN + QC * nbp;         // [3][QC][nbp]
+  double* sphi = sG + 3 * QC * nbp;   // [QC][3][SC_MAXP1]
+  double* sdph = sphi + QC * 3 * SC_MAXP1;
+  double* sw = sdph + QC * 3 * SC_MAXP1;  // [QC] weight incl alpha
+  __shared__ int cand[MAXCAND];
+  __shared__ int s_nc;
+  const int e = blockIdx.x;
+  const long long cell = cells[e];
+  const int sl = slot[e];
+  const int d = g.dim, P1 = g.p + 1;
+  int ci[3];
+  cell_coords(g, cell, ci);
+  if (threadIdx.x == 0) {
+    double blo[3], bhi[3];
+    cell_box(g, ci, blo, bhi);
+    s_nc = box_candidates(V, nv, blo, bhi, cand, MAXCAND);
+  }
+  __syncthreads();
+  const int nc = s_nc;
+  const int T = nbp / 4;
+  const int i0 = (threadIdx.x % T) * 4, j0 = (threadIdx.x / T) * 4;
+  const bool active = threadIdx.x < T * T;
+  double accM[4][4], accK[4][4];
+  for (int a = 0; a < 4; ++a)
+    for (int b = 0; b < 4; ++b) accM[a][b] = accK[a][b] = 0.0;
+  const int npts = (d == 1) ? P1 : (d == 2 ? P1 * P1 : P1 * P1 * P1);
+  const int nl = nleaves[sl];
+  const long long total = (long long)nl * npts;
+  double hk[3] = {g.h[0], g.h[1], g.h[2]};
+  for (long long q0 = 0; q0 < total; q0 += QC) {
+    const int nq = (int)min((long long)QC, total - q0);
+    // per point, per axis: 1D basis values/derivatives; weight with alpha
+    for (int t = threadIdx.x; t < nq * 3; t += blockDim.x) {
+      const int qq = t / 3, k = t % 3;
+      const long long q = q0 + qq;
+      const unsigned long long lf = leaves[(long long)sl * cap + q / npts];
+      const int l = (int)(lf >> 48);
+      const int a = (int)((lf >> (16 * k)) & 0xFFFF);
+      int loc = (int)(q % npts);
+      int gk = (k == 0) ? loc % P1 : (k == 1 ? (loc / P1) % P1 : loc / (P1 * P1));
+      if (k < d) {
+        double xi = -1.0 + (2.0 * a + 1.0 + gx[gk]) * ldexp(1.0, -l);
+        for (int i = 0; i < P1; ++i) {
+          double dd;
+          sphi[(qq * 3 + k) * SC_MAXP1 + i] = d_lagr(gll, P1, i, xi, &dd);
+          sdph[(qq * 3 + k) * SC_MAXP1 + i] = dd * (2.0 / hk[k]);
+        }
+      }
+      if (k == 0) {
+        // alpha at the physical Gauss point (same arithmetic as the classifier)
+        double x[3] = {0.0, 0.0, 0.0};
+        double w = 1.0;
+        int gg[3] = {loc % P1, (loc / P1) % P1, loc / (P1 * P1)};
+        for (int kk = 0; kk < d; ++kk) {
+          const int ak = (int)((lf >> (16 * kk)) & 0xFFFF);
+          const long long den = (long long)g.N[kk] * g.s << l;
+          const long long m0 = ((long long)ci[kk] * g.s << l) + (long long)ak * g.s;
+          double xlo = lat_coord(g.lo[kk], g.hi[kk], m0, den);
+          double xhi = lat_coord(g.lo[kk], g.hi[kk], m0 + g.s, den);
+          x[kk] = __dadd_rn(xlo, __dmul_rn(__dadd_rn(xhi, -xlo), tq[gg[kk]]));
+          w *= gw[gg[kk]] * 0.5 * hk[kk] * ldexp(1.0, -l);
+        }
+        const bool ph = phys_cand(V, nv, cand, nc, x[0], x[1], x[2]);
+        sw[qq] = w * (ph ? 1.0 : alpha);
+      }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < nq * nbp; t += blockDim.x) {
+      const int qq = t / nbp, i = t % nbp;
+      double N = 0.0, G0 = 0.0, G1 = 0.0, G2 = 0.0;
+      if (i < nb) {
+        const int a0 = i % P1, a1 = (i / P1) % P1, a2 = i / (P1 * P1);
+        const double* ph = &sphi[qq * 3 * SC_MAXP1];
+        const double* dp = &sdph[qq * 3 * SC_MAXP1];
+        if (d == 1) {
+          N = ph[a0];
+          G0 = dp[a0];
+        } else if (d == 2) {
+          N = ph[a0] * ph[SC_MAXP1 + a1];
+          G0 = dp[a0] * ph[SC_MAXP1 + a1];
+          G1 = ph[a0] * dp[SC_MAXP1 + a1];
+        } else {
+          const double f0 = ph[a0], f1 = ph[SC_MAXP1 + a1], f2 = ph[2 * SC_MAXP1 + a2];
+          N = f0 * f1 * f2;
+          G0 = dp[a0] * f1 * f2;
+          G1 = f0 * dp[SC_MAXP1 + a1] * f2;
+          G2 = f0 * f1 * dp[2 * SC_MAXP1 + a2];
+        }
+      }
+      sN[qq * nbp + i] = N;
+      sG[(0 * QC + qq) * nbp + i] = G0;
+      sG[(1 * QC + qq) * nbp + i] = G1;
+      sG[(2 * QC + qq) * nbp + i] = G2;
+    }
+    __syncthreads();
+    if (active) {
+      for (int qq = 0; qq < nq; ++qq) {
+        const double w = sw[qq];
+        double ni[4], nj[4];
+        for (int a = 0; a < 4; ++a) {
+          ni[a] = w * sN[qq * nbp + i0 + a];
+          nj[a] = sN[qq * nbp + j0 + a];
+        }
+        for (int a = 0; a < 4; ++a)
+          for (int b = 0; b < 4; ++b) accM[a][b] += ni[a] * nj[b];
+        for (int k = 0; k < d; ++k) {
+          const double* G = &sG[(k * QC + qq) * nbp];
+          for (int a = 0; a < 4; ++a) {
+            ni[a] = w * G[i0 + a];
+            nj[a] = G[j0 + a];
+          }
+          for (int a = 0; a < 4; ++a)
+            for (int b = 0; b < 4; ++b) accK[a][b] += ni[a] * nj[b];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (active) {
+    for (int a = 0; a < 4; ++a)
+      for (int b = 0; b < 4; ++b) {
+        const int i = i0 + a, j = j0 + b;
+        if (i < nb && j < nb) {
+          Kout[(long long)e * nb * nb + (long long)i * nb + j] = rho * c2 * accK[a][b];
+          Mout[(long long)e * nb * nb + (long long)i * nb + j] = rho * accM[a][b];
+        }
+      }
+  }
+}
+
+}  // namespace
+
+static void upload_voids(sc_ctx* c) {
+  for (DVoid& v : c->voids) {
+    for (int k = 0; k < 3; ++k) {
+      v.bblo[k] = -INFINITY;
+      v.bbhi[k] = INFINITY;
+    }
+    if (v.kind != SC_VOID_ELLIPSOID) continue;
+    const int d = c->g.dim;
+    // inverse of the leading d x d block of A: half-extents sqrt((A^-1)_kk)
+    double A[3][3] = {{v.A[0], v.A[3], v.A[4]}, {v.A[3], v.A[1], v.A[5]}, {v.A[4], v.A[5], v.A[2]}};
+    double inv[3] = {0, 0, 0};
+    if (d == 1) {
+      inv[0] = 1.0 / A[0][0];
+    } else if (d == 2) {
+      double det = A[0][0] * A[1][1] - A[0][1] * A[1][0];
+      inv[0] = A[1][1] / det;
+      inv[1] = A[0][0] / det;
+    } else {
+      double c00 = A[1][1] * A[2][2] - A[1][2] * A[2][1];
+      double c11 = A[0][0] * A[2][2] - A[0][2] * A[2][0];
+      double c22 = A[0][0] * A[1][1] - A[0][1] * A[1][0];
+      double det = A[0][0] * c00 - A[0][1] * (A[1][0] * A[2][2] - A[1][2] * A[2][0]) +
+                   A[0][2] * (A[1][0] * A[2][1] - A[1][1] * A[2][0]);
+      inv[0] = c00 / det;
+      inv[1] = c11 / det;
+      inv[2] = c22 / det;
+    }
+    for (int k = 0; k < d; ++k) {
+      if (!(inv[k] > 0.0) || !std::isfinite(inv[k]))
+        throw ScError(SC_ERR_CONFIG, "void quadratic form is not positive definite");
+      double ext = std::sqrt(inv[k]) * (1.0 + 1e-6) + 1e-12;
+      v.bblo[k] = v.c[k] - ext;
+      v.bbhi[k] = v.c[k] + ext;
+    }
+  }
+  if (!c->voids.empty()) {
+    SC_CUDA(cudaMalloc(&c->d_voids, sizeof(DVoid) * c->voids.size()));
+    SC_CUDA(cudaMemcpy(c->d_voids, c->voids.data(), sizeof(DVoid) * c->voids.size(), cudaMemcpyHostToDevice));
+  }
+}
+
+// Classification, DOF partition, cut-cell matrices.  Fills host vectors in c and returns
+// the cut-cell mass matrices (host) for the factorisation.
+void setup_device_geometry(sc_ctx* c) {
+  upload_voids(c);
+  const GridP& g = c->g;
+  const int nv = (int)c->voids.size();
+  const long long n_cells = c->n_cells;
+  uint8_t* d_root = nullptr;
+  SC_CUDA(cudaMalloc(&d_root, n_cells));
+  SC_CUDA(cudaMalloc(&c->d_cell_class, n_cells));
+  k_root_classify<<<(unsigned)((n_cells + 255) / 256), 256, 0, c->stream>>>(g, c->d_voids, nv, n_cells, d_root);
+  SC_CUDA(cudaGetLastError());
+  std::vector<uint8_t> root(n_cells);
+  SC_CUDA(cudaMemcpyAsync(root.data(), d_root, n_cells, cudaMemcpyDeviceToHost, c->stream));
+  SC_CUDA(cudaStreamSynchronize(c->stream));
+  cudaFree(d_root);
+  c->cell_class.assign(n_cells, 0);
+  std::vector<long long> cand;
+  for (long long i = 0; i < n_cells; ++i)
+    if (root[i] != 0) cand.push_back(i);
+  // spacetree of candidate cells
+  int cap = 1;
+  for (int l = 0; l < g.depth; ++l) cap *= (1 << g.dim);
+  if (cap > 4096) throw ScError(SC_ERR_CONFIG, "tree_depth too large (more than 4096 leaves per cell)");
+  const int n_cand = (int)cand.size();
+  long long* d_cand = nullptr;
+  unsigned long long* d_leaves = nullptr;
+  int *d_nleaves = nullptr, *d_err = nullptr;
+  double* d_tq = nullptr;
+  std::vector<double> tq(g.p + 1);
+  for (int i = 0; i <= g.p; ++i) tq[i] = (c->gau_x[i] + 1.0) * 0.5;
+  SC_CUDA(cudaMalloc(&d_tq, sizeof(double) * tq.size()));
+  SC_CUDA(cudaMemcpy(d_tq, tq.data(), sizeof(double) * tq.size(), cudaMemcpyHostToDevice));
+  SC_CUDA(cudaMalloc(&d_err, sizeof(int)));
+  SC_CUDA(cudaMemset(d_err, 0, sizeof(int)));
+  SC_CUDA(cudaMemsetAsync(c->d_cell_class, 0, n_cells, c->stream));
+  if (n_cand > 0) {
+    SC_CUDA(cudaMalloc(&d_cand, sizeof(long long) * n_cand));
+    SC_CUDA(cudaMalloc(&d_leaves, sizeof(unsigned long long) * (size_t)n_cand * cap));
+    SC_CUDA(cudaMalloc(&d_nleaves, sizeof(int) * n_cand));
+    SC_CUDA(cudaMemcpyAsync(d_cand, cand.data(), sizeof(long long) * n_cand, cudaMemcpyHostToDevice, c->stream));
+    k_tree<<<(n_cand + 127) / 128, 128, 0, c->stream>>>(g, c->d_voids, nv, d_cand, n_cand, cap, d_tq, d_leaves,
+                                                          d_nleaves, c->d_cell_class, d_err);
+    SC_CUDA(cudaGetLastError());
+  }
+  int herr = 0;
+  SC_CUDA(cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  SC_CUDA(cudaMemcpyAsync(c->cell_class.data(), c->d_cell_class, n_cells, cudaMemcpyDeviceToHost, c->stream));
+  SC_CUDA(cudaStreamSynchronize(c->stream));
+  if (herr) throw ScError(SC_ERR_CONFIG, "spacetree capacity exceeded");
+  c->cells_uncut = c->cells_cut = c->cells_empty = 0;
+  for (long long i = 0; i < n_cells; ++i) {
+    int8_t k = c->cell_class[i];
+    if (k == 0) ++c->cells_uncut;
+    else if (k == 1) ++c->cells_cut;
+    else ++c->cells_empty;
+  }
+  // node types
+  SC_CUDA(cudaMalloc(&c->d_ntype, c->n_lat));
+  k_node_type<<<(unsigned)((c->n_lat + 255) / 256), 256, 0, c->stream>>>(g, c->d_cell_class, c->n_lat, c->d_ntype);
+  SC_CUDA(cudaGetLastError());
+  c->ntype.resize(c->n_lat);
+  SC_CUDA(cudaMemcpyAsync(c->ntype.data(), c->d_ntype, c->n_lat, cudaMemcpyDeviceToHost, c->stream));
+  SC_CUDA(cudaStreamSynchronize(c->stream));
+  // cut-cell element matrices (cut cells in ascending cell order)
+  std::vector<long long> cutcells;
+  std::vector<int> slots;
+  for (int i = 0; i < n_cand; ++i)
+    if (c->cell_class[cand[i]] == 1) {
+      cutcells.push_back(cand[i]);
+      slots.push_back(i);
+    }
+  c->n_cut = (int64_t)cutcells.size();
+  const int nb = c->nb;
+  if (c->n_cut > 0) {
+    long long* d_cc = nullptr;
+    int* d_slots = nullptr;
+    double *d_gll = nullptr, *d_gx = nullptr, *d_gw = nullptr, *d_M = nullptr;
+    SC_CUDA(cudaMalloc(&d_cc, sizeof(long long) * c->n_cut));
+    SC_CUDA(cudaMalloc(&d_slots, sizeof(int) * c->n_cut));
+    SC_CUDA(cudaMemcpy(d_cc, cutcells.data(), sizeof(long long) * c->n_cut, cudaMemcpyHostToDevice));
+    SC_CUDA(cudaMemcpy(d_slots, slots.data(), sizeof(int) * c->n_cut, cudaMemcpyHostToDevice));
+    SC_CUDA(cudaMalloc(&d_gll, sizeof(double) * (g.p + 1)));
+    SC_CUDA(cudaMalloc(&d_gx, sizeof(double) * (g.p + 1)));
+    SC_CUDA(cudaMalloc(&d_gw, sizeof(double) * (g.p + 1)));
+    SC_CUDA(cudaMemcpy(d_gll, c->gll_x.data(), sizeof(double) * (g.p + 1), cudaMemcpyHostToDevice));
+    SC_CUDA(cudaMemcpy(d_gx, c->gau_x.data(), sizeof(double) * (g.p + 1), cudaMemcpyHostToDevice));
+    SC_CUDA(cudaMemcpy(d_gw, c->gau_w.data(), sizeof(double) * (g.p + 1), cudaMemcpyHostToDevice));
+    const size_t mat = (size_t)c->n_cut * nb * nb;
+    SC_CUDA(cudaMalloc(&c->d_Kcut, sizeof(double) * mat));
+    SC_CUDA(cudaMalloc(&d_M, sizeof(double) * mat));
+    const int nbp = ((nb + 15) / 16) * 16;
+    if (nbp > 128) throw ScError(SC_ERR_CONFIG, "(p+1)^dim > 128 not supported by the cut-cell kernel");
+    const int threads = std::max(32, (nbp / 4) * (nbp / 4));
+    const size_t smem = sizeof(double) * (4 * QC * nbp + 2 * QC * 3 * SC_MAXP1 + QC);
+    SC_CUDA(cudaFuncSetAttribute(k_cut_matrices, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_cut_matrices<<<(unsigned)c->n_cut, threads, smem, c->stream>>>(
+        g, c->d_voids, nv, d_cc, d_slots, d_leaves, d_nleaves, cap, d_gll, d_gx, d_gw, d_tq, c->alpha, c->rho,
+        c->c * c->c, nb, nbp, c->d_Kcut, d_M);
+    SC_CUDA(cudaGetLastError());
+    c->Kcut_host.resize(mat);
+    c->Mcut_host.resize(mat);
+    SC_CUDA(cudaMemcpyAsync(c->Kcut_host.data(), c->d_Kcut, sizeof(double) * mat, cudaMemcpyDeviceToHost, c->stream));
+    SC_CUDA(cudaMemcpyAsync(c->Mcut_host.data(), d_M, sizeof(double) * mat, cudaMemcpyDeviceToHost, c->stream));
+    SC_CUDA(cudaStreamSynchronize(c->stream));
+    cudaFree(d_cc);
+    cudaFree(d_slots);
+    cudaFree(d_gll);
+    cudaFree(d_gx);
+    cudaFree(d_gw);
+    cudaFree(d_M);
+  }
+  c->cut_cells = cutcells;
+  if (d_cand) cudaFree(d_cand);
+  if (d_leaves) cudaFree(d_leaves);
+  if (d_nleaves) cudaFree(d_nleaves);
+  cudaFree(d_tq);
+  cudaFree(d_err);
+}

@@ -1,0 +1,725 @@
+// Per-step kernels of libsc: one Newmark IMEX step:
+//  (a1)+(a2)  k_explicit_{1,2,3}d : r^d = -K^d u_n on the all-uncut lattice (tensor form,
+//             assembled 1D operators, sum factorised) fused with the CDM sum step
+//             u^d_{n+1} = 2u^d_n - u^d_{n-1} + dt^2 r^d / M^dd
+//  (a1)+(a2)  k_irregular : the same for d DOFs touching an empty cell or carrying f_x
+//  (a3)+(a4)  k_celem     : predictor u~^c fused into the element products K_e w_e of the
+//             c elements (dense cut K_e, reference uncut K_e);  k_crhs gathers
+//             r^c = f_t(t_{n+1}) f_x^c - (K w)_c
+//  (a5)       k_fwdA/k_fwdB/k_bwdA/k_bwdB : supernodal triangular solves with L_ss^{-1}
+//  (a6)       k_corrector
+// Buffers: d_u[cur] = u_n (lattice, holes = 0), d_u[cur^1] = u_{n-1} on d nodes; the step
+// writes u_{n+1} into d_u[cur^1] (d nodes by (a2), c nodes by (a6)) and flips cur.
+#include <algorithm>
+#include <cmath>
+
+#include "sc_internal.h"
+
+__constant__ double c_Mh[SC_MAXP1 * SC_MAXP1];
+__constant__ double c_Kh[SC_MAXP1 * SC_MAXP1];
+__constant__ double c_w[SC_MAXP1];
+
+struct ExpP {
+  int nl[3];
+  int N[3];
+  double s[3];      // (2/h_k)^2
+  double a1, a2, coefR;  // out = a1 u + a2 P - coefR * r' / prod(wt)
+};
+
+namespace {
+
+__device__ __forceinline__ double wt(int i, int e_cnt, int P) {
+  // assembled 1D GLL weight of lattice node i (N elements of order P)
+  const int l = i % P, e = i / P;
+  if (l) return c_w[l];
+  return (e > 0 ? c_w[P] : 0.0) + (e < e_cnt ? c_w[0] : 0.0);
+}
+
+// assembled 1D operator A (c_Mh or c_Kh) applied at node gi; v(k) returns the value at
+// global index k.  Sums over the (1 or 2) incident elements inside [0, Ne).
+template <int P, typename F>
+__device__ __forceinline__ double op1d(const double* A, int gi, int Ne, F v) {
+  const int e = gi / P, l = gi - e * P;
+  double s = 0.0;
+  if (l) {
+#pragma unroll
+    for (int k = 0; k <= P; ++k) s += A[l * (P + 1) + k] * v(e * P + k);
+    return s;
+  }
+  if (e > 0) {
+#pragma unroll
+    for (int k = 0; k <= P; ++k) s += A[P * (P + 1) + k] * v((e - 1) * P + k);
+  }
+  if (e < Ne) {
+#pragma unroll
+    for (int k = 0; k <= P; ++k) s += A[k] * v(e * P + k);
+  }
+  return s;
+}
+
+// ------------------------------------------------------------------ 1D
+template <int P>
+__global__ void k_explicit_1d(const double* __restrict__ U, const double* Pv, double* out,
+                              const uint8_t* __restrict__ nt, ExpP e, int* flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= e.nl[0] || nt[i] != 1) return;
+  const double r = e.s[0] * op1d<P>(c_Kh, i, e.N[0], [&](int k) { return U[k]; });
+  const double u = U[i];
+  const double res = e.a1 * u + e.a2 * Pv[i] - e.coefR * r / wt(i, e.N[0], P);
+  out[i] = res;
+  if (!isfinite(res)) atomicExch(flag, 1);
+}
+
+// ------------------------------------------------------------------ 2D
+template <int P, int EX, int EY>
+__global__ void __launch_bounds__(256) k_explicit_2d(const double* __restrict__ U, const double* Pv,
+                                                     double* out, const uint8_t* __restrict__ nt, ExpP e,
+                                                     int* flag) {
+  constexpr int RX = EX * P + P + 1, RY = EY * P + P + 1, TY = EY * P + 1;
+  __shared__ double su[RY][RX];
+  __shared__ double sm[TY][RX];
+  __shared__ double sk[TY][RX];
+  const int nx = e.nl[0], ny = e.nl[1];
+  const int x0 = blockIdx.x * EX * P, y0 = blockIdx.y * EY * P;
+  const int x1 = (x0 + EX * P >= nx - 1) ? nx : x0 + EX * P;
+  const int y1 = (y0 + EY * P >= ny - 1) ? ny : y0 + EY * P;
+  const int xr0 = x0 - P, yr0 = y0 - P;
+  const int RXn = min(x1, nx - 1) - xr0 + 1, RYn = min(y1, ny - 1) - yr0 + 1;
+  for (int t = threadIdx.x; t < RXn * RYn; t += blockDim.x) {
+    const int ix = t % RXn, iy = t / RXn;
+    const int gx = xr0 + ix, gy = yr0 + iy;
+    su[iy][ix] = (gx >= 0 && gy >= 0) ? U[gx + (size_t)nx * gy] : 0.0;
+  }
+  __syncthreads();
+  const int OY = y1 - y0, OX = x1 - x0;
+  for (int t = threadIdx.x; t < OY * RXn; t += blockDim.x) {
+    const int ix = t % RXn, oy = t / RXn;
+    const int gy = y0 + oy;
+    auto col = [&](int k) { return su[k - yr0][ix]; };
+    sm[oy][ix] = op1d<P>(c_Mh, gy, e.N[1], col);
+    sk[oy][ix] = op1d<P>(c_Kh, gy, e.N[1], col);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < OY * OX; t += blockDim.x) {
+    const int ox = t % OX, oy = t / OX;
+    const int gx = x0 + ox, gy = y0 + oy;
+    const size_t g = gx + (size_t)nx * gy;
+    if (nt[g] != 1) continue;
+    const double r = e.s[0] * op1d<P>(c_Kh, gx, e.N[0], [&](int k) { return sm[oy][k - xr0]; }) +
+                     e.s[1] * op1d<P>(c_Mh, gx, e.N[0], [&](int k) { return sk[oy][k - xr0]; });
+    const double u = su[gy - yr0][gx - xr0];
+    const double res = e.a1 * u + e.a2 * Pv[g] - e.coefR * r / (wt(gx, e.N[0], P) * wt(gy, e.N[1], P));
+    out[g] = res;
+    if (!isfinite(res)) atomicExch(flag, 1);
+  }
+}
+
+// ------------------------------------------------------------------ 3D
+// xy tile of EX x EY elements, streaming along z over EZ element layers (plus one warm-up
+// layer below).  z contraction per column in registers; y and x contractions per plane in
+// shared memory.
+template <int P, int EX, int EY, int EZ>
+__global__ void __launch_bounds__(256) k_explicit_3d(const double* __restrict__ U, const double* Pv, double* out,
+                                                     const uint8_t* __restrict__ nt, ExpP e, int* flag) {
+  constexpr int RX = EX * P + P + 1, RY = EY * P + P + 1, TY = EY * P + 1;
+  constexpr int NCOL = (RX * RY + 255) / 256;
+  extern __shared__ double smem[];
+  double* sa = smem;                          // [P+1][RY][RX]
+  double* sb = sa + (P + 1) * RY * RX;        // [P+1][RY][RX]
+  double* sm = sb + (P + 1) * RY * RX;        // [P+1][TY][RX]
+  double* st = sm + (P + 1) * TY * RX;        // [P+1][TY][RX]
+  const int nx = e.nl[0], ny = e.nl[1];
+  const size_t pl = (size_t)nx * ny;
+  const int x0 = blockIdx.x * EX * P, y0 = blockIdx.y * EY * P;
+  const int x1 = (x0 + EX * P >= nx - 1) ? nx : x0 + EX * P;
+  const int y1 = (y0 + EY * P >= ny - 1) ? ny : y0 + EY * P;
+  const int xr0 = x0 - P, yr0 = y0 - P;
+  const int RXn = min(x1, nx - 1) - xr0 + 1, RYn = min(y1, ny - 1) - yr0 + 1;
+  const int OX = x1 - x0, OY = y1 - y0;
+  const int Nz = e.N[2];
+  const int ez0 = blockIdx.z * EZ, ez1 = min(ez0 + EZ, Nz);
+  double carry_a[NCOL], carry_b[NCOL];
+#pragma unroll
+  for (int c = 0; c < NCOL; ++c) carry_a[c] = carry_b[c] = 0.0;
+  for (int ez = max(ez0 - 1, 0); ez < ez1; ++ez) {
+    const bool warm = ez < ez0;
+    const bool top = (ez == Nz - 1);
+#pragma unroll
+    for (int c = 0; c < NCOL; ++c) {
+      const int col = threadIdx.x + c * 256;
+      if (col >= RXn * RYn) continue;
+      const int ix = col % RXn, iy = col / RXn;
+      const int gx = xr0 + ix, gy = yr0 + iy;
+      double u[P + 1];
+      if (gx >= 0 && gy >= 0) {
+        const double* base = U + gx + (size_t)nx * gy + pl * (size_t)(ez * P);
+#pragma unroll
+        for (int k = 0; k <= P; ++k) u[k] = base[pl * k];
+      } else {
+#pragma unroll
+        for (int k = 0; k <= P; ++k) u[k] = 0.0;
+      }
+      double aa[P + 1], bb[P + 1];
+#pragma unroll
+      for (int k = 0; k <= P; ++k) {
+        double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+        for (int m = 0; m <= P; ++m) {
+          s1 += c_Mh[k * (P + 1) + m] * u[m];
+          s2 += c_Kh[k * (P + 1) + m] * u[m];
+        }
+        aa[k] = s1;
+        bb[k] = s2;
+      }
+      if (!warm) {
+        const int o = iy * RX + ix;
+        sa[o] = aa[0] + carry_a[c];
+        sb[o] = bb[0] + carry_b[c];
+#pragma unroll
+        for (int k = 1; k < P; ++k) {
+          sa[k * RY * RX + o] = aa[k];
+          sb[k * RY * RX + o] = bb[k];
+        }
+        if (top) {
+          sa[P * RY * RX + o] = aa[P];
+          sb[P * RY * RX + o] = bb[P];
+        }
+      }
+      carry_a[c] = aa[P];
+      carry_b[c] = bb[P];
+    }
+    if (warm) continue;
+    __syncthreads();
+    const int np = top ? P + 1 : P;
+    // y pass: sm = M_y sa ; st = s1 K_y sa + s2 M_y sb
+    for (int t = threadIdx.x; t < np * OY * RXn; t += blockDim.x) {
+      const int ix = t % RXn;
+      const int rest = t / RXn;
+      const int oy = rest % OY, k = rest / OY;
+      const int gy = y0 + oy;
+      const double* A = sa + k * RY * RX + ix;
+      const double* B = sb + k * RY * RX + ix;
+      auto fa = [&](int j) { return A[(j - yr0) * RX]; };
+      auto fb = [&](int j) { return B[(j - yr0) * RX]; };
+      sm[(k * TY + oy) * RX + ix] = op1d<P>(c_Mh, gy, e.N[1], fa);
+      st[(k * TY + oy) * RX + ix] = e.s[1] * op1d<P>(c_Kh, gy, e.N[1], fa) + e.s[2] * op1d<P>(c_Mh, gy, e.N[1], fb);
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < np * OY * OX; t += blockDim.x) {
+      const int ox = t % OX;
+      const int rest = t / OX;
+      const int oy = rest % OY, k = rest / OY;
+      const int gx = x0 + ox, gy = y0 + oy, gz = ez * P + k;
+      const size_t g = gx + (size_t)nx * gy + pl * gz;
+      if (nt[g] != 1) continue;
+      const double* M = sm + (k * TY + oy) * RX;
+      const double* T = st + (k * TY + oy) * RX;
+      const double r = e.s[0] * op1d<P>(c_Kh, gx, e.N[0], [&](int j) { return M[j - xr0]; }) +
+                       op1d<P>(c_Mh, gx, e.N[0], [&](int j) { return T[j - xr0]; });
+      const double u = U[g];
+      const double res = e.a1 * u + e.a2 * Pv[g] -
+                         e.coefR * r / (wt(gx, e.N[0], P) * wt(gy, e.N[1], P) * wt(gz, Nz, P));
+      out[g] = res;
+      if (!isfinite(res)) atomicExch(flag, 1);
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ irregular d nodes
+__device__ __forceinline__ double ft_at(const double* ft, long long nt_, const long long* step, int off) {
+  const long long n = *step + off;
+  return (n >= 0 && n < nt_) ? ft[n] : 0.0;
+}
+
+__global__ void k_irregular(const double* __restrict__ U, const double* Pv, double* out, const int32_t* __restrict__ lat,
+                            const double* __restrict__ invm, const double* __restrict__ fx, int n,
+                            const int8_t* __restrict__ cls, const double* __restrict__ Kref, GridP g,
+                            const double* __restrict__ ft, long long n_t, const long long* step, double a1,
+                            double a2, double a3, int* flag) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const long long L = lat[t];
+  const int P = g.p, n1 = P + 1;
+  int nb = n1;
+  if (g.dim > 1) nb *= n1;
+  if (g.dim > 2) nb *= n1;
+  long long ijk[3];
+  long long rem = L;
+  int e0[3], e1[3];
+  for (int k = 0; k < 3; ++k) {
+    if (k < g.dim) {
+      ijk[k] = rem % g.nl[k];
+      rem /= g.nl[k];
+      if (ijk[k] % P == 0) {
+        e0[k] = (int)(ijk[k] / P) - 1;
+        e1[k] = (int)(ijk[k] / P);
+      } else {
+        e0[k] = e1[k] = (int)(ijk[k] / P);
+      }
+      if (e0[k] < 0) e0[k] = e1[k];
+      if (e1[k] >= g.N[k]) e1[k] = e0[k];
+    } else {
+      ijk[k] = 0;
+      e0[k] = e1[k] = 0;
+    }
+  }
+  double Ku = 0.0;
+  for (int c2 = e0[2]; c2 <= e1[2]; ++c2)
+    for (int c1 = e0[1]; c1 <= e1[1]; ++c1)
+      for (int c0 = e0[0]; c0 <= e1[0]; ++c0) {
+        const long long ci = c0 + (long long)g.N[0] * (c1 + (long long)(g.dim > 1 ? g.N[1] : 1) * c2);
+        if (cls[ci] == 2) continue;
+        const int cc[3] = {c0, c1, c2};
+        int li = 0, mul = 1;
+        for (int k = 0; k < g.dim; ++k) {
+          li += (int)(ijk[k] - (long long)cc[k] * P) * mul;
+          mul *= n1;
+        }
+        for (int loc = 0; loc < nb; ++loc) {
+          const int l0 = loc % n1, l1 = (loc / n1) % n1, l2 = loc / (n1 * n1);
+          long long gl = (long long)c0 * P + l0;
+          if (g.dim > 1) gl += g.nl[0] * ((long long)c1 * P + l1);
+          if (g.dim > 2) gl += g.nl[0] * g.nl[1] * ((long long)c2 * P + l2);
+          Ku += Kref[(size_t)li * nb + loc] * U[gl];
+        }
+      }
+  const double r = ft_at(ft, n_t, step, 0) * fx[t] - Ku;
+  const double res = a1 * U[L] + a2 * Pv[L] + a3 * r * invm[t];
+  out[L] = res;
+  if (!isfinite(res)) atomicExch(flag, 1);
+}
+
+// ------------------------------------------------------------------ c elements
+// mode 0 (step): w = predictor u~^c on c nodes, u^d_{n+1} (buffer B) elsewhere;
+// mode 1 (start): w = A everywhere.   Y[e][i] = sum_j K_e[i][j] w_j (K_e symmetric).
+__global__ void k_celem(int mode, const double* __restrict__ A, const double* __restrict__ B,
+                        const double* __restrict__ vc, const double* __restrict__ ac, double dt,
+                        const int32_t* __restrict__ ecell, const int32_t* __restrict__ ekidx,
+                        const int32_t* __restrict__ ecidx, const double* __restrict__ Kcut,
+                        const double* __restrict__ Kref, double* __restrict__ Y, int ne, int nb, int tpe, GridP g) {
+  extern __shared__ double sw[];
+  const int epb = blockDim.x / tpe;
+  const int le = threadIdx.x / tpe, i = threadIdx.x % tpe;
+  const int e = blockIdx.x * epb + le;
+  const bool ok = e < ne;
+  const int n1 = g.p + 1;
+  double* w = sw + le * nb;
+  if (ok) {
+    const long long cell = ecell[e];
+    long long ci[3];
+    long long rem = cell;
+    for (int k = 0; k < 3; ++k) {
+      if (k < g.dim) {
+        ci[k] = rem % g.N[k];
+        rem /= g.N[k];
+      } else {
+        ci[k] = 0;
+      }
+    }
+    for (int j = i; j < nb; j += tpe) {
+      const int l0 = j % n1, l1 = (j / n1) % n1, l2 = j / (n1 * n1);
+      long long gl = ci[0] * g.p + l0;
+      if (g.dim > 1) gl += g.nl[0] * (ci[1] * g.p + l1);
+      if (g.dim > 2) gl += g.nl[0] * g.nl[1] * (ci[2] * g.p + l2);
+      double v;
+      if (mode == 1) {
+        v = A[gl];
+      } else {
+        const int cc = ecidx[(size_t)e * nb + j];
+        v = cc >= 0 ? A[gl] + dt * vc[cc] + 0.25 * dt * dt * ac[cc] : B[gl];
+      }
+      w[j] = v;
+    }
+  }
+  __syncthreads();
+  if (!ok) return;
+  const int kidx = ekidx[e];
+  const double* K = kidx >= 0 ? Kcut + (size_t)kidx * nb * nb : Kref;
+  for (int r = i; r < nb; r += tpe) {
+    double s = 0.0;
+    for (int j = 0; j < nb; ++j) s += K[(size_t)j * nb + r] * w[j];
+    Y[(size_t)e * nb + r] = s;
+  }
+}
+
+__global__ void k_crhs(double* __restrict__ b, const double* __restrict__ fxc, const int32_t* __restrict__ ptr,
+                       const int32_t* __restrict__ idx, const double* __restrict__ Y, int nc,
+                       const double* __restrict__ ft, long long n_t, const long long* step, int off) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nc) return;
+  double s = 0.0;
+  for (int q = ptr[i]; q < ptr[i + 1]; ++q) s += Y[idx[q]];
+  b[i] = ft_at(ft, n_t, step, off) * fxc[i] - s;
+}
+
+// ------------------------------------------------------------------ supernodal solves
+struct SolveArgs {
+  const int32_t *items, *c0, *w, *r, *roff, *uoff, *goff, *R, *gptr, *gidx;
+  const int64_t *linv_off, *lr_off;
+  const double *Linv, *LR;
+  double *U, *b, *y, *x, *z;
+};
+
+// y_s = L_ss^{-1} (b_s - gathered child updates); rows (32 per item) x warps over columns
+__global__ void __launch_bounds__(256) k_fwdA(SolveArgs a, int off) {
+  extern __shared__ double F[];
+  __shared__ double part[8][33];
+  const int s = a.items[2 * (off + blockIdx.x)], i0 = a.items[2 * (off + blockIdx.x) + 1];
+  const int w = a.w[s], c0 = a.c0[s], go = a.goff[s];
+  for (int t = threadIdx.x; t < w; t += blockDim.x) {
+    double f = a.b[c0 + t];
+    for (int q = a.gptr[go + t]; q < a.gptr[go + t + 1]; ++q) f -= a.U[a.gidx[q]];
+    F[t] = f;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i = i0 + lane;
+  const int jmax = min(w, i0 + 32);
+  const double* L = a.Linv + a.linv_off[s];
+  double acc = 0.0;
+  if (i < w) {
+    for (int j = warp; j < jmax; j += 8) acc += L[i + (size_t)j * w] * F[j];
+  }
+  part[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && i < w) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += part[k][lane];
+    a.y[c0 + i] = t;
+  }
+}
+
+// U_s = gathered child updates (rows R_s) + L_{R_s,s} y_s
+__global__ void __launch_bounds__(256) k_fwdB(SolveArgs a, int off) {
+  extern __shared__ double ys[];
+  __shared__ double part[8][33];
+  const int s = a.items[2 * (off + blockIdx.x)], i0 = a.items[2 * (off + blockIdx.x) + 1];
+  const int w = a.w[s], r = a.r[s], c0 = a.c0[s], go = a.goff[s];
+  for (int t = threadIdx.x; t < w; t += blockDim.x) ys[t] = a.y[c0 + t];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i = i0 + lane;
+  const double* L = a.LR + a.lr_off[s];
+  double acc = 0.0;
+  if (i < r) {
+    for (int j = warp; j < w; j += 8) acc += L[i + (size_t)j * r] * ys[j];
+  }
+  part[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && i < r) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += part[k][lane];
+    for (int q = a.gptr[go + w + i]; q < a.gptr[go + w + i + 1]; ++q) t += a.U[a.gidx[q]];
+    a.U[a.uoff[s] + i] = t;
+  }
+}
+
+// z_j = y_j - sum_i L_R[i,j] x[R_i]   (warp per column j)
+__global__ void __launch_bounds__(256) k_bwdA(SolveArgs a, int off) {
+  const int s = a.items[2 * (off + blockIdx.x)], j0 = a.items[2 * (off + blockIdx.x) + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int w = a.w[s], r = a.r[s], c0 = a.c0[s];
+  const int j = j0 + warp;
+  if (j >= w) return;
+  const double* L = a.LR + a.lr_off[s] + (size_t)j * r;
+  const int32_t* R = a.R + a.roff[s];
+  double acc = 0.0;
+  for (int i = lane; i < r; i += 32) acc += L[i] * a.x[R[i]];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) a.z[c0 + j] = a.y[c0 + j] - acc;
+}
+
+// x_i = sum_{j>=i} Linv[j,i] z_j   (warp per output i; column i of Linv is contiguous)
+__global__ void __launch_bounds__(256) k_bwdB(SolveArgs a, int off) {
+  const int s = a.items[2 * (off + blockIdx.x)], i0 = a.items[2 * (off + blockIdx.x) + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int w = a.w[s], c0 = a.c0[s];
+  const int i = i0 + warp;
+  if (i >= w) return;
+  const double* L = a.Linv + a.linv_off[s] + (size_t)i * w;
+  double acc = 0.0;
+  for (int j = i + lane; j < w; j += 32) acc += L[j] * a.z[c0 + j];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) a.x[c0 + i] = acc;
+}
+
+// ------------------------------------------------------------------ corrector / misc
+__global__ void k_corrector(const double* __restrict__ A, double* __restrict__ B, double* __restrict__ vc,
+                            double* __restrict__ ac, const double* __restrict__ x, const int32_t* __restrict__ clat,
+                            int nc, double dt, int* flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nc) return;
+  const int32_t L = clat[i];
+  const double v = vc[i], a = ac[i];
+  const double ut = A[L] + dt * v + 0.25 * dt * dt * a;   // (a3) predictor
+  const double vt = v + 0.5 * dt * a;
+  const double an = x[i];                                  // (a5) result
+  const double un = ut + 0.25 * dt * dt * an;              // (a6) corrector
+  B[L] = un;
+  vc[i] = vt + 0.5 * dt * an;
+  ac[i] = an;
+  if (!isfinite(un)) atomicExch(flag, 1);
+}
+
+__global__ void k_start_c(double* __restrict__ ac, double* __restrict__ vc, const double* __restrict__ x,
+                          const double* __restrict__ vlat, const int32_t* __restrict__ clat, int nc) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nc) return;
+  ac[i] = x[i];
+  vc[i] = vlat ? vlat[clat[i]] : 0.0;
+}
+
+__global__ void k_advance(long long* step) { *step += 1; }
+
+__global__ void k_gather(const double* __restrict__ lat, const int64_t* __restrict__ idx, double* __restrict__ out,
+                         long long n) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = lat[idx[i]];
+}
+
+__global__ void k_scatter(const double* __restrict__ in, const int64_t* __restrict__ idx, double* __restrict__ lat,
+                          long long n) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) lat[idx[i]] = in[i];
+}
+
+// ------------------------------------------------------------------ launch helpers
+template <int P> struct Tile2 { static constexpr int E = P <= 4 ? 8 : 4; };
+constexpr int EX3 = 4, EY3 = 4, EZ3 = 8;
+
+template <int P>
+void launch_explicit_p(sc_ctx* c, const double* U, const double* Pv, double* out, const ExpP& e) {
+  const GridP& g = c->g;
+  if (g.dim == 1) {
+    k_explicit_1d<P><<<(unsigned)((g.nl[0] + 255) / 256), 256, 0, c->stream>>>(U, Pv, out, c->d_ntype, e,
+                                                                                c->d_flag);
+  } else if (g.dim == 2) {
+    constexpr int E2 = Tile2<P>::E;
+    dim3 grid((g.N[0] + E2 - 1) / E2, (g.N[1] + E2 - 1) / E2);
+    k_explicit_2d<P, E2, E2><<<grid, 256, 0, c->stream>>>(U, Pv, out, c->d_ntype, e, c->d_flag);
+  } else {
+    if constexpr (P <= 6) {
+      constexpr int RX = EX3 * P + P + 1, RY = EY3 * P + P + 1, TY = EY3 * P + 1;
+      const size_t smem = sizeof(double) * (2 * (P + 1) * RY * RX + 2 * (P + 1) * TY * RX);
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(k_explicit_3d<P, EX3, EY3, EZ3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+      }
+      dim3 grid((g.N[0] + EX3 - 1) / EX3, (g.N[1] + EY3 - 1) / EY3, (g.N[2] + EZ3 - 1) / EZ3);
+      k_explicit_3d<P, EX3, EY3, EZ3><<<grid, 256, smem, c->stream>>>(U, Pv, out, c->d_ntype, e, c->d_flag);
+    }
+  }
+}
+
+void launch_explicit(sc_ctx* c, const double* U, const double* Pv, double* out, double a1, double a2, double a3) {
+  const GridP& g = c->g;
+  ExpP e;
+
+  for (int k = 0; k < 3; ++k) {
+    e.nl[k] = (int)g.nl[k];
+    e.N[k] = g.N[k];
+    e.s[k] = k < g.dim ? (2.0 / g.h[k]) * (2.0 / g.h[k]) : 0.0;
+  }
+
+  e.a1 = a1;
+  e.a2 = a2;
+  e.coefR = a3 * c->c * c->c;
+  switch (g.p) {
+    case 1: launch_explicit_p<1>(c, U, Pv, out, e); break;
+    case 2: launch_explicit_p<2>(c, U, Pv, out, e); break;
+    case 3: launch_explicit_p<3>(c, U, Pv, out, e); break;
+    case 4: launch_explicit_p<4>(c, U, Pv, out, e); break;
+    case 5: launch_explicit_p<5>(c, U, Pv, out, e); break;
+    case 6: launch_explicit_p<6>(c, U, Pv, out, e); break;
+    case 7: launch_explicit_p<7>(c, U, Pv, out, e); break;
+    case 8: launch_explicit_p<8>(c, U, Pv, out, e); break;
+    default: throw ScError(SC_ERR_CONFIG, "p out of range");
+  }
+  SC_CUDA(cudaGetLastError());
+}
+
+SolveArgs solve_args(sc_ctx* c, const Factor& f) {
+  SolveArgs a;
+  a.items = c->d_items;
+  a.c0 = c->d_sn_c0;
+  a.w = c->d_sn_w;
+  a.r = c->d_sn_r;
+  a.roff = c->d_sn_roff;
+  a.uoff = c->d_sn_uoff;
+  a.goff = c->d_sn_goff;
+  a.R = c->d_R;
+  a.gptr = c->d_gptr;
+  a.gidx = c->d_gidx;
+  a.linv_off = c->d_sn_linv;
+  a.lr_off = c->d_sn_lr;
+  a.Linv = f.Linv;
+  a.LR = f.LR;
+  a.U = c->d_U;
+  a.b = c->d_b;
+  a.y = c->d_y;
+  a.x = c->d_x;
+  a.z = c->d_z;
+  return a;
+}
+
+}  // namespace
+
+void launch_solve(sc_ctx* c, const Factor& f) {
+  if (c->n_c == 0) return;
+  SolveArgs a = solve_args(c, f);
+  const size_t smemw = sizeof(double) * c->max_w;
+  for (int h = 0; h < c->height; ++h) {
+    const SolveLevel& L = c->levels[h];
+    if (L.nA) k_fwdA<<<L.nA, 256, smemw, c->stream>>>(a, L.offA);
+    if (L.nB) k_fwdB<<<L.nB, 256, smemw, c->stream>>>(a, L.offB);
+  }
+  for (int h = c->height - 1; h >= 0; --h) {
+    const SolveLevel& L = c->levels[h];
+    if (L.nbA) k_bwdA<<<L.nbA, 256, 0, c->stream>>>(a, L.offbA);
+    if (L.nbB) k_bwdB<<<L.nbB, 256, 0, c->stream>>>(a, L.offbB);
+  }
+  SC_CUDA(cudaGetLastError());
+}
+
+static int count_solve_launches(sc_ctx* c) {
+  int k = 0;
+  for (auto& L : c->levels) k += (L.nA > 0) + (L.nB > 0) + (L.nbA > 0) + (L.nbB > 0);
+  return k;
+}
+
+static void launch_celem(sc_ctx* c, int mode, const double* A, const double* B) {
+  if (c->n_celem == 0) return;
+  const int nb = c->nb;
+  const int tpe = std::min(256, ((nb + 31) / 32) * 32);
+  const int epb = 256 / tpe;
+  const unsigned blocks = (unsigned)((c->n_celem + epb - 1) / epb);
+  k_celem<<<blocks, epb * tpe, sizeof(double) * epb * nb, c->stream>>>(
+      mode, A, B, c->d_vc, c->d_ac, c->dt, c->d_celem_cell, c->d_celem_kidx, c->d_celem_cidx, c->d_Kcut,
+      c->d_Kref, c->d_Y, (int)c->n_celem, nb, tpe, c->g);
+  SC_CUDA(cudaGetLastError());
+}
+
+static void launch_irregular(sc_ctx* c, const double* U, const double* Pv, double* out, double a1, double a2,
+                             double a3) {
+  if (c->n_irr == 0) return;
+  k_irregular<<<(unsigned)((c->n_irr + 127) / 128), 128, 0, c->stream>>>(
+      U, Pv, out, c->d_irr_lat, c->d_irr_invm, c->d_irr_fx, (int)c->n_irr, c->d_cell_class, c->d_Kref, c->g,
+      c->d_ft, c->n_t, c->d_step, a1, a2, a3, c->d_flag);
+  SC_CUDA(cudaGetLastError());
+}
+
+// one Newmark IMEX step: u_n in d_u[parity], writes u_{n+1} into d_u[parity^1]
+void enqueue_step(sc_ctx* c, int parity) {
+  const double* A = c->d_u[parity];
+  double* B = c->d_u[parity ^ 1];
+  const double dt = c->dt;
+  // (a1)+(a2): explicit CDM on d DOFs
+  launch_explicit(c, A, B, B, 2.0, -1.0, dt * dt);
+  launch_irregular(c, A, B, B, 2.0, -1.0, dt * dt);
+  if (c->n_c > 0) {
+    // (a3)+(a4): predictor fused into the c-element products, then r^c
+    launch_celem(c, 0, A, B);
+    k_crhs<<<(unsigned)((c->n_c + 255) / 256), 256, 0, c->stream>>>(c->d_b, c->d_fxc, c->d_rhs_ptr, c->d_rhs_idx,
+                                                                     c->d_Y, (int)c->n_c, c->d_ft, c->n_t,
+                                                                     c->d_step, 1);
+    // (a5): S a^c_{n+1} = r^c
+    launch_solve(c, c->fS);
+    // (a6)
+    k_corrector<<<(unsigned)((c->n_c + 255) / 256), 256, 0, c->stream>>>(A, B, c->d_vc, c->d_ac, c->d_x,
+                                                                         c->d_c_lat, (int)c->n_c, dt, c->d_flag);
+  }
+  k_advance<<<1, 1, 0, c->stream>>>(c->d_step);
+  SC_CUDA(cudaGetLastError());
+}
+
+void build_graphs(sc_ctx* c) {
+  for (int par = 0; par < 2; ++par) {
+    cudaGraph_t gr;
+    SC_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    enqueue_step(c, par);
+    SC_CUDA(cudaStreamEndCapture(c->stream, &gr));
+    SC_CUDA(cudaGraphInstantiate(&c->graph[par], gr, 0));
+    cudaGraphDestroy(gr);
+  }
+  c->kernels_per_step = 1 + (c->n_irr > 0) + 1;
+  if (c->n_c > 0) c->kernels_per_step += 3 + count_solve_launches(c);
+}
+
+void device_upload_reference(sc_ctx* c) {
+  const int n1 = c->g.p + 1;
+  std::vector<double> M(SC_MAXP1 * SC_MAXP1, 0.0), K(SC_MAXP1 * SC_MAXP1, 0.0), w(SC_MAXP1, 0.0);
+  for (int i = 0; i < n1; ++i) {
+    w[i] = c->gll_w[i];
+    for (int j = 0; j < n1; ++j) {
+      M[i * n1 + j] = c->Mhat[i * n1 + j];
+      K[i * n1 + j] = c->Khat[i * n1 + j];
+    }
+  }
+  SC_CUDA(cudaMemcpyToSymbol(c_Mh, M.data(), sizeof(double) * M.size()));
+  SC_CUDA(cudaMemcpyToSymbol(c_Kh, K.data(), sizeof(double) * K.size()));
+  SC_CUDA(cudaMemcpyToSymbol(c_w, w.data(), sizeof(double) * w.size()));
+  SC_CUDA(cudaMalloc(&c->d_Kref, sizeof(double) * c->Kref.size()));
+  SC_CUDA(cudaMemcpy(c->d_Kref, c->Kref.data(), sizeof(double) * c->Kref.size(), cudaMemcpyHostToDevice));
+}
+
+void gather_dofs(sc_ctx* c, const double* d_lat, double* d_out) {
+  if (c->n_dof == 0) return;
+  k_gather<<<(unsigned)((c->n_dof + 255) / 256), 256, 0, c->stream>>>(d_lat, c->d_dof_lat, d_out, c->n_dof);
+  SC_CUDA(cudaGetLastError());
+}
+
+// Consistent start (reading C3): a_0 = M^-1 (f_t(0) f_x - K u_0) blockwise,
+// u^d_{-1} = u^d_0 - dt v^d_0 + dt^2/2 a^d_0; v^c = v^c_0, a^c = a^c_0.
+// u0, v0: DEVICE arrays of length n_dof (canonical) or nullptr.
+void run_startup(sc_ctx* c, const double* u0, const double* v0) {
+  const size_t latb = sizeof(double) * c->n_lat;
+  c->cur = 0;
+  double* A = c->d_u[0];
+  double* B = c->d_u[1];
+  SC_CUDA(cudaMemsetAsync(A, 0, latb, c->stream));
+  SC_CUDA(cudaMemsetAsync(B, 0, latb, c->stream));
+  SC_CUDA(cudaMemsetAsync(c->d_step, 0, sizeof(long long), c->stream));
+  SC_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+  const unsigned gb = (unsigned)((c->n_dof + 255) / 256);
+  if (u0 && c->n_dof) k_scatter<<<gb, 256, 0, c->stream>>>(u0, c->d_dof_lat, A, c->n_dof);
+  double* vlat = nullptr;
+  if (v0 && c->n_dof) {
+    SC_CUDA(cudaMalloc(&vlat, latb));
+    SC_CUDA(cudaMemsetAsync(vlat, 0, latb, c->stream));
+    k_scatter<<<gb, 256, 0, c->stream>>>(v0, c->d_dof_lat, vlat, c->n_dof);
+  }
+  const double dt = c->dt;
+  // d part: B = u0 - dt v0 + dt^2/2 a0  (P = v0 lattice, or A with a2 = 0 when v0 == 0)
+  const double* Pv = vlat ? vlat : A;
+  const double a2 = vlat ? -dt : 0.0;
+  launch_explicit(c, A, Pv, B, 1.0, a2, 0.5 * dt * dt);
+  launch_irregular(c, A, Pv, B, 1.0, a2, 0.5 * dt * dt);
+  if (c->n_c > 0) {
+    launch_celem(c, 1, A, A);
+    k_crhs<<<(unsigned)((c->n_c + 255) / 256), 256, 0, c->stream>>>(c->d_b, c->d_fxc, c->d_rhs_ptr, c->d_rhs_idx,
+                                                                     c->d_Y, (int)c->n_c, c->d_ft, c->n_t,
+                                                                     c->d_step, 0);
+    launch_solve(c, c->fM);
+    k_start_c<<<(unsigned)((c->n_c + 255) / 256), 256, 0, c->stream>>>(c->d_ac, c->d_vc, c->d_x, vlat, c->d_c_lat,
+                                                                        (int)c->n_c);
+  }
+  SC_CUDA(cudaGetLastError());
+  SC_CUDA(cudaStreamSynchronize(c->stream));
+  if (vlat) cudaFree(vlat);
+  c->host_step = 0;
+}
+
+// instrumentation (sc_profile): one launch of a single sub-kernel on the context stream
+void profile_launch(sc_ctx* c, int which) {
+  const double* A = c->d_u[c->cur];
+  double* B = c->d_u[c->cur ^ 1];
+  if (which == 0) launch_explicit(c, A, B, B, 2.0, -1.0, c->dt * c->dt);
+  else if (which == 1) launch_celem(c, 0, A, B);
+  else launch_solve(c, c->fS);
+}
