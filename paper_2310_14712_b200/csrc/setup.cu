@@ -211,7 +211,7 @@ __device__ double d_lagr(const double* nodes, int n, int i, double xi, double* d
 // Cut-cell element matrices: one CTA per CUT cell; each thread owns a 4x4 tile of both M_e
 // and K_e; quadrature points are staged in chunks of QC points in shared memory.
 #define QC 8
-__global__ void k_cut_matrices(GridP g, const DVoid* __restrict__ V, int nv, const long long* __restrict__ cells,
+__global__ void __launch_bounds__(256) k_cut_matrices(GridP g, const DVoid* __restrict__ V, int nv, const long long* __restrict__ cells,
                                const int* __restrict__ slot, const unsigned long long* __restrict__ leaves,
                                const int* __restrict__ nleaves, int cap, const double* __restrict__ gll,
                                const double* __restrict__ gx, const double* __restrict__ gw,
@@ -239,15 +239,19 @@ __global__ void k_cut_matrices(GridP g, const DVoid* __restrict__ V, int nv, con
   __syncthreads();
   const int nc = s_nc;
   const int T = nbp / 4;
-  const int i0 = (threadIdx.x % T) * 4, j0 = (threadIdx.x / T) * 4;
-  const bool active = threadIdx.x < T * T;
-  double accM[4][4], accK[4][4];
-  for (int a = 0; a < 4; ++a)
-    for (int b = 0; b < 4; ++b) accM[a][b] = accK[a][b] = 0.0;
+  const int ntiles = T * T;
   const int npts = (d == 1) ? P1 : (d == 2 ? P1 * P1 : P1 * P1 * P1);
   const int nl = nleaves[sl];
   const long long total = (long long)nl * npts;
   double hk[3] = {g.h[0], g.h[1], g.h[2]};
+  // tile groups: each thread owns one 4x4 tile per group; the quadrature is replayed per group
+  for (int tg = 0; tg * (int)blockDim.x < ntiles; ++tg) {
+  const int tile = tg * blockDim.x + threadIdx.x;
+  const int i0 = (tile % T) * 4, j0 = (tile / T) * 4;
+  const bool active = tile < ntiles;
+  double accM[4][4], accK[4][4];
+  for (int a = 0; a < 4; ++a)
+    for (int b = 0; b < 4; ++b) accM[a][b] = accK[a][b] = 0.0;
   for (long long q0 = 0; q0 < total; q0 += QC) {
     const int nq = (int)min((long long)QC, total - q0);
     // per point, per axis: 1D basis values/derivatives; weight with alpha
@@ -346,6 +350,8 @@ __global__ void k_cut_matrices(GridP g, const DVoid* __restrict__ V, int nv, con
           Mout[(long long)e * nb * nb + (long long)i * nb + j] = rho * accM[a][b];
         }
       }
+  }
+  __syncthreads();
   }
 }
 
@@ -485,7 +491,7 @@ void setup_device_geometry(sc_ctx* c) {
     SC_CUDA(cudaMalloc(&d_M, sizeof(double) * mat));
     const int nbp = ((nb + 15) / 16) * 16;
     if (nbp > 128) throw ScError(SC_ERR_CONFIG, "(p+1)^dim > 128 not supported by the cut-cell kernel");
-    const int threads = std::max(32, (nbp / 4) * (nbp / 4));
+    const int threads = std::min(256, std::max(32, (nbp / 4) * (nbp / 4)));
     const size_t smem = sizeof(double) * (4 * QC * nbp + 2 * QC * 3 * SC_MAXP1 + QC);
     SC_CUDA(cudaFuncSetAttribute(k_cut_matrices, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_cut_matrices<<<(unsigned)c->n_cut, threads, smem, c->stream>>>(
