@@ -10,7 +10,7 @@ OUT = os.path.join(HERE, "libsc.so")
 BUILD = os.path.join(HERE, "_build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU = ["setup.cu", "step.cu"]
+CU = ["setup.cu", "step.cu", "solve.cu"]
 CPP = ["rules.cpp", "factor.cpp", "api.cpp"]
 
 

@@ -515,6 +515,28 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   }
   // ---------------- numeric multifrontal factorisation of S and M^cc
   const double beta_dt2 = 0.25 * c->dt * c->dt;
+  // symmetric Jacobi scaling D A D (unit diagonal): the fictitious-region rows of S are
+  // ~1/alpha smaller than the physical ones; scaling keeps L_ss^{-1} well conditioned so
+  // the inverse-based device sweeps stay as accurate as substitution.
+  std::vector<double> dS(nc, 0.0), dM(nc, 0.0);
+  for (int e = 0; e < ne; ++e) {
+    const int kidx = b.celem_kidx[e];
+    for (int l = 0; l < nb; ++l) {
+      const int i = b.celem_cidx[(size_t)e * nb + l];
+      if (i < 0) continue;
+      const double m = kidx >= 0 ? c->Mcut_host[(size_t)kidx * nb * nb + (size_t)l * nb + l] : c->Mref[l];
+      const double k = kidx >= 0 ? c->Kcut_host[(size_t)kidx * nb * nb + (size_t)l * nb + l]
+                                 : c->Kref[(size_t)l * nb + l];
+      dS[i] += m + beta_dt2 * k;
+      dM[i] += m;
+    }
+  }
+  for (int i = 0; i < nc; ++i) {
+    if (!(dS[i] > 0.0) || !(dM[i] > 0.0))
+      throw ScError(SC_ERR_NUMERIC, "non-positive diagonal of S or M^cc at c DOF " + std::to_string(i));
+    dS[i] = 1.0 / std::sqrt(dS[i]);
+    dM[i] = 1.0 / std::sqrt(dM[i]);
+  }
   std::vector<int64_t> linv_off(nsn + 1, 0), lr_off(nsn + 1, 0);
   for (int s = 0; s < nsn; ++s) {
     linv_off[s + 1] = linv_off[s] + (int64_t)b.sn[s].w * b.sn[s].w;
@@ -555,7 +577,8 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
               if (i < jnd) continue;
               double m = Me ? Me[(size_t)li * nb + lj] : (li == lj ? Mref[li] : 0.0);
               double val = which == 0 ? m + beta_dt2 * Ke[(size_t)li * nb + lj] : m;
-              F[(size_t)jj * n + pos(i)] += val;
+              const std::vector<double>& dd = which == 0 ? dS : dM;
+              F[(size_t)jj * n + pos(i)] += val * dd[i] * dd[jnd];
             }
           }
         }
@@ -638,29 +661,35 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
     gptr[t + 1] = gptr[t] + (int32_t)gl[t].size();
     gidx.insert(gidx.end(), gl[t].begin(), gl[t].end());
   }
-  // work items per height: fwdA (rows of Linv, 32 per item), fwdB (rows of L_R, 32 per item),
-  // bwdA (columns, 8 per item), bwdB (outputs, 8 per item)
-  std::vector<int32_t> items;
-  c->levels.assign(c->height, SolveLevel{});
+  // persistent-solve work list in topological order (solve.cu):
+  //  forward, heights ascending:  fA items (32 rows of L_ss^{-1}) then fB items (32 rows of L_R)
+  //  backward, heights descending: bA items (8 columns) then bB items (8 outputs)
+  std::vector<int32_t> items;  // int4 (type, s, start, 0)
+  std::vector<int32_t> nitem(4 * (size_t)nsn, 0);
+  std::vector<std::vector<int>> by_h(c->height);
+  for (int s = 0; s < nsn; ++s) by_h[b.sn[s].height].push_back(s);
+  auto push = [&](int type, int s, int start) {
+    items.insert(items.end(), {type, s, start, 0});
+    ++nitem[(size_t)type * nsn + s];
+  };
   for (int h = 0; h < c->height; ++h) {
-    SolveLevel& L = c->levels[h];
-    L.offA = (int)items.size() / 2;
-    for (int s = 0; s < nsn; ++s)
-      if (b.sn[s].height == h)
-        for (int i = 0; i < wv[s]; i += 32) items.insert(items.end(), {s, i});
-    L.nA = (int)items.size() / 2 - L.offA;
-    L.offB = (int)items.size() / 2;
-    for (int s = 0; s < nsn; ++s)
-      if (b.sn[s].height == h)
-        for (int i = 0; i < rv[s]; i += 32) items.insert(items.end(), {s, i});
-    L.nB = (int)items.size() / 2 - L.offB;
-    L.offbA = (int)items.size() / 2;
-    for (int s = 0; s < nsn; ++s)
-      if (b.sn[s].height == h)
-        for (int i = 0; i < wv[s]; i += 8) items.insert(items.end(), {s, i});
-    L.nbA = (int)items.size() / 2 - L.offbA;
-    L.offbB = L.offbA;  // same decomposition (8 columns / outputs per item)
-    L.nbB = L.nbA;
+    for (int s : by_h[h])
+      for (int i = 0; i < wv[s]; i += 32) push(0, s, i);
+    for (int s : by_h[h])
+      for (int i = 0; i < rv[s]; i += 32) push(1, s, i);
+  }
+  for (int h = c->height - 1; h >= 0; --h) {
+    for (int s : by_h[h])
+      for (int i = 0; i < wv[s]; i += 8) push(2, s, i);
+    for (int s : by_h[h])
+      for (int i = 0; i < wv[s]; i += 8) push(3, s, i);
+  }
+  c->n_items = (int)(items.size() / 4);
+  std::vector<int32_t> chptr(nsn + 1, 0), chidx, parent(nsn, -1);
+  for (int s = 0; s < nsn; ++s) {
+    for (int ch : b.sn[s].children) chidx.push_back(ch);
+    chptr[s + 1] = (int32_t)chidx.size();
+    parent[s] = b.sn[s].parent;
   }
   auto up32 = [&](int32_t** dst, const std::vector<int32_t>& v) {
     SC_CUDA(cudaMalloc(dst, sizeof(int32_t) * std::max<size_t>(1, v.size())));
@@ -686,6 +715,11 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   up32(&c->d_gptr, gptr);
   up32(&c->d_gidx, gidx);
   up32(&c->d_items, items);
+  up32(&c->d_nitem, nitem);
+  up32(&c->d_chptr, chptr);
+  up32(&c->d_chidx, chidx);
+  up32(&c->d_parent, parent);
+  SC_CUDA(cudaMalloc(&c->d_solve_cnt, sizeof(int) * (4 * (size_t)nsn + 1)));
   upd_(&c->fS.Linv, hLinvS);
   upd_(&c->fS.LR, hLRS);
   upd_(&c->fM.Linv, hLinvM);
@@ -720,6 +754,8 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   }
   up32(&c->d_c_lat, clat32);
   upd_(&c->d_fxc, fxc);
+  upd_(&c->fS.d, dS);
+  upd_(&c->fM.d, dM);
   const size_t ncs = std::max(1, nc);
   SC_CUDA(cudaMalloc(&c->d_vc, sizeof(double) * ncs));
   SC_CUDA(cudaMalloc(&c->d_ac, sizeof(double) * ncs));
@@ -728,6 +764,32 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   SC_CUDA(cudaMalloc(&c->d_x, sizeof(double) * ncs));
   SC_CUDA(cudaMalloc(&c->d_z, sizeof(double) * ncs));
   SC_CUDA(cudaMalloc(&c->d_Y, sizeof(double) * std::max<size_t>(1, (size_t)ne * nb)));
+  SolveDev& sd = c->solve_dev;
+  sd.items = reinterpret_cast<const int4*>(c->d_items);
+  sd.n_items = c->n_items;
+  sd.n_sn = nsn;
+  sd.w = c->d_sn_w;
+  sd.r = c->d_sn_r;
+  sd.c0 = c->d_sn_c0;
+  sd.goff = c->d_sn_goff;
+  sd.gptr = c->d_gptr;
+  sd.gidx = c->d_gidx;
+  sd.uoff = c->d_sn_uoff;
+  sd.roff = c->d_sn_roff;
+  sd.R = c->d_R;
+  sd.linv_off = c->d_sn_linv;
+  sd.lr_off = c->d_sn_lr;
+  sd.nitem = c->d_nitem;
+  sd.chptr = c->d_chptr;
+  sd.chidx = c->d_chidx;
+  sd.parent = c->d_parent;
+  sd.U = c->d_U;
+  sd.b = c->d_b;
+  sd.y = c->d_y;
+  sd.x = c->d_x;
+  sd.z = c->d_z;
+  sd.cnt = c->d_solve_cnt;
+  sd.head = c->d_solve_cnt + 4 * (size_t)nsn;
   c->Kcut_host.clear();
   c->Kcut_host.shrink_to_fit();
   c->Mcut_host.clear();

@@ -30,14 +30,24 @@ struct GridP {
   double h[3];
 };
 
-struct SolveLevel {      // work items of one supernode-height level
-  int nA, nB, nbA, nbB;  // item counts (forward A/B, backward A/B)
-  int offA, offB, offbA, offbB;
+// device view of the supernodal factor structure + persistent-solve work list (solve.cu)
+struct SolveDev {
+  const int4* items;           // (type, supernode, start, 0) in topological order
+  int n_items, n_sn;
+  const int32_t *w, *r, *c0, *goff, *gptr, *gidx, *uoff, *roff, *R;
+  const int64_t *linv_off, *lr_off;
+  const int32_t *nitem;        // [4][n_sn] item counts per phase
+  const int32_t *chptr, *chidx, *parent;
+  const double *Linv, *LR;
+  double *U, *b, *y, *x, *z;
+  int* cnt;                    // [4][n_sn] completed items per phase
+  int* head;                   // dequeue counter
 };
 
 struct Factor {          // device factor of one SPD matrix (S or M^cc), shared symbolic
   double* Linv = nullptr;  // per supernode w x w column-major inverse of L_ss (lower)
   double* LR = nullptr;    // per supernode r x w column-major L_{R_s, s}
+  double* d = nullptr;     // Jacobi scaling: the factor is of D A D, D = diag(A)^{-1/2}
 };
 
 struct sc_ctx {
@@ -102,8 +112,11 @@ struct sc_ctx {
   int32_t *d_sn_roff = nullptr, *d_sn_uoff = nullptr, *d_sn_goff = nullptr;
   int32_t* d_R = nullptr;             // row structures (ND c indices)
   int32_t *d_gptr = nullptr, *d_gidx = nullptr;
-  int32_t* d_items = nullptr;         // work items (sn, start) pairs
-  std::vector<SolveLevel> levels;
+  int32_t* d_items = nullptr;         // int4 work items
+  int32_t *d_nitem = nullptr, *d_chptr = nullptr, *d_chidx = nullptr, *d_parent = nullptr;
+  int* d_solve_cnt = nullptr;         // [4*n_sn] counters + head
+  int n_items = 0, solve_grid = 0;
+  SolveDev solve_dev{};
   Factor fS, fM;
   int64_t nnz_factor = 0;
   int64_t n_components = 0;

@@ -237,7 +237,9 @@ __global__ void k_irregular(const double* __restrict__ U, const double* Pv, doub
                             const int8_t* __restrict__ cls, const double* __restrict__ Kref, GridP g,
                             const double* __restrict__ ft, long long n_t, const long long* step, double a1,
                             double a2, double a3, int* flag) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  // one warp per node; lanes split the element-local dot products
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (t >= n) return;
   const long long L = lat[t];
   const int P = g.p, n1 = P + 1;
@@ -276,7 +278,7 @@ __global__ void k_irregular(const double* __restrict__ U, const double* Pv, doub
           li += (int)(ijk[k] - (long long)cc[k] * P) * mul;
           mul *= n1;
         }
-        for (int loc = 0; loc < nb; ++loc) {
+        for (int loc = lane; loc < nb; loc += 32) {
           const int l0 = loc % n1, l1 = (loc / n1) % n1, l2 = loc / (n1 * n1);
           long long gl = (long long)c0 * P + l0;
           if (g.dim > 1) gl += g.nl[0] * ((long long)c1 * P + l1);
@@ -284,6 +286,9 @@ __global__ void k_irregular(const double* __restrict__ U, const double* Pv, doub
           Ku += Kref[(size_t)li * nb + loc] * U[gl];
         }
       }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) Ku += __shfl_xor_sync(0xffffffffu, Ku, o);
+  if (lane) return;
   const double r = ft_at(ft, n_t, step, 0) * fx[t] - Ku;
   const double res = a1 * U[L] + a2 * Pv[L] + a3 * r * invm[t];
   out[L] = res;
@@ -345,120 +350,26 @@ __global__ void k_celem(int mode, const double* __restrict__ A, const double* __
 
 __global__ void k_crhs(double* __restrict__ b, const double* __restrict__ fxc, const int32_t* __restrict__ ptr,
                        const int32_t* __restrict__ idx, const double* __restrict__ Y, int nc,
-                       const double* __restrict__ ft, long long n_t, const long long* step, int off) {
+                       const double* __restrict__ ft, long long n_t, const long long* step, int off,
+                       const double* __restrict__ dscale) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nc) return;
   double s = 0.0;
   for (int q = ptr[i]; q < ptr[i + 1]; ++q) s += Y[idx[q]];
-  b[i] = ft_at(ft, n_t, step, off) * fxc[i] - s;
-}
-
-// ------------------------------------------------------------------ supernodal solves
-struct SolveArgs {
-  const int32_t *items, *c0, *w, *r, *roff, *uoff, *goff, *R, *gptr, *gidx;
-  const int64_t *linv_off, *lr_off;
-  const double *Linv, *LR;
-  double *U, *b, *y, *x, *z;
-};
-
-// y_s = L_ss^{-1} (b_s - gathered child updates); rows (32 per item) x warps over columns
-__global__ void __launch_bounds__(256) k_fwdA(SolveArgs a, int off) {
-  extern __shared__ double F[];
-  __shared__ double part[8][33];
-  const int s = a.items[2 * (off + blockIdx.x)], i0 = a.items[2 * (off + blockIdx.x) + 1];
-  const int w = a.w[s], c0 = a.c0[s], go = a.goff[s];
-  for (int t = threadIdx.x; t < w; t += blockDim.x) {
-    double f = a.b[c0 + t];
-    for (int q = a.gptr[go + t]; q < a.gptr[go + t + 1]; ++q) f -= a.U[a.gidx[q]];
-    F[t] = f;
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int i = i0 + lane;
-  const int jmax = min(w, i0 + 32);
-  const double* L = a.Linv + a.linv_off[s];
-  double acc = 0.0;
-  if (i < w) {
-    for (int j = warp; j < jmax; j += 8) acc += L[i + (size_t)j * w] * F[j];
-  }
-  part[warp][lane] = acc;
-  __syncthreads();
-  if (warp == 0 && i < w) {
-    double t = 0.0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) t += part[k][lane];
-    a.y[c0 + i] = t;
-  }
-}
-
-// U_s = gathered child updates (rows R_s) + L_{R_s,s} y_s
-__global__ void __launch_bounds__(256) k_fwdB(SolveArgs a, int off) {
-  extern __shared__ double ys[];
-  __shared__ double part[8][33];
-  const int s = a.items[2 * (off + blockIdx.x)], i0 = a.items[2 * (off + blockIdx.x) + 1];
-  const int w = a.w[s], r = a.r[s], c0 = a.c0[s], go = a.goff[s];
-  for (int t = threadIdx.x; t < w; t += blockDim.x) ys[t] = a.y[c0 + t];
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int i = i0 + lane;
-  const double* L = a.LR + a.lr_off[s];
-  double acc = 0.0;
-  if (i < r) {
-    for (int j = warp; j < w; j += 8) acc += L[i + (size_t)j * r] * ys[j];
-  }
-  part[warp][lane] = acc;
-  __syncthreads();
-  if (warp == 0 && i < r) {
-    double t = 0.0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) t += part[k][lane];
-    for (int q = a.gptr[go + w + i]; q < a.gptr[go + w + i + 1]; ++q) t += a.U[a.gidx[q]];
-    a.U[a.uoff[s] + i] = t;
-  }
-}
-
-// z_j = y_j - sum_i L_R[i,j] x[R_i]   (warp per column j)
-__global__ void __launch_bounds__(256) k_bwdA(SolveArgs a, int off) {
-  const int s = a.items[2 * (off + blockIdx.x)], j0 = a.items[2 * (off + blockIdx.x) + 1];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int w = a.w[s], r = a.r[s], c0 = a.c0[s];
-  const int j = j0 + warp;
-  if (j >= w) return;
-  const double* L = a.LR + a.lr_off[s] + (size_t)j * r;
-  const int32_t* R = a.R + a.roff[s];
-  double acc = 0.0;
-  for (int i = lane; i < r; i += 32) acc += L[i] * a.x[R[i]];
-#pragma unroll
-  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) a.z[c0 + j] = a.y[c0 + j] - acc;
-}
-
-// x_i = sum_{j>=i} Linv[j,i] z_j   (warp per output i; column i of Linv is contiguous)
-__global__ void __launch_bounds__(256) k_bwdB(SolveArgs a, int off) {
-  const int s = a.items[2 * (off + blockIdx.x)], i0 = a.items[2 * (off + blockIdx.x) + 1];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int w = a.w[s], c0 = a.c0[s];
-  const int i = i0 + warp;
-  if (i >= w) return;
-  const double* L = a.Linv + a.linv_off[s] + (size_t)i * w;
-  double acc = 0.0;
-  for (int j = i + lane; j < w; j += 32) acc += L[j] * a.z[c0 + j];
-#pragma unroll
-  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) a.x[c0 + i] = acc;
+  b[i] = dscale[i] * (ft_at(ft, n_t, step, off) * fxc[i] - s);   // D r^c (scaled system)
 }
 
 // ------------------------------------------------------------------ corrector / misc
 __global__ void k_corrector(const double* __restrict__ A, double* __restrict__ B, double* __restrict__ vc,
                             double* __restrict__ ac, const double* __restrict__ x, const int32_t* __restrict__ clat,
-                            int nc, double dt, int* flag) {
+                            int nc, double dt, int* flag, const double* __restrict__ dscale) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nc) return;
   const int32_t L = clat[i];
   const double v = vc[i], a = ac[i];
   const double ut = A[L] + dt * v + 0.25 * dt * dt * a;   // (a3) predictor
   const double vt = v + 0.5 * dt * a;
-  const double an = x[i];                                  // (a5) result
+  const double an = dscale[i] * x[i];                      // (a5) result, x = D y
   const double un = ut + 0.25 * dt * dt * an;              // (a6) corrector
   B[L] = un;
   vc[i] = vt + 0.5 * dt * an;
@@ -467,10 +378,11 @@ __global__ void k_corrector(const double* __restrict__ A, double* __restrict__ B
 }
 
 __global__ void k_start_c(double* __restrict__ ac, double* __restrict__ vc, const double* __restrict__ x,
-                          const double* __restrict__ vlat, const int32_t* __restrict__ clat, int nc) {
+                          const double* __restrict__ vlat, const int32_t* __restrict__ clat, int nc,
+                          const double* __restrict__ dscale) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nc) return;
-  ac[i] = x[i];
+  ac[i] = dscale[i] * x[i];
   vc[i] = vlat ? vlat[clat[i]] : 0.0;
 }
 
@@ -544,54 +456,7 @@ void launch_explicit(sc_ctx* c, const double* U, const double* Pv, double* out, 
   SC_CUDA(cudaGetLastError());
 }
 
-SolveArgs solve_args(sc_ctx* c, const Factor& f) {
-  SolveArgs a;
-  a.items = c->d_items;
-  a.c0 = c->d_sn_c0;
-  a.w = c->d_sn_w;
-  a.r = c->d_sn_r;
-  a.roff = c->d_sn_roff;
-  a.uoff = c->d_sn_uoff;
-  a.goff = c->d_sn_goff;
-  a.R = c->d_R;
-  a.gptr = c->d_gptr;
-  a.gidx = c->d_gidx;
-  a.linv_off = c->d_sn_linv;
-  a.lr_off = c->d_sn_lr;
-  a.Linv = f.Linv;
-  a.LR = f.LR;
-  a.U = c->d_U;
-  a.b = c->d_b;
-  a.y = c->d_y;
-  a.x = c->d_x;
-  a.z = c->d_z;
-  return a;
-}
-
 }  // namespace
-
-void launch_solve(sc_ctx* c, const Factor& f) {
-  if (c->n_c == 0) return;
-  SolveArgs a = solve_args(c, f);
-  const size_t smemw = sizeof(double) * c->max_w;
-  for (int h = 0; h < c->height; ++h) {
-    const SolveLevel& L = c->levels[h];
-    if (L.nA) k_fwdA<<<L.nA, 256, smemw, c->stream>>>(a, L.offA);
-    if (L.nB) k_fwdB<<<L.nB, 256, smemw, c->stream>>>(a, L.offB);
-  }
-  for (int h = c->height - 1; h >= 0; --h) {
-    const SolveLevel& L = c->levels[h];
-    if (L.nbA) k_bwdA<<<L.nbA, 256, 0, c->stream>>>(a, L.offbA);
-    if (L.nbB) k_bwdB<<<L.nbB, 256, 0, c->stream>>>(a, L.offbB);
-  }
-  SC_CUDA(cudaGetLastError());
-}
-
-static int count_solve_launches(sc_ctx* c) {
-  int k = 0;
-  for (auto& L : c->levels) k += (L.nA > 0) + (L.nB > 0) + (L.nbA > 0) + (L.nbB > 0);
-  return k;
-}
 
 static void launch_celem(sc_ctx* c, int mode, const double* A, const double* B) {
   if (c->n_celem == 0) return;
@@ -608,7 +473,7 @@ static void launch_celem(sc_ctx* c, int mode, const double* A, const double* B) 
 static void launch_irregular(sc_ctx* c, const double* U, const double* Pv, double* out, double a1, double a2,
                              double a3) {
   if (c->n_irr == 0) return;
-  k_irregular<<<(unsigned)((c->n_irr + 127) / 128), 128, 0, c->stream>>>(
+  k_irregular<<<(unsigned)((c->n_irr * 32 + 127) / 128), 128, 0, c->stream>>>(
       U, Pv, out, c->d_irr_lat, c->d_irr_invm, c->d_irr_fx, (int)c->n_irr, c->d_cell_class, c->d_Kref, c->g,
       c->d_ft, c->n_t, c->d_step, a1, a2, a3, c->d_flag);
   SC_CUDA(cudaGetLastError());
@@ -627,12 +492,12 @@ void enqueue_step(sc_ctx* c, int parity) {
     launch_celem(c, 0, A, B);
     k_crhs<<<(unsigned)((c->n_c + 255) / 256), 256, 0, c->stream>>>(c->d_b, c->d_fxc, c->d_rhs_ptr, c->d_rhs_idx,
                                                                      c->d_Y, (int)c->n_c, c->d_ft, c->n_t,
-                                                                     c->d_step, 1);
+                                                                     c->d_step, 1, c->fS.d);
     // (a5): S a^c_{n+1} = r^c
     launch_solve(c, c->fS);
     // (a6)
     k_corrector<<<(unsigned)((c->n_c + 255) / 256), 256, 0, c->stream>>>(A, B, c->d_vc, c->d_ac, c->d_x,
-                                                                         c->d_c_lat, (int)c->n_c, dt, c->d_flag);
+                                                                         c->d_c_lat, (int)c->n_c, dt, c->d_flag, c->fS.d);
   }
   k_advance<<<1, 1, 0, c->stream>>>(c->d_step);
   SC_CUDA(cudaGetLastError());
@@ -648,7 +513,7 @@ void build_graphs(sc_ctx* c) {
     cudaGraphDestroy(gr);
   }
   c->kernels_per_step = 1 + (c->n_irr > 0) + 1;
-  if (c->n_c > 0) c->kernels_per_step += 3 + count_solve_launches(c);
+  if (c->n_c > 0) c->kernels_per_step += 3 + (c->n_items > 0 ? 1 : 0);
 }
 
 void device_upload_reference(sc_ctx* c) {
@@ -704,10 +569,10 @@ void run_startup(sc_ctx* c, const double* u0, const double* v0) {
     launch_celem(c, 1, A, A);
     k_crhs<<<(unsigned)((c->n_c + 255) / 256), 256, 0, c->stream>>>(c->d_b, c->d_fxc, c->d_rhs_ptr, c->d_rhs_idx,
                                                                      c->d_Y, (int)c->n_c, c->d_ft, c->n_t,
-                                                                     c->d_step, 0);
+                                                                     c->d_step, 0, c->fM.d);
     launch_solve(c, c->fM);
     k_start_c<<<(unsigned)((c->n_c + 255) / 256), 256, 0, c->stream>>>(c->d_ac, c->d_vc, c->d_x, vlat, c->d_c_lat,
-                                                                        (int)c->n_c);
+                                                                        (int)c->n_c, c->fM.d);
   }
   SC_CUDA(cudaGetLastError());
   SC_CUDA(cudaStreamSynchronize(c->stream));
