@@ -208,6 +208,17 @@ __device__ double d_lagr(const double* nodes, int n, int i, double xi, double* d
   return val;
 }
 
+// s + c += x*y with an error-free product (fma) and Neumaier's compensated addition; the
+// _rn intrinsics keep the compiler from contracting the error terms into FMAs.
+__device__ __forceinline__ void comp_add(double& s, double& c, double x, double y) {
+  const double p = __dmul_rn(x, y);
+  const double e = fma(x, y, -p);
+  const double t = __dadd_rn(s, p);
+  const double z = fabs(s) >= fabs(p) ? __dadd_rn(__dadd_rn(s, -t), p) : __dadd_rn(__dadd_rn(p, -t), s);
+  c = __dadd_rn(c, __dadd_rn(z, e));
+  s = t;
+}
+
 // Cut-cell element matrices: one CTA per CUT cell; each thread owns a 4x4 tile of both M_e
 // and K_e; quadrature points are staged in chunks of QC points in shared memory.
 #define QC 8
@@ -249,9 +260,12 @@ __global__ void __launch_bounds__(256) k_cut_matrices(GridP g, const DVoid* __re
   const int tile = tg * blockDim.x + threadIdx.x;
   const int i0 = (tile % T) * 4, j0 = (tile / T) * 4;
   const bool active = tile < ntiles;
-  double accM[4][4], accK[4][4];
+  // compensated (Neumaier + exact-product) accumulation: the quadrature sums have up to
+  // (2^D)^d (p+1)^d terms with cancellation; plain accumulation loses ~sqrt(n) ulps, which
+  // the IMEX recursion amplifies over thousands of steps (reading C23)
+  double accM[4][4], accK[4][4], cmpM[4][4], cmpK[4][4];
   for (int a = 0; a < 4; ++a)
-    for (int b = 0; b < 4; ++b) accM[a][b] = accK[a][b] = 0.0;
+    for (int b = 0; b < 4; ++b) accM[a][b] = accK[a][b] = cmpM[a][b] = cmpK[a][b] = 0.0;
   for (long long q0 = 0; q0 < total; q0 += QC) {
     const int nq = (int)min((long long)QC, total - q0);
     // per point, per axis: 1D basis values/derivatives; weight with alpha
@@ -327,7 +341,7 @@ __global__ void __launch_bounds__(256) k_cut_matrices(GridP g, const DVoid* __re
           nj[a] = sN[qq * nbp + j0 + a];
         }
         for (int a = 0; a < 4; ++a)
-          for (int b = 0; b < 4; ++b) accM[a][b] += ni[a] * nj[b];
+          for (int b = 0; b < 4; ++b) comp_add(accM[a][b], cmpM[a][b], ni[a], nj[b]);
         for (int k = 0; k < d; ++k) {
           const double* G = &sG[(k * QC + qq) * nbp];
           for (int a = 0; a < 4; ++a) {
@@ -335,7 +349,7 @@ __global__ void __launch_bounds__(256) k_cut_matrices(GridP g, const DVoid* __re
             nj[a] = G[j0 + a];
           }
           for (int a = 0; a < 4; ++a)
-            for (int b = 0; b < 4; ++b) accK[a][b] += ni[a] * nj[b];
+            for (int b = 0; b < 4; ++b) comp_add(accK[a][b], cmpK[a][b], ni[a], nj[b]);
         }
       }
     }
@@ -346,8 +360,8 @@ __global__ void __launch_bounds__(256) k_cut_matrices(GridP g, const DVoid* __re
       for (int b = 0; b < 4; ++b) {
         const int i = i0 + a, j = j0 + b;
         if (i < nb && j < nb) {
-          Kout[(long long)e * nb * nb + (long long)i * nb + j] = rho * c2 * accK[a][b];
-          Mout[(long long)e * nb * nb + (long long)i * nb + j] = rho * accM[a][b];
+          Kout[(long long)e * nb * nb + (long long)i * nb + j] = rho * c2 * (accK[a][b] + cmpK[a][b]);
+          Mout[(long long)e * nb * nb + (long long)i * nb + j] = rho * (accM[a][b] + cmpM[a][b]);
         }
       }
   }

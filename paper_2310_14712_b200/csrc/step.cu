@@ -119,8 +119,8 @@ __global__ void __launch_bounds__(256) k_explicit_2d(const double* __restrict__ 
 // layer below).  z contraction per column in registers; y and x contractions per plane in
 // shared memory.
 template <int P, int EX, int EY, int EZ>
-__global__ void __launch_bounds__(256) k_explicit_3d(const double* __restrict__ U, const double* Pv, double* out,
-                                                     const uint8_t* __restrict__ nt, ExpP e, int* flag) {
+__global__ void __launch_bounds__(256) k_explicit_3d_v1(const double* __restrict__ U, const double* Pv, double* out,
+                                                        const uint8_t* __restrict__ nt, ExpP e, int* flag) {
   constexpr int RX = EX * P + P + 1, RY = EY * P + P + 1, TY = EY * P + 1;
   constexpr int NCOL = (RX * RY + 255) / 256;
   extern __shared__ double smem[];
@@ -225,6 +225,8 @@ __global__ void __launch_bounds__(256) k_explicit_3d(const double* __restrict__ 
     __syncthreads();
   }
 }
+
+#include "explicit3d.cuh"
 
 // ------------------------------------------------------------------ irregular d nodes
 __device__ __forceinline__ double ft_at(const double* ft, long long nt_, const long long* step, int off) {
@@ -416,15 +418,15 @@ void launch_explicit_p(sc_ctx* c, const double* U, const double* Pv, double* out
     k_explicit_2d<P, E2, E2><<<grid, 256, 0, c->stream>>>(U, Pv, out, c->d_ntype, e, c->d_flag);
   } else {
     if constexpr (P <= 6) {
-      constexpr int RX = EX3 * P + P + 1, RY = EY3 * P + P + 1, TY = EY3 * P + 1;
-      const size_t smem = sizeof(double) * (2 * (P + 1) * RY * RX + 2 * (P + 1) * TY * RX);
+      using T = Tile3<P>;
+      auto kern = k_explicit_3d<P, T::E, T::E, T::EZ, T::NT>;
       static bool attr = false;
       if (!attr) {
-        cudaFuncSetAttribute(k_explicit_3d<P, EX3, EY3, EZ3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::smem);
         attr = true;
       }
-      dim3 grid((g.N[0] + EX3 - 1) / EX3, (g.N[1] + EY3 - 1) / EY3, (g.N[2] + EZ3 - 1) / EZ3);
-      k_explicit_3d<P, EX3, EY3, EZ3><<<grid, 256, smem, c->stream>>>(U, Pv, out, c->d_ntype, e, c->d_flag);
+      dim3 grid((g.N[0] + T::E - 1) / T::E, (g.N[1] + T::E - 1) / T::E, (g.N[2] + T::EZ - 1) / T::EZ);
+      kern<<<grid, T::NT, T::smem, c->stream>>>(U, Pv, out, c->d_ntype, e, c->d_flag);
     }
   }
 }
