@@ -490,28 +490,41 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   std::vector<int> sn_of(nc);
   for (int s = 0; s < nsn; ++s)
     for (int j = 0; j < b.sn[s].w; ++j) sn_of[b.sn[s].c0 + j] = s;
-  for (int s = 0; s < nsn; ++s) {  // creation order is a postorder
-    SNode& S = b.sn[s];
-    const int last = S.c0 + S.w - 1;
-    std::vector<int> R;
-    for (int v : S.cols) {  // canonical ids
-      for (int q = b.node_eptr[v]; q < b.node_eptr[v + 1]; ++q) {
-        const int e = b.node_eidx[q] / nb;
-        for (int loc = 0; loc < nb; ++loc) {
-          int j = b.celem_cidx[(size_t)e * nb + loc];
-          if (j > last) R.push_back(j);
+  // supernodes of each component form a contiguous postorder range; components are
+  // independent, so the symbolic and numeric phases run one component per OpenMP task
+  std::vector<std::vector<int>> comp_sn(comps.size());
+  for (int s = 0; s < nsn; ++s) comp_sn[b.sn[s].comp].push_back(s);
+#pragma omp parallel
+  {
+    std::vector<int> stamp(std::max(ne, 1), -1);   // element already scanned for supernode s
+#pragma omp for schedule(dynamic, 1)
+    for (int k = 0; k < (int)comps.size(); ++k) {
+      for (int s : comp_sn[k]) {  // postorder: children first
+        SNode& S = b.sn[s];
+        const int last = S.c0 + S.w - 1;
+        std::vector<int> R;
+        for (int v : S.cols) {  // canonical ids
+          for (int q = b.node_eptr[v]; q < b.node_eptr[v + 1]; ++q) {
+            const int e = b.node_eidx[q] / nb;
+            if (stamp[e] == s) continue;
+            stamp[e] = s;
+            for (int loc = 0; loc < nb; ++loc) {
+              int j = b.celem_cidx[(size_t)e * nb + loc];
+              if (j > last) R.push_back(j);
+            }
+          }
         }
+        for (int ch : S.children)
+          for (int j : b.sn[ch].R)
+            if (j > last) R.push_back(j);
+        std::sort(R.begin(), R.end());
+        R.erase(std::unique(R.begin(), R.end()), R.end());
+        S.R = std::move(R);
+        int h = 0;
+        for (int ch : S.children) h = std::max(h, b.sn[ch].height + 1);
+        S.height = h;
       }
     }
-    for (int ch : S.children)
-      for (int j : b.sn[ch].R)
-        if (j > last) R.push_back(j);
-    std::sort(R.begin(), R.end());
-    R.erase(std::unique(R.begin(), R.end()), R.end());
-    S.R = std::move(R);
-    int h = 0;
-    for (int ch : S.children) h = std::max(h, b.sn[ch].height + 1);
-    S.height = h;
   }
   // ---------------- numeric multifrontal factorisation of S and M^cc
   const double beta_dt2 = 0.25 * c->dt * c->dt;
@@ -544,9 +557,6 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   }
   c->nnz_factor = linv_off[nsn] + lr_off[nsn];
   std::vector<double> hLinvS(linv_off[nsn]), hLRS(lr_off[nsn]), hLinvM(linv_off[nsn]), hLRM(lr_off[nsn]);
-  // supernodes grouped by component, in postorder
-  std::vector<std::vector<int>> comp_sn(comps.size());
-  for (int s = 0; s < nsn; ++s) comp_sn[b.sn[s].comp].push_back(s);
   int fail_comp = -1, fail_row = -1, fail_which = 0;
   const double* Kref = c->Kref.data();
   const double* Mref = c->Mref.data();

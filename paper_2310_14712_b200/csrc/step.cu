@@ -72,7 +72,7 @@ __global__ void k_explicit_1d(const double* __restrict__ U, const double* Pv, do
 
 // ------------------------------------------------------------------ 2D
 template <int P, int EX, int EY>
-__global__ void __launch_bounds__(256) k_explicit_2d(const double* __restrict__ U, const double* Pv,
+__global__ void __launch_bounds__(256) k_explicit_2d_v1(const double* __restrict__ U, const double* Pv,
                                                      double* out, const uint8_t* __restrict__ nt, ExpP e,
                                                      int* flag) {
   constexpr int RX = EX * P + P + 1, RY = EY * P + P + 1, TY = EY * P + 1;
@@ -226,6 +226,7 @@ __global__ void __launch_bounds__(256) k_explicit_3d_v1(const double* __restrict
   }
 }
 
+#include "explicit2d.cuh"
 #include "explicit3d.cuh"
 
 // ------------------------------------------------------------------ irregular d nodes
@@ -413,13 +414,14 @@ void launch_explicit_p(sc_ctx* c, const double* U, const double* Pv, double* out
     k_explicit_1d<P><<<(unsigned)((g.nl[0] + 255) / 256), 256, 0, c->stream>>>(U, Pv, out, c->d_ntype, e,
                                                                                 c->d_flag);
   } else if (g.dim == 2) {
-    constexpr int E2 = Tile2<P>::E;
+    constexpr int E2 = Tile2v<P>::E;
     dim3 grid((g.N[0] + E2 - 1) / E2, (g.N[1] + E2 - 1) / E2);
-    k_explicit_2d<P, E2, E2><<<grid, 256, 0, c->stream>>>(U, Pv, out, c->d_ntype, e, c->d_flag);
+    k_explicit_2d<P, E2, E2, Tile2v<P>::NT><<<grid, Tile2v<P>::NT, 0, c->stream>>>(U, Pv, out, c->d_ntype, e,
+                                                                                   c->d_flag);
   } else {
     if constexpr (P <= 6) {
       using T = Tile3<P>;
-      auto kern = k_explicit_3d<P, T::E, T::E, T::EZ, T::NT>;
+      auto kern = k_explicit_3d<P, T::E, T::E, T::EZ, T::NT, T::MINB>;
       static bool attr = false;
       if (!attr) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::smem);
