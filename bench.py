@@ -211,6 +211,15 @@ def main():
     torch.cuda.synchronize()
     t_exp = e0.elapsed_time(e1) / nprof
     ach = info["bytes_explicit_per_step"] / (t_exp / 1e3) / 1e9
+    breakdown = {"explicit_ms": t_exp}
+    for which, name in ((1, "celem_ms"), (2, "solve_ms")):
+        if info["n_c"] > 0:
+            with torch.cuda.stream(stream):
+                e0.record(stream)
+                s.profile(which, 20)
+                e1.record(stream)
+            torch.cuda.synchronize()
+            breakdown[name] = e0.elapsed_time(e1) / 20
     roof = {"kernel": "k_explicit (a1)+(a2) fused", "bound": "hbm", "achieved": ach, "peak": peak,
             "unit": "GB/s", "frac": ach / peak, "traffic": None, "peak_kind": peak_kind,
             "kernel_ms": t_exp, "share_of_step": t_exp / (t_ms / K),
@@ -250,8 +259,13 @@ def main():
                 "dtype": "f64", "data": "synthetic",
                 "config": _config_dict(cfg, n_dof, {"n_c": info["n_c"], "n_d": info["n_d"],
                                                      "cells_cut": info["cells_cut"], "l2": l2,
+                                                     "n_components": info["n_components"],
+                                                     "n_supernodes": info["n_supernodes"],
+                                                     "nnz_factor": info["nnz_factor"],
+                                                     "factor_height": info["factor_height"],
+                                                     "kernels_per_step": info["kernels_per_step"],
                                                      "parallelism": f"{world} independent replicas"}),
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+                "roofline": roof, "breakdown_ms": breakdown, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
                 "gpu_launches": int(info["kernels_per_step"]) * K,
                 "step_bytes_algorithmic": info["bytes_per_step"],
                 "step_achieved_GBps": info["bytes_per_step"] / (t_ms / K / 1e3) / 1e9,

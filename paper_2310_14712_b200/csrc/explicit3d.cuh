@@ -5,15 +5,21 @@
 // s2 Mx My Kz u.  Each 1D operator is applied element by element ((P+1) outputs from (P+1)
 // inputs held in registers) and assembled at element-boundary nodes: z by a register carry
 // across element layers, y through shared memory (boundary contributions kept apart and
-// added when read), x by a warp shuffle between neighbouring elements.
+// added when read), x by a warp shuffle between neighbouring x elements.
 //
 // CTA: xy tile of EX x EY elements (+1 halo element on the low side of each axis, whose
 // only output is its contribution to the tile's first boundary node), streaming along z
-// over EZ element layers (+1 warm-up layer that only produces the z carry).  Each layer
-// ((P+1) lattice planes of the region) is staged into shared memory with cp.async
-// (zero-fill outside the grid), double buffered: layer ez+1 is in flight while layer ez is
-// computed.  Per plane: z-contract -> SA, SB | barrier | y pass -> BM, BT (+BMP, BTP) |
-// barrier | x pass + CDM update.
+// over EZ element layers (+1 warm-up layer that only produces the z carry).
+//  * each layer ((P+1) lattice planes of the region) is staged into shared memory with
+//    cp.async (zero fill outside the grid), double buffered (layer ez+1 in flight while
+//    layer ez is computed);
+//  * z and y contractions are thread-local: a "column item" (x, y-element) holds its
+//    (P+1) x (P+1) block of u in registers and produces the y-element's outputs for every
+//    plane; results go to BM/BT (double-buffered per plane parity);
+//  * one barrier per plane, then the x pass: a "row item" (row, x-element) contracts in x,
+//    assembles the shared node with shfl_up and applies the CDM update; u_{n-1} and the node
+//    type of the NEXT plane are prefetched into registers;
+//  * the lumped-mass division uses precomputed reciprocal GLL weights.
 #pragma once
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
@@ -26,6 +32,13 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// reciprocal of the assembled 1D GLL weight of lattice node i
+__device__ __forceinline__ double inv_wt(int i, int e_cnt, int P) {
+  const int l = i % P, e = i / P;
+  if (l) return c_iw[l];
+  return (e > 0 && e < e_cnt) ? c_iw2 : c_iw[0];
+}
+
 template <int P, int EX, int EY, int EZ, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_explicit_3d(const double* __restrict__ U, const double* Pv,
                                                           double* out, const uint8_t* __restrict__ nt, ExpP e,
@@ -34,18 +47,18 @@ __global__ void __launch_bounds__(NT, MINB) k_explicit_3d(const double* __restri
   constexpr int EXH = EX + 1, EYH = EY + 1;
   constexpr int RX = EXH * P + 1, RY = EYH * P + 1, TY = EY * P + 1;
   constexpr int RC = RX * RY;                     // region columns
-  constexpr int NCOL = (RC + NT - 1) / NT;
-  constexpr int NYI = (RX * EYH + NT - 1) / NT;   // y-pass items per thread
+  constexpr int NYI = (RX * EYH + NT - 1) / NT;   // column items per thread
   constexpr int RPW = 32 / EXH;                   // x-pass rows per warp
+  constexpr int NW = NT / 32;
+  constexpr int NXI = (TY + NW * RPW - 1) / (NW * RPW);   // row-item rounds per warp
   extern __shared__ double smem[];
-  double* LU = smem;                 // [2][P1][RY][RX] staged layers
-  double* SA = LU + 2 * P1 * RC;     // [RY][RX]  Mz u (plane)
-  double* SB = SA + RC;              // [RY][RX]  Kz u
-  double* BM = SB + RC;              // [TY][RX]  My Mz u (l < P contributions)
-  double* BT = BM + TY * RX;         // [TY][RX]  s1 Ky Mz u + s2 My Kz u
-  double* BMP = BT + TY * RX;        // [EYH][RX] l = P contributions (boundary rows)
-  double* BTP = BMP + EYH * RX;
+  double* LU = smem;                   // [2][P1][RY][RX] staged layers
+  double* BMb = LU + 2 * P1 * RC;      // [2][TY][RX]  My Mz u (l < P contributions)
+  double* BTb = BMb + 2 * TY * RX;     // [2][TY][RX]  s1 Ky Mz u + s2 My Kz u
+  double* BMPb = BTb + 2 * TY * RX;    // [2][EYH][RX] l = P contributions (boundary rows)
+  double* BTPb = BMPb + 2 * EYH * RX;
   const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
   const int Nx = e.N[0], Ny = e.N[1], Nz = e.N[2];
   const int nx = e.nl[0], ny = e.nl[1];
   const size_t pl = (size_t)nx * ny;
@@ -57,6 +70,7 @@ __global__ void __launch_bounds__(NT, MINB) k_explicit_3d(const double* __restri
   const int y0 = ey0 * P;
   const int OY = nEY * P + (ey1 == Ny ? 1 : 0);
   const bool lastx = (ex1 == Nx);
+  const int rin = lane / EXH, exl = lane % EXH;
 
   auto issue = [&](int ez, int buf) {
     double* dst = LU + buf * P1 * RC;
@@ -71,11 +85,35 @@ __global__ void __launch_bounds__(NT, MINB) k_explicit_3d(const double* __restri
     cp_async_commit();
   };
 
-  double ca[NCOL], cb[NCOL];
+  // row-item prefetch of u_{n-1} and node types for one plane
+  double pv[NXI][P1];
+  uint8_t ntv[NXI][P1];
+  auto prefetch = [&](int gz) {
 #pragma unroll
-  for (int c = 0; c < NCOL; ++c) ca[c] = cb[c] = 0.0;
+    for (int q = 0; q < NXI; ++q) {
+      const int oy = (warp + q * NW) * RPW + rin;
+      const bool act = rin < RPW && oy < OY && exl > 0 && exl <= nEX;
+      const int gy = y0 + oy;
+#pragma unroll
+      for (int l = 0; l < P1; ++l) {
+        const int gx = (ex0 - 1 + exl) * P + l;
+        const bool ok = act && (l < P || (exl == nEX && lastx)) && gz < e.nl[2];
+        const size_t g = gx + (size_t)nx * gy + pl * gz;
+        ntv[q][l] = ok ? __ldg(nt + g) : (uint8_t)0;
+        pv[q][l] = ok ? Pv[g] : 0.0;
+      }
+    }
+  };
+
+  double ca[NYI][P1], cb[NYI][P1];   // z carries of the column items' P+1 rows
+#pragma unroll
+  for (int q = 0; q < NYI; ++q)
+#pragma unroll
+    for (int j = 0; j < P1; ++j) ca[q][j] = cb[q][j] = 0.0;
   const int ezs = max(ez0 - 1, 0);
   issue(ezs, 0);
+  int pp = 0;  // plane parity (BM/BT double buffer)
+  prefetch(ez0 * P);
   for (int ez = ezs; ez < ez1; ++ez) {
     const int buf = (ez - ezs) & 1;
     if (ez + 1 < ez1) {
@@ -86,139 +124,145 @@ __global__ void __launch_bounds__(NT, MINB) k_explicit_3d(const double* __restri
     }
     __syncthreads();
     const double* L = LU + buf * P1 * RC;
-    double u[NCOL][P1];
+    const bool warm = ez < ez0;
+    const bool top = (ez == Nz - 1);
+    const int np = warm ? 0 : (top ? P1 : P);
+    // column items: (x, y-element) blocks of u in registers: u[q][row j][plane m]
+    double u[NYI][P1][P1];
 #pragma unroll
-    for (int c = 0; c < NCOL; ++c) {
-      const int col = tid + c * NT;
+    for (int q = 0; q < NYI; ++q) {
+      const int it = tid + q * NT;
+      const int ix = it % RX, eyl = it / RX;
+      const bool ok = it < RX * EYH;
 #pragma unroll
-      for (int k = 0; k < P1; ++k) u[c][k] = col < RC ? L[k * RC + col] : 0.0;
+      for (int j = 0; j < P1; ++j)
+#pragma unroll
+        for (int m = 0; m < P1; ++m) u[q][j][m] = ok ? L[m * RC + (eyl * P + j) * RX + ix] : 0.0;
     }
-    if (ez >= ez0) {
-      const bool top = (ez == Nz - 1);
-      const int np = top ? P1 : P;
-      for (int k = 0; k < np; ++k) {
-        // ---- z contraction for plane k -> SA, SB
+    for (int k = 0; k < np; ++k) {
+      double* BM = BMb + pp * TY * RX;
+      double* BT = BTb + pp * TY * RX;
+      double* BMP = BMPb + pp * EYH * RX;
+      double* BTP = BTPb + pp * EYH * RX;
+      // ---- z then y contraction (thread-local)
 #pragma unroll
-        for (int c = 0; c < NCOL; ++c) {
-          const int col = tid + c * NT;
-          if (col < RC) {
-            double a = k == 0 ? ca[c] : 0.0, b = k == 0 ? cb[c] : 0.0;
+      for (int q = 0; q < NYI; ++q) {
+        const int it = tid + q * NT;
+        const int ix = it % RX, eyl = it / RX;
+        if (it < RX * EYH && eyl <= nEY && (eyl > 0 || ey0 > 0)) {
+          double sa[P1], sb[P1];
+#pragma unroll
+          for (int j = 0; j < P1; ++j) {
+            double a = k == 0 ? ca[q][j] : 0.0, b = k == 0 ? cb[q][j] : 0.0;
 #pragma unroll
             for (int m = 0; m < P1; ++m) {
-              a += c_Mh[k * P1 + m] * u[c][m];
-              b += c_Kh[k * P1 + m] * u[c][m];
+              a += c_Mh[k * P1 + m] * u[q][j][m];
+              b += c_Kh[k * P1 + m] * u[q][j][m];
             }
-            SA[col] = a;
-            SB[col] = b;
+            sa[j] = a;
+            sb[j] = b;
           }
-        }
-        __syncthreads();
-        // ---- y pass (element-local); l = P outputs go to BMP/BTP
 #pragma unroll
-        for (int q = 0; q < NYI; ++q) {
-          const int it = tid + q * NT;
-          const int ix = it % RX, eyl = it / RX;
-          if (it < RX * EYH && eyl <= nEY && (eyl > 0 || ey0 > 0)) {
-            double sa[P1], sb[P1];
+          for (int l = 0; l < P1; ++l) {
+            double m = 0.0, tk = 0.0, tm = 0.0;
 #pragma unroll
             for (int j = 0; j < P1; ++j) {
-              sa[j] = SA[(eyl * P + j) * RX + ix];
-              sb[j] = SB[(eyl * P + j) * RX + ix];
+              m += c_Mh[l * P1 + j] * sa[j];
+              tk += c_Kh[l * P1 + j] * sa[j];
+              tm += c_Mh[l * P1 + j] * sb[j];
             }
-#pragma unroll
-            for (int l = 0; l < P1; ++l) {
-              double m = 0.0, tk = 0.0, tm = 0.0;
-#pragma unroll
-              for (int j = 0; j < P1; ++j) {
-                m += c_Mh[l * P1 + j] * sa[j];
-                tk += c_Kh[l * P1 + j] * sa[j];
-                tm += c_Mh[l * P1 + j] * sb[j];
+            const double t = e.s[1] * tk + e.s[2] * tm;
+            if (l < P) {
+              if (eyl > 0) {
+                BM[((eyl - 1) * P + l) * RX + ix] = m;
+                BT[((eyl - 1) * P + l) * RX + ix] = t;
               }
-              const double t = e.s[1] * tk + e.s[2] * tm;
-              if (l < P) {
-                if (eyl > 0) {
-                  BM[((eyl - 1) * P + l) * RX + ix] = m;
-                  BT[((eyl - 1) * P + l) * RX + ix] = t;
-                }
-              } else {
-                BMP[eyl * RX + ix] = m;
-                BTP[eyl * RX + ix] = t;
-              }
+            } else {
+              BMP[eyl * RX + ix] = m;
+              BTP[eyl * RX + ix] = t;
             }
           }
         }
-        __syncthreads();
-        // ---- x pass: lane = (row, element); boundary nodes assembled by shfl_up
-        const int warp = tid >> 5, lane = tid & 31;
-        const int rin = lane / EXH, exl = lane % EXH;
-        const int gz = ez * P + k;
-        const double* Lk = L + k * RC;
-        for (int rb = warp * RPW; rb < OY; rb += (NT / 32) * RPW) {
-          const int oy = rb + rin;
-          const bool act = rin < RPW && oy < OY && exl <= nEX && (exl > 0 || ex0 > 0);
-          const int q = oy / P;
-          const bool brow = (oy - q * P) == 0;
-          const bool hasA = oy < nEY * P;              // written by an element above (l < P)
-          const bool hasP = brow && (q > 0 || ey0 > 0);  // l = P contribution of element q
-          double r[P1];
+      }
+      __syncthreads();
+      // ---- x pass + CDM update
+      const int gz = ez * P + k;
+      const double* Lk = L + k * RC;
+      double pvc[NXI][P1];
+      uint8_t ntc[NXI][P1];
 #pragma unroll
-          for (int l = 0; l < P1; ++l) r[l] = 0.0;
-          if (act) {
-            double bm[P1], bt[P1];
+      for (int q = 0; q < NXI; ++q)
+#pragma unroll
+        for (int l = 0; l < P1; ++l) {
+          pvc[q][l] = pv[q][l];
+          ntc[q][l] = ntv[q][l];
+        }
+      prefetch(k + 1 < np ? gz + 1 : (ez + 1) * P);   // next plane (next layer's plane 0)
+      const double iwz = inv_wt(gz, Nz, P);
+#pragma unroll
+      for (int q = 0; q < NXI; ++q) {
+        const int oy = (warp + q * NW) * RPW + rin;
+        const bool act = rin < RPW && oy < OY && exl <= nEX && (exl > 0 || ex0 > 0);
+        const int qq = oy / P;
+        const bool hasA = oy < nEY * P;
+        const bool hasP = (oy - qq * P) == 0 && (qq > 0 || ey0 > 0);
+        double r[P1];
+#pragma unroll
+        for (int l = 0; l < P1; ++l) r[l] = 0.0;
+        if (act) {
+          double bm[P1], bt[P1];
+#pragma unroll
+          for (int j = 0; j < P1; ++j) {
+            const int cidx = exl * P + j;
+            bm[j] = (hasA ? BM[oy * RX + cidx] : 0.0) + (hasP ? BMP[qq * RX + cidx] : 0.0);
+            bt[j] = (hasA ? BT[oy * RX + cidx] : 0.0) + (hasP ? BTP[qq * RX + cidx] : 0.0);
+          }
+#pragma unroll
+          for (int l = 0; l < P1; ++l) {
+            double kx = 0.0, mx = 0.0;
 #pragma unroll
             for (int j = 0; j < P1; ++j) {
-              const int cidx = exl * P + j;
-              bm[j] = (hasA ? BM[oy * RX + cidx] : 0.0) + (hasP ? BMP[q * RX + cidx] : 0.0);
-              bt[j] = (hasA ? BT[oy * RX + cidx] : 0.0) + (hasP ? BTP[q * RX + cidx] : 0.0);
+              kx += c_Kh[l * P1 + j] * bm[j];
+              mx += c_Mh[l * P1 + j] * bt[j];
             }
-#pragma unroll
-            for (int l = 0; l < P1; ++l) {
-              double kx = 0.0, mx = 0.0;
-#pragma unroll
-              for (int j = 0; j < P1; ++j) {
-                kx += c_Kh[l * P1 + j] * bm[j];
-                mx += c_Mh[l * P1 + j] * bt[j];
-              }
-              r[l] = e.s[0] * kx + mx;
-            }
+            r[l] = e.s[0] * kx + mx;
           }
-          const double left = __shfl_up_sync(0xffffffffu, r[P], 1);
-          if (act && exl > 0) {
-            const int gy = y0 + oy;
-            const double wyz = wt(gy, Ny, P) * wt(gz, Nz, P);
-            const int nl = (exl == nEX && lastx) ? P1 : P;
+        }
+        const double left = __shfl_up_sync(0xffffffffu, r[P], 1);
+        if (act && exl > 0) {
+          const int gy = y0 + oy;
+          const double cyz = e.coefR * inv_wt(gy, Ny, P) * iwz;
 #pragma unroll
-            for (int l = 0; l < P1; ++l) {
-              if (l < nl) {
-                const int gx = (ex0 - 1 + exl) * P + l;
-                double rr = r[l];
-                if (l == 0 && (exl > 1 || ex0 > 0)) rr += left;
-                const size_t g = gx + (size_t)nx * gy + pl * gz;
-                if (nt[g] == 1) {
-                  const double uu = Lk[(oy + P) * RX + exl * P + l];
-                  const double res = e.a1 * uu + e.a2 * Pv[g] - e.coefR * rr / (wt(gx, Nx, P) * wyz);
-                  out[g] = res;
-                  if (!isfinite(res)) atomicExch(flag, 1);
-                }
-              }
+          for (int l = 0; l < P1; ++l) {
+            if (ntc[q][l] == 1) {
+              const int gx = (ex0 - 1 + exl) * P + l;
+              double rr = r[l];
+              if (l == 0 && (exl > 1 || ex0 > 0)) rr += left;
+              const size_t g = gx + (size_t)nx * gy + pl * gz;
+              const double uu = Lk[(oy + P) * RX + exl * P + l];
+              const double res = e.a1 * uu + e.a2 * pvc[q][l] - cyz * inv_wt(gx, Nx, P) * rr;
+              out[g] = res;
+              if (!isfinite(res)) atomicExch(flag, 1);
             }
           }
         }
-        __syncthreads();
       }
+      pp ^= 1;
     }
-    // ---- z carry for the next layer's bottom plane
+    // ---- z carries for the next layer's bottom plane
 #pragma unroll
-    for (int c = 0; c < NCOL; ++c) {
-      double a = 0.0, b = 0.0;
+    for (int q = 0; q < NYI; ++q)
 #pragma unroll
-      for (int m = 0; m < P1; ++m) {
-        a += c_Mh[P * P1 + m] * u[c][m];
-        b += c_Kh[P * P1 + m] * u[c][m];
+      for (int j = 0; j < P1; ++j) {
+        double a = 0.0, b = 0.0;
+#pragma unroll
+        for (int m = 0; m < P1; ++m) {
+          a += c_Mh[P * P1 + m] * u[q][j][m];
+          b += c_Kh[P * P1 + m] * u[q][j][m];
+        }
+        ca[q][j] = a;
+        cb[q][j] = b;
       }
-      ca[c] = a;
-      cb[c] = b;
-    }
     __syncthreads();  // all reads of this layer's buffer done before it is refilled
   }
 }
@@ -228,8 +272,9 @@ struct Tile3 {
   static constexpr int E = P <= 2 ? 8 : (P == 3 ? 7 : (P == 4 ? 5 : 3));
   static constexpr int EZ = 8;
   static constexpr int NT = 256;
-  static constexpr int MINB = P <= 4 ? 3 : 1;
+  static constexpr int MINB = P <= 4 ? 2 : 1;
   static constexpr int RX = (E + 1) * P + 1;
   static constexpr int TY = E * P + 1;
-  static constexpr size_t smem = sizeof(double) * (2 * (P + 1) * RX * RX + 2 * RX * RX + 2 * TY * RX + 2 * (E + 1) * RX);
+  static constexpr size_t smem =
+      sizeof(double) * (2 * (P + 1) * RX * RX + 4 * TY * RX + 4 * (E + 1) * RX);
 };

@@ -18,6 +18,8 @@
 __constant__ double c_Mh[SC_MAXP1 * SC_MAXP1];
 __constant__ double c_Kh[SC_MAXP1 * SC_MAXP1];
 __constant__ double c_w[SC_MAXP1];
+__constant__ double c_iw[SC_MAXP1];   // 1 / w_l
+__constant__ double c_iw2;            // 1 / (2 w_0): interior element-boundary node
 
 struct ExpP {
   int nl[3];
@@ -533,6 +535,11 @@ void device_upload_reference(sc_ctx* c) {
   SC_CUDA(cudaMemcpyToSymbol(c_Mh, M.data(), sizeof(double) * M.size()));
   SC_CUDA(cudaMemcpyToSymbol(c_Kh, K.data(), sizeof(double) * K.size()));
   SC_CUDA(cudaMemcpyToSymbol(c_w, w.data(), sizeof(double) * w.size()));
+  std::vector<double> iw(SC_MAXP1, 0.0);
+  for (int i = 0; i < n1; ++i) iw[i] = 1.0 / c->gll_w[i];
+  const double iw2 = 1.0 / (c->gll_w[0] + c->gll_w[c->g.p]);
+  SC_CUDA(cudaMemcpyToSymbol(c_iw, iw.data(), sizeof(double) * iw.size()));
+  SC_CUDA(cudaMemcpyToSymbol(c_iw2, &iw2, sizeof(double)));
   SC_CUDA(cudaMalloc(&c->d_Kref, sizeof(double) * c->Kref.size()));
   SC_CUDA(cudaMemcpy(c->d_Kref, c->Kref.data(), sizeof(double) * c->Kref.size(), cudaMemcpyHostToDevice));
 }
