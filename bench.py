@@ -253,7 +253,8 @@ def main():
         except Exception as ex:  # report, do not fail the bench
             cpu = {"value": None, "unit": UNIT, "cores": _cores(), "kind": "oracle", "sample": f"failed: {ex}"}
     if rank == 0:
-        l2 = "inputs larger than L2" if 16.0 * info["lattice_nodes"] > 126e6 else "L2-resident (no flush)"
+        l2 = ("per-step working set larger than L2 (no flush)" if info["bytes_per_step"] > 126e6
+              else "L2-resident working set (no flush)")
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
                 "ms_per_step": t_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic",

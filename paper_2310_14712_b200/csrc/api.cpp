@@ -26,7 +26,8 @@ static void free_ctx(sc_ctx* c) {
                   c->d_celem_cell, c->d_celem_kidx, c->d_celem_cidx, c->d_Kcut, c->d_Y, c->d_rhs_ptr,
                   c->d_rhs_idx, c->d_sn_c0, c->d_sn_w, c->d_sn_r, c->d_sn_linv, c->d_sn_lr, c->d_sn_roff,
                   c->d_sn_uoff, c->d_sn_goff, c->d_R, c->d_gptr, c->d_gidx, c->d_items, c->fS.Linv, c->fS.LR,
-                  c->fM.Linv, c->fM.LR, c->fS.d, c->fM.d, c->d_tmp, c->d_nitem, c->d_chptr, c->d_chidx, c->d_parent, c->d_solve_cnt};
+                  c->fM.Linv, c->fM.LR, c->fS.d, c->fM.d, c->d_tmp, c->d_nitem, c->d_chptr, c->d_chidx, c->d_parent, c->d_solve_cnt,
+                  c->d_part};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);

@@ -674,27 +674,39 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   // persistent-solve work list in topological order (solve.cu):
   //  forward, heights ascending:  fA items (32 rows of L_ss^{-1}) then fB items (32 rows of L_R)
   //  backward, heights descending: bA items (8 columns) then bB items (8 outputs)
-  std::vector<int32_t> items;  // int4 (type, s, start, 0)
-  std::vector<int32_t> nitem(4 * (size_t)nsn, 0);
+  // tiles (solve.cu): 32-wide output blocks x 256-long reduction tiles; per tile two int4:
+  // (type, s, block, tile) (ntiles, partial slot, ticket counter, first col/row of tile)
+  const int TILE = 256;
+  std::vector<int32_t> items;
+  std::vector<int32_t> nblk(4 * (size_t)nsn, 0);
   std::vector<std::vector<int>> by_h(c->height);
   for (int s = 0; s < nsn; ++s) by_h[b.sn[s].height].push_back(s);
-  auto push = [&](int type, int s, int start) {
-    items.insert(items.end(), {type, s, start, 0});
-    ++nitem[(size_t)type * nsn + s];
+  int64_t pslot = 0;
+  int n_bctr = 0;
+  // one 32-block of phase `type` of supernode s whose reduction range is [r0, r1)
+  auto block = [&](int type, int s, int blk, int r0, int r1) {
+    const int ntb = std::max(1, (r1 - r0 + TILE - 1) / TILE);
+    for (int t = 0; t < ntb; ++t)
+      items.insert(items.end(), {type, s, blk, t, ntb, (int32_t)pslot, n_bctr, r0 + t * TILE});
+    if (pslot + (int64_t)ntb * 32 > INT32_MAX) throw ScError(SC_ERR_CONFIG, "solve partial buffer too large");
+    pslot += (int64_t)ntb * 32;
+    ++n_bctr;
+    ++nblk[(size_t)type * nsn + s];
   };
   for (int h = 0; h < c->height; ++h) {
-    for (int s : by_h[h])
-      for (int i = 0; i < wv[s]; i += 32) push(0, s, i);
-    for (int s : by_h[h])
-      for (int i = 0; i < rv[s]; i += 32) push(1, s, i);
+    for (int s : by_h[h])  // fA: rows of L_ss^{-1}; columns 0 .. block end (lower triangle)
+      for (int rb = 0; rb * 32 < wv[s]; ++rb) block(0, s, rb, 0, std::min(wv[s], rb * 32 + 32));
+    for (int s : by_h[h])  // fB: rows of L_R; all w columns
+      for (int rb = 0; rb * 32 < rv[s]; ++rb) block(1, s, rb, 0, wv[s]);
   }
   for (int h = c->height - 1; h >= 0; --h) {
-    for (int s : by_h[h])
-      for (int i = 0; i < wv[s]; i += 8) push(2, s, i);
-    for (int s : by_h[h])
-      for (int i = 0; i < wv[s]; i += 8) push(3, s, i);
+    for (int s : by_h[h])  // bA: columns of L_R; all r rows
+      for (int cb = 0; cb * 32 < wv[s]; ++cb) block(2, s, cb, 0, rv[s]);
+    for (int s : by_h[h])  // bB: columns i of L_ss^{-1}; rows j >= block start
+      for (int ob = 0; ob * 32 < wv[s]; ++ob) block(3, s, ob, ob * 32, wv[s]);
   }
-  c->n_items = (int)(items.size() / 4);
+  c->n_items = (int)(items.size() / 8);
+  c->n_counters = 4 * (size_t)nsn + n_bctr + 1;
   std::vector<int32_t> chptr(nsn + 1, 0), chidx, parent(nsn, -1);
   for (int s = 0; s < nsn; ++s) {
     for (int ch : b.sn[s].children) chidx.push_back(ch);
@@ -725,11 +737,12 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   up32(&c->d_gptr, gptr);
   up32(&c->d_gidx, gidx);
   up32(&c->d_items, items);
-  up32(&c->d_nitem, nitem);
+  up32(&c->d_nitem, nblk);
+  SC_CUDA(cudaMalloc(&c->d_part, sizeof(double) * std::max<int64_t>(1, pslot)));
   up32(&c->d_chptr, chptr);
   up32(&c->d_chidx, chidx);
   up32(&c->d_parent, parent);
-  SC_CUDA(cudaMalloc(&c->d_solve_cnt, sizeof(int) * (4 * (size_t)nsn + 1)));
+  SC_CUDA(cudaMalloc(&c->d_solve_cnt, sizeof(int) * c->n_counters));
   upd_(&c->fS.Linv, hLinvS);
   upd_(&c->fS.LR, hLRS);
   upd_(&c->fM.Linv, hLinvM);
@@ -789,7 +802,8 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   sd.R = c->d_R;
   sd.linv_off = c->d_sn_linv;
   sd.lr_off = c->d_sn_lr;
-  sd.nitem = c->d_nitem;
+  sd.nblk = c->d_nitem;
+  sd.part = c->d_part;
   sd.chptr = c->d_chptr;
   sd.chidx = c->d_chidx;
   sd.parent = c->d_parent;
@@ -799,7 +813,8 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   sd.x = c->d_x;
   sd.z = c->d_z;
   sd.cnt = c->d_solve_cnt;
-  sd.head = c->d_solve_cnt + 4 * (size_t)nsn;
+  sd.bcnt = c->d_solve_cnt + 4 * (size_t)nsn;
+  sd.head = c->d_solve_cnt + c->n_counters - 1;
   c->Kcut_host.clear();
   c->Kcut_host.shrink_to_fit();
   c->Mcut_host.clear();

@@ -32,15 +32,17 @@ struct GridP {
 
 // device view of the supernodal factor structure + persistent-solve work list (solve.cu)
 struct SolveDev {
-  const int4* items;           // (type, supernode, start, 0) in topological order
+  const int4* items;           // 2 x int4 per tile: (type, s, block, tile) (ntiles, pslot, bctr, lo)
   int n_items, n_sn;
   const int32_t *w, *r, *c0, *goff, *gptr, *gidx, *uoff, *roff, *R;
   const int64_t *linv_off, *lr_off;
-  const int32_t *nitem;        // [4][n_sn] item counts per phase
+  const int32_t *nblk;         // [4][n_sn] 32-blocks per phase
   const int32_t *chptr, *chidx, *parent;
   const double *Linv, *LR;
   double *U, *b, *y, *x, *z;
-  int* cnt;                    // [4][n_sn] completed items per phase
+  double* part;                // tile partial sums
+  int* cnt;                    // [4][n_sn] completed blocks per phase
+  int* bcnt;                   // per block: tiles done (ticket)
   int* head;                   // dequeue counter
 };
 
@@ -114,8 +116,10 @@ struct sc_ctx {
   int32_t *d_gptr = nullptr, *d_gidx = nullptr;
   int32_t* d_items = nullptr;         // int4 work items
   int32_t *d_nitem = nullptr, *d_chptr = nullptr, *d_chidx = nullptr, *d_parent = nullptr;
-  int* d_solve_cnt = nullptr;         // [4*n_sn] counters + head
+  int* d_solve_cnt = nullptr;         // [4*n_sn] phase counters, [n_bctr] tickets, head
+  double* d_part = nullptr;           // tile partials
   int n_items = 0, solve_grid = 0;
+  size_t n_counters = 0;
   SolveDev solve_dev{};
   Factor fS, fM;
   int64_t nnz_factor = 0;

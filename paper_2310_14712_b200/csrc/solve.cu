@@ -1,144 +1,174 @@
 // (a5) implicit cut-DOF solve S a^c_{n+1} = r^c with the factor computed once at setup
 // ("triangular matrix system with the factorized system
-// matrix S" each step).
+// matrix S" each step).  The factor is of the Jacobi-scaled matrix D S D (factor.cpp).
 //
-// One persistent kernel performs both sweeps.  Work items (supernode s, row/column chunk)
-// are stored in a topological order (forward: by supernode height, phase A before B;
-// backward: by height descending, phase A before B).  CTAs dequeue items from a global
-// counter; an item spins until the counters of the items it depends on are complete.
-// Every dependency points to an EARLIER item, and an item is only dequeued by a running
-// CTA, so all producers are resident: no deadlock without a cooperative launch.
-// Producer: writes results, __threadfence, atomicAdd(counter).  Consumer: spins on the
-// counter, __threadfence, reads produced data with ld.global.cg (bypassing L1).
+// One persistent kernel performs both sweeps.  Every supernode GEMV is cut into tiles
+// (forward: 32 rows x 256 columns, backward: 32 outputs x 256 rows); a tile writes its 32
+// partial sums to a private slot, and the LAST tile of each 32-wide block (atomic ticket)
+// sums the block's partials in fixed tile order -> deterministic results.  Tiles are stored
+// in a topological order (forward by supernode height, backward by height descending);
+// CTAs dequeue them from a global counter and spin until the phase counters they depend
+// on are complete.  Every dependency points to an EARLIER tile and tiles are only dequeued
+// by running CTAs, so all producers are resident: no deadlock, no cooperative launch.
+// Producer: partials / results, __threadfence, atomicAdd.  Consumer: spin, __threadfence,
+// reads of produced data with ld.global.cg (L1 bypass).
 //
-// Forward (multifrontal, deterministic):  fA: y_s = L_ss^{-1} (b_s - sum child updates)
-//                                         fB: U_s = sum child updates + L_{R_s,s} y_s
-// Backward:                               bA: z_s = y_s - L_{R_s,s}^T x[R_s]
-//                                         bB: x_s = L_ss^{-T} z_s
+// Phases per supernode s (w columns, r rows below, c0 first column):
+//  fA: y_s = L_ss^{-1} (b_s - child updates)            tiles over (row block, column tile)
+//  fB: U_s = child updates + L_{R,s} y_s                  tiles over (row block, column tile)
+//  bA: z_s = y_s - L_{R,s}^T x[R_s]                       tiles over (column block, row tile)
+//  bB: x_s = L_ss^{-T} z_s                                tiles over (output block, row tile)
 #include "sc_internal.h"
 
 namespace {
 
 enum { IT_FA = 0, IT_FB = 1, IT_BA = 2, IT_BB = 3 };
+constexpr int TILE = 256;  // columns (forward) / rows (backward) per tile
 
 __device__ __forceinline__ void wait_ge(const int* p, int target) {
   if (target <= 0) return;
-  while (atomicAdd((int*)p, 0) < target) __nanosleep(32);
+  while (atomicAdd((int*)p, 0) < target) __nanosleep(20);
 }
 
 __global__ void __launch_bounds__(256) k_solve(SolveDev a) {
-  extern __shared__ double sh[];  // [max_w]
+  __shared__ double vs[TILE];
   __shared__ double part[8][33];
-  __shared__ int s_item;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ int s_item, s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   while (true) {
-    if (threadIdx.x == 0) s_item = atomicAdd(a.head, 1);
+    if (tid == 0) s_item = atomicAdd(a.head, 1);
     __syncthreads();
     const int it = s_item;
     if (it >= a.n_items) return;
-    const int4 d = a.items[it];
-    const int type = d.x, s = d.y, st = d.z;
+    const int4 d0 = a.items[2 * it], d1 = a.items[2 * it + 1];
+    const int type = d0.x, s = d0.y, blk = d0.z, t = d0.w;   // blk: 32-block, t: tile in block
+    const int ntb = d1.x, pslot = d1.y, bctr = d1.z, lo = d1.w;  // lo: first column/row of tile
     const int w = a.w[s], r = a.r[s], c0 = a.c0[s];
-    // ---- wait for dependencies
-    if (threadIdx.x == 0) {
+    const int n_sn = a.n_sn;
+    // ---- dependencies
+    if (tid == 0) {
       if (type == IT_FA) {
         for (int q = a.chptr[s]; q < a.chptr[s + 1]; ++q) {
           const int c = a.chidx[q];
-          wait_ge(a.cnt + 1 * a.n_sn + c, a.nitem[1 * a.n_sn + c]);
+          wait_ge(a.cnt + 1 * n_sn + c, a.nblk[1 * n_sn + c]);
         }
       } else if (type == IT_FB) {
-        wait_ge(a.cnt + 0 * a.n_sn + s, a.nitem[0 * a.n_sn + s]);
+        wait_ge(a.cnt + 0 * n_sn + s, a.nblk[0 * n_sn + s]);
       } else if (type == IT_BA) {
         const int p = a.parent[s];
-        if (p >= 0) wait_ge(a.cnt + 3 * a.n_sn + p, a.nitem[3 * a.n_sn + p]);
-        // y_s of the forward sweep is complete once all fB items were dequeued and done:
-        wait_ge(a.cnt + 1 * a.n_sn + s, a.nitem[1 * a.n_sn + s]);
-        wait_ge(a.cnt + 0 * a.n_sn + s, a.nitem[0 * a.n_sn + s]);
+        if (p >= 0) wait_ge(a.cnt + 3 * n_sn + p, a.nblk[3 * n_sn + p]);
+        wait_ge(a.cnt + 0 * n_sn + s, a.nblk[0 * n_sn + s]);
       } else {
-        wait_ge(a.cnt + 2 * a.n_sn + s, a.nitem[2 * a.n_sn + s]);
+        wait_ge(a.cnt + 2 * n_sn + s, a.nblk[2 * n_sn + s]);
       }
       __threadfence();
     }
     __syncthreads();
-    if (type == IT_FA) {
+    double* P = a.part + pslot;   // this block's partials: [ntb][32]
+    if (type == IT_FA || type == IT_FB) {
+      // ---- row-oriented tile: rows blk*32 + lane, columns [lo, hi)
+      const int nrows = (type == IT_FA) ? w : r;
+      const int hi = (type == IT_FA) ? min(min(w, blk * 32 + 32), lo + TILE) : min(w, lo + TILE);
+      const int ncols = hi - lo;
       const int go = a.goff[s];
-      for (int t = threadIdx.x; t < w; t += blockDim.x) {
-        double f = a.b[c0 + t];
-        for (int q = a.gptr[go + t]; q < a.gptr[go + t + 1]; ++q) f -= __ldcg(a.U + a.gidx[q]);
-        sh[t] = f;
-      }
-      __syncthreads();
-      const int i = st + lane;
-      const int jmax = min(w, st + 32);
-      const double* L = a.Linv + a.linv_off[s];
-      double acc0 = 0.0, acc1 = 0.0;
-      if (i < w) {
-        int j = warp;
-        for (; j + 8 < jmax; j += 16) {
-          acc0 += L[i + (size_t)j * w] * sh[j];
-          acc1 += L[i + (size_t)(j + 8) * w] * sh[j + 8];
+      for (int j = tid; j < ncols; j += 256) {
+        double v;
+        if (type == IT_FA) {
+          v = a.b[c0 + lo + j];
+          for (int q = a.gptr[go + lo + j]; q < a.gptr[go + lo + j + 1]; ++q) v -= __ldcg(a.U + a.gidx[q]);
+        } else {
+          v = __ldcg(a.y + c0 + lo + j);
         }
-        if (j < jmax) acc0 += L[i + (size_t)j * w] * sh[j];
+        vs[j] = v;
       }
-      part[warp][lane] = acc0 + acc1;
       __syncthreads();
-      if (warp == 0 && i < w) {
-        double t = 0.0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) t += part[k][lane];
-        a.y[c0 + i] = t;
-      }
-    } else if (type == IT_FB) {
-      for (int t = threadIdx.x; t < w; t += blockDim.x) sh[t] = __ldcg(a.y + c0 + t);
-      __syncthreads();
-      const int i = st + lane;
-      const double* L = a.LR + a.lr_off[s];
-      double acc0 = 0.0, acc1 = 0.0;
-      if (i < r) {
-        int j = warp;
-        for (; j + 8 < w; j += 16) {
-          acc0 += L[i + (size_t)j * r] * sh[j];
-          acc1 += L[i + (size_t)(j + 8) * r] * sh[j + 8];
+      const int i = blk * 32 + lane;
+      const int ld = nrows;
+      const double* A = (type == IT_FA ? a.Linv + a.linv_off[s] : a.LR + a.lr_off[s]) + (size_t)lo * ld;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      if (i < nrows) {
+        // warp covers columns warp*32 .. warp*32+31 of the tile
+        const int j0 = warp * 32, j1 = min(ncols, j0 + 32);
+        int j = j0;
+        for (; j + 4 <= j1; j += 4) {
+          const double x0 = A[i + (size_t)(j + 0) * ld], x1 = A[i + (size_t)(j + 1) * ld];
+          const double x2 = A[i + (size_t)(j + 2) * ld], x3 = A[i + (size_t)(j + 3) * ld];
+          acc[0] += x0 * vs[j + 0];
+          acc[1] += x1 * vs[j + 1];
+          acc[2] += x2 * vs[j + 2];
+          acc[3] += x3 * vs[j + 3];
         }
-        if (j < w) acc0 += L[i + (size_t)j * r] * sh[j];
+        for (; j < j1; ++j) acc[0] += A[i + (size_t)j * ld] * vs[j];
       }
-      part[warp][lane] = acc0 + acc1;
+      part[warp][lane] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
       __syncthreads();
-      if (warp == 0 && i < r) {
-        double t = 0.0;
+      if (warp == 0) {
+        double v = 0.0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) t += part[k][lane];
-        const int go = a.goff[s];
-        for (int q = a.gptr[go + w + i]; q < a.gptr[go + w + i + 1]; ++q) t += __ldcg(a.U + a.gidx[q]);
-        a.U[a.uoff[s] + i] = t;
-      }
-    } else if (type == IT_BA) {
-      const int j = st + warp;
-      if (j < w) {
-        const double* L = a.LR + a.lr_off[s] + (size_t)j * r;
-        const int32_t* R = a.R + a.roff[s];
-        double acc = 0.0;
-        for (int i = lane; i < r; i += 32) acc += L[i] * __ldcg(a.x + R[i]);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) a.z[c0 + j] = __ldcg(a.y + c0 + j) - acc;
+        for (int k = 0; k < 8; ++k) v += part[k][lane];
+        P[t * 32 + lane] = v;
       }
     } else {
-      const int i = st + warp;
-      if (i < w) {
-        const double* L = a.Linv + a.linv_off[s] + (size_t)i * w;
-        double acc = 0.0;
-        for (int j = i + lane; j < w; j += 32) acc += L[j] * __ldcg(a.z + c0 + j);
+      // ---- column-oriented tile: outputs (columns) blk*32 + o, rows [lo, hi)
+      const int o0 = blk * 32;
+      const int hi = (type == IT_BA) ? min(r, lo + TILE) : min(w, lo + TILE);
+      const int nr = hi - lo;
+      for (int j = tid; j < nr; j += 256)
+        vs[j] = (type == IT_BA) ? __ldcg(a.x + a.R[a.roff[s] + lo + j]) : __ldcg(a.z + c0 + lo + j);
+      __syncthreads();
+      const int ld = (type == IT_BA) ? r : w;
+      const double* A = (type == IT_BA ? a.LR + a.lr_off[s] : a.Linv + a.linv_off[s]);
+      // warp handles 4 output columns; lanes stride rows
 #pragma unroll
-        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) a.x[c0 + i] = acc;
+      for (int cc = 0; cc < 4; ++cc) {
+        const int col = o0 + warp * 4 + cc;
+        double v = 0.0;
+        if (col < w) {
+          const double* Ac = A + (size_t)col * ld + lo;
+          double v0 = 0.0, v1 = 0.0;
+          int q = lane;
+          for (; q + 32 < nr; q += 64) {
+            v0 += Ac[q] * vs[q];
+            v1 += Ac[q + 32] * vs[q + 32];
+          }
+          if (q < nr) v0 += Ac[q] * vs[q];
+          v = v0 + v1;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) P[t * 32 + warp * 4 + cc] = v;
       }
     }
+    // ---- last tile of the block reduces the partials in tile order
+    __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (tid == 0) s_last = (atomicAdd(a.bcnt + bctr, 1) == ntb - 1);
+    __syncthreads();
+    if (s_last) {
       __threadfence();
-      atomicAdd(a.cnt + type * a.n_sn + s, 1);
+      if (tid < 32) {
+        const int o = blk * 32 + tid;
+        double v = 0.0;
+        for (int k = 0; k < ntb; ++k) v += __ldcg(P + k * 32 + tid);
+        if (type == IT_FA) {
+          if (o < w) a.y[c0 + o] = v;
+        } else if (type == IT_FB) {
+          if (o < r) {
+            const int go = a.goff[s];
+            for (int q = a.gptr[go + w + o]; q < a.gptr[go + w + o + 1]; ++q) v += __ldcg(a.U + a.gidx[q]);
+            a.U[a.uoff[s] + o] = v;
+          }
+        } else if (type == IT_BA) {
+          if (o < w) a.z[c0 + o] = __ldcg(a.y + c0 + o) - v;
+        } else {
+          if (o < w) a.x[c0 + o] = v;
+        }
+      }
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) atomicAdd(a.cnt + type * n_sn + s, 1);
     }
+    __syncthreads();
   }
 }
 
@@ -149,20 +179,14 @@ void launch_solve(sc_ctx* c, const Factor& f) {
   SolveDev a = c->solve_dev;
   a.Linv = f.Linv;
   a.LR = f.LR;
-  SC_CUDA(cudaMemsetAsync(c->d_solve_cnt, 0, sizeof(int) * (4 * (size_t)c->n_sn + 1), c->stream));
-  const size_t smem = sizeof(double) * std::max(1, c->max_w);
-  static int attr_set = 0;
-  if (!attr_set) {
-    SC_CUDA(cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(48 * 1024)));
-    attr_set = 1;
-  }
+  SC_CUDA(cudaMemsetAsync(c->d_solve_cnt, 0, sizeof(int) * c->n_counters, c->stream));
   if (c->solve_grid == 0) {
     int per_sm = 0, sms = 0, dev = 0;
     SC_CUDA(cudaGetDevice(&dev));
     SC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve, 256, smem));
+    SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve, 256, 0));
     c->solve_grid = std::max(1, std::min(c->n_items, per_sm * sms));
   }
-  k_solve<<<c->solve_grid, 256, smem, c->stream>>>(a);
+  k_solve<<<c->solve_grid, 256, 0, c->stream>>>(a);
   SC_CUDA(cudaGetLastError());
 }
