@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(NT) k_explicit_2d(const double* __restrict__ U
     const double left = __shfl_up_sync(0xffffffffu, r[P], 1);
     if (act && exl > 0) {
       const int gy = y0 + oy;
-      const double wy = wt(gy, Ny, P);
+      const double cy = e.coefR * inv_wt(gy, Ny, P);
       const int nl = (exl == nEX && lastx) ? P1 : P;
 #pragma unroll
       for (int l = 0; l < P1; ++l) {
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(NT) k_explicit_2d(const double* __restrict__ U
           const size_t g = gx + (size_t)nx * gy;
           if (nt[g] == 1) {
             const double uu = SU[(oy + P) * RX + exl * P + l];
-            const double res = e.a1 * uu + e.a2 * Pv[g] - e.coefR * rr / (wt(gx, Nx, P) * wy);
+            const double res = e.a1 * uu + e.a2 * Pv[g] - cy * inv_wt(gx, Nx, P) * rr;
             out[g] = res;
             if (!isfinite(res)) atomicExch(flag, 1);
           }

@@ -139,7 +139,9 @@ __global__ void __launch_bounds__(NT, MINB) k_explicit_3d(const double* __restri
 #pragma unroll
         for (int m = 0; m < P1; ++m) u[q][j][m] = ok ? L[m * RC + (eyl * P + j) * RX + ix] : 0.0;
     }
-    for (int k = 0; k < np; ++k) {
+#pragma unroll
+    for (int k = 0; k < P1; ++k) {
+      if (k >= np) break;
       double* BM = BMb + pp * TY * RX;
       double* BT = BTb + pp * TY * RX;
       double* BMP = BMPb + pp * EYH * RX;

@@ -693,17 +693,34 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
     ++n_bctr;
     ++nblk[(size_t)type * nsn + s];
   };
+  auto fused = [&](int s) {
+    return wv[s] <= FUSE_W && rv[s] <= FUSE_R && (int64_t)wv[s] * (wv[s] + rv[s]) <= FUSE_ENTRIES;
+  };
+  auto fused_item = [&](int type, int s) {  // one CTA does both phases of the sweep
+    items.insert(items.end(), {type, s, 0, 0, 1, 0, 0, 0});
+    const int p0 = type == 4 ? 0 : 2;
+    nblk[(size_t)p0 * nsn + s] = 1;
+    nblk[(size_t)(p0 + 1) * nsn + s] = 1;
+  };
   for (int h = 0; h < c->height; ++h) {
+    for (int s : by_h[h])
+      if (fused(s)) fused_item(4, s);
     for (int s : by_h[h])  // fA: rows of L_ss^{-1}; columns 0 .. block end (lower triangle)
-      for (int rb = 0; rb * 32 < wv[s]; ++rb) block(0, s, rb, 0, std::min(wv[s], rb * 32 + 32));
+      if (!fused(s))
+        for (int rb = 0; rb * 32 < wv[s]; ++rb) block(0, s, rb, 0, std::min(wv[s], rb * 32 + 32));
     for (int s : by_h[h])  // fB: rows of L_R; all w columns
-      for (int rb = 0; rb * 32 < rv[s]; ++rb) block(1, s, rb, 0, wv[s]);
+      if (!fused(s))
+        for (int rb = 0; rb * 32 < rv[s]; ++rb) block(1, s, rb, 0, wv[s]);
   }
   for (int h = c->height - 1; h >= 0; --h) {
+    for (int s : by_h[h])
+      if (fused(s)) fused_item(5, s);
     for (int s : by_h[h])  // bA: columns of L_R; all r rows
-      for (int cb = 0; cb * 32 < wv[s]; ++cb) block(2, s, cb, 0, rv[s]);
+      if (!fused(s))
+        for (int cb = 0; cb * 32 < wv[s]; ++cb) block(2, s, cb, 0, rv[s]);
     for (int s : by_h[h])  // bB: columns i of L_ss^{-1}; rows j >= block start
-      for (int ob = 0; ob * 32 < wv[s]; ++ob) block(3, s, ob, ob * 32, wv[s]);
+      if (!fused(s))
+        for (int ob = 0; ob * 32 < wv[s]; ++ob) block(3, s, ob, ob * 32, wv[s]);
   }
   c->n_items = (int)(items.size() / 8);
   c->n_counters = 4 * (size_t)nsn + n_bctr + 1;

@@ -10,6 +10,11 @@
 
 #define SC_MAXP1 9            // p <= 8
 #define SC_MAX_VOIDS 4096
+// supernodes with w <= FUSE_W, r <= FUSE_R and (w*w + r*w) <= FUSE_ENTRIES are solved by a
+// single CTA per sweep (solve.cu); larger ones are tiled
+#define FUSE_W 128
+#define FUSE_R 1024
+#define FUSE_ENTRIES 16384
 
 // ---------------------------------------------------------------- device-side data
 struct DVoid {

@@ -22,17 +22,57 @@
 
 namespace {
 
-enum { IT_FA = 0, IT_FB = 1, IT_BA = 2, IT_BB = 3 };
+enum { IT_FA = 0, IT_FB = 1, IT_BA = 2, IT_BB = 3, IT_FF = 4, IT_BF = 5 };
 constexpr int TILE = 256;  // columns (forward) / rows (backward) per tile
 
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// poll with plain acquire loads (no RMW traffic on the L2 atomic units) and backoff
 __device__ __forceinline__ void wait_ge(const int* p, int target) {
   if (target <= 0) return;
-  while (atomicAdd((int*)p, 0) < target) __nanosleep(20);
+  unsigned ns = 32;
+  while (ld_acquire(p) < target) {
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+  }
+}
+
+// y[0..nr) = A[0..nr, 0..nc) v  (A column-major, leading dimension ld; v, y in smem).
+// lanes = rows of a 32-row block, warps split the columns, partials reduced via smem.
+__device__ __forceinline__ void cta_gemv_rows(const double* A, int ld, int nr, int nc, const double* v, double* y,
+                                              double (*part)[33]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int rb = 0; rb < nr; rb += 32) {
+    const int i = rb + lane;
+    double a0 = 0.0, a1 = 0.0;
+    if (i < nr) {
+      int j = warp;
+      for (; j + 8 < nc; j += 16) {
+        a0 += A[i + (size_t)j * ld] * v[j];
+        a1 += A[i + (size_t)(j + 8) * ld] * v[j + 8];
+      }
+      if (j < nc) a0 += A[i + (size_t)j * ld] * v[j];
+    }
+    part[warp][lane] = a0 + a1;
+    __syncthreads();
+    if (warp == 0 && i < nr) {
+      double t = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t += part[k][lane];
+      y[i] = t;
+    }
+    __syncthreads();
+  }
 }
 
 __global__ void __launch_bounds__(256) k_solve(SolveDev a) {
   __shared__ double vs[TILE];
   __shared__ double part[8][33];
+  __shared__ double fv[FUSE_W], fy[FUSE_W], fu[FUSE_R];   // fused small-supernode phases
   __shared__ int s_item, s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   while (true) {
@@ -47,14 +87,14 @@ __global__ void __launch_bounds__(256) k_solve(SolveDev a) {
     const int n_sn = a.n_sn;
     // ---- dependencies
     if (tid == 0) {
-      if (type == IT_FA) {
+      if (type == IT_FA || type == IT_FF) {
         for (int q = a.chptr[s]; q < a.chptr[s + 1]; ++q) {
           const int c = a.chidx[q];
           wait_ge(a.cnt + 1 * n_sn + c, a.nblk[1 * n_sn + c]);
         }
       } else if (type == IT_FB) {
         wait_ge(a.cnt + 0 * n_sn + s, a.nblk[0 * n_sn + s]);
-      } else if (type == IT_BA) {
+      } else if (type == IT_BA || type == IT_BF) {
         const int p = a.parent[s];
         if (p >= 0) wait_ge(a.cnt + 3 * n_sn + p, a.nblk[3 * n_sn + p]);
         wait_ge(a.cnt + 0 * n_sn + s, a.nblk[0 * n_sn + s]);
@@ -64,6 +104,62 @@ __global__ void __launch_bounds__(256) k_solve(SolveDev a) {
       __threadfence();
     }
     __syncthreads();
+    if (type == IT_FF) {
+      // ---- fused forward phase of a small supernode (one CTA)
+      const int go = a.goff[s];
+      for (int j = tid; j < w; j += 256) {
+        double v = a.b[c0 + j];
+        for (int q = a.gptr[go + j]; q < a.gptr[go + j + 1]; ++q) v -= __ldcg(a.U + a.gidx[q]);
+        fv[j] = v;
+      }
+      __syncthreads();
+      cta_gemv_rows(a.Linv + a.linv_off[s], w, w, w, fv, fy, part);
+      for (int j = tid; j < w; j += 256) a.y[c0 + j] = fy[j];
+      if (r > 0) {
+        cta_gemv_rows(a.LR + a.lr_off[s], r, r, w, fy, fu, part);
+        for (int i = tid; i < r; i += 256) {
+          double v = fu[i];
+          for (int q = a.gptr[go + w + i]; q < a.gptr[go + w + i + 1]; ++q) v += __ldcg(a.U + a.gidx[q]);
+          a.U[a.uoff[s] + i] = v;
+        }
+      }
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) {
+        atomicAdd(a.cnt + 0 * n_sn + s, 1);
+        atomicAdd(a.cnt + 1 * n_sn + s, 1);
+      }
+      continue;
+    }
+    if (type == IT_BF) {
+      // ---- fused backward phase of a small supernode (one CTA)
+      for (int i = tid; i < r; i += 256) fu[i] = __ldcg(a.x + a.R[a.roff[s] + i]);
+      __syncthreads();
+      const double* LR = a.LR + a.lr_off[s];
+      for (int j = warp; j < w; j += 8) {
+        double v = 0.0;
+        for (int i = lane; i < r; i += 32) v += LR[i + (size_t)j * r] * fu[i];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) fv[j] = __ldcg(a.y + c0 + j) - v;
+      }
+      __syncthreads();
+      const double* Li = a.Linv + a.linv_off[s];
+      for (int i = warp; i < w; i += 8) {
+        double v = 0.0;
+        for (int j = i + lane; j < w; j += 32) v += Li[j + (size_t)i * w] * fv[j];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) a.x[c0 + i] = v;
+      }
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) {
+        atomicAdd(a.cnt + 2 * n_sn + s, 1);
+        atomicAdd(a.cnt + 3 * n_sn + s, 1);
+      }
+      continue;
+    }
     double* P = a.part + pslot;   // this block's partials: [ntb][32]
     if (type == IT_FA || type == IT_FB) {
       // ---- row-oriented tile: rows blk*32 + lane, columns [lo, hi)

@@ -228,8 +228,8 @@ __global__ void __launch_bounds__(256) k_explicit_3d_v1(const double* __restrict
   }
 }
 
-#include "explicit2d.cuh"
 #include "explicit3d.cuh"
+#include "explicit2d.cuh"
 
 // ------------------------------------------------------------------ irregular d nodes
 __device__ __forceinline__ double ft_at(const double* ft, long long nt_, const long long* step, int off) {
