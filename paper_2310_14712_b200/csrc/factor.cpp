@@ -18,6 +18,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <numeric>
@@ -723,6 +725,18 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
         for (int ob = 0; ob * 32 < wv[s]; ++ob) block(3, s, ob, ob * 32, wv[s]);
   }
   c->n_items = (int)(items.size() / 8);
+  if (getenv("SC_DEBUG")) {
+    int64_t nf = 0, ef = 0, nt = 0, et = 0, maxw = 0, maxr = 0;
+    for (int s = 0; s < nsn; ++s) {
+      const int64_t ent = (int64_t)wv[s] * (wv[s] + rv[s]);
+      if (fused(s)) { ++nf; ef += ent; } else { ++nt; et += ent; }
+      maxw = std::max<int64_t>(maxw, wv[s]);
+      maxr = std::max<int64_t>(maxr, rv[s]);
+    }
+    fprintf(stderr, "[sc] supernodes %d (fused %lld, %.3g entries; tiled %lld, %.3g entries) max w %lld max r %lld "
+            "height %d items %d components %lld\n", nsn, (long long)nf, (double)ef, (long long)nt, (double)et,
+            (long long)maxw, (long long)maxr, c->height, c->n_items, (long long)c->n_components);
+  }
   c->n_counters = 4 * (size_t)nsn + n_bctr + 1;
   std::vector<int32_t> chptr(nsn + 1, 0), chidx, parent(nsn, -1);
   for (int s = 0; s < nsn; ++s) {

@@ -34,7 +34,15 @@ torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / steps
 s.sync()
 u = s.read()
+prof = {}
+for which, name in ((0, "explicit_ms"), (1, "celem_ms"), (2, "solve_ms")):
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        s.profile(which, 10)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    prof[name] = e0.elapsed_time(e1) / 10
 out = {"config": cid, "setup_s": setup, "ms_per_step": ms, "dof_steps_per_s": info["n_dof"] / (ms / 1e3),
-       "u_norm": float(np.linalg.norm(u)), "mem_alloc_GB": torch.cuda.mem_get_info()}
+       "u_norm": float(np.linalg.norm(u)), "mem_free_total": torch.cuda.mem_get_info(), "breakdown_ms": prof}
 out.update({k: info[k] for k in info})
 print(json.dumps(out, default=str))
