@@ -41,32 +41,50 @@ __device__ __forceinline__ void wait_ge(const int* p, int target) {
   }
 }
 
-// y[0..nr) = A[0..nr, 0..nc) v  (A column-major, leading dimension ld; v, y in smem).
-// lanes = rows of a 32-row block, warps split the columns, partials reduced via smem.
-__device__ __forceinline__ void cta_gemv_rows(const double* A, int ld, int nr, int nc, const double* v, double* y,
-                                              double (*part)[33]) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int rb = 0; rb < nr; rb += 32) {
-    const int i = rb + lane;
-    double a0 = 0.0, a1 = 0.0;
-    if (i < nr) {
-      int j = warp;
-      for (; j + 8 < nc; j += 16) {
-        a0 += A[i + (size_t)j * ld] * v[j];
-        a1 += A[i + (size_t)(j + 8) * ld] * v[j + 8];
-      }
-      if (j < nc) a0 += A[i + (size_t)j * ld] * v[j];
-    }
-    part[warp][lane] = a0 + a1;
-    __syncthreads();
-    if (warp == 0 && i < nr) {
-      double t = 0.0;
+// sum_{j in [j0, j1) step js} A[i + j ld] v[j] for one row per lane, 8 loads in flight
+__device__ __forceinline__ double row_dot(const double* A, size_t ld, int i, bool ok, int j0, int j1, int js,
+                                          const double* v) {
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  if (ok) {
+    int j = j0;
+    for (; j + 7 * js < j1; j += 8 * js) {
+      double x[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) t += part[k][lane];
-      y[i] = t;
+      for (int k = 0; k < 8; ++k) x[k] = A[i + (size_t)(j + k * js) * ld];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k & 3] += x[k] * v[j + k * js];
     }
-    __syncthreads();
+    for (; j < j1; j += js) acc[0] += A[i + (size_t)j * ld] * v[j];
   }
+  return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+
+// sum_{q in [q0, q1) step 32} Ac[q] v[q] by one lane (column dot product, 8 loads in flight)
+__device__ __forceinline__ double col_dot(const double* Ac, int q0, int q1, const double* v) {
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  int q = q0;
+  for (; q + 7 * 32 < q1; q += 256) {
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = Ac[q + 32 * k];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k & 3] += x[k] * v[q + 32 * k];
+  }
+  for (; q < q1; q += 32) acc[0] += Ac[q] * v[q];
+  return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+
+// y[0..nr) = A[0..nr, 0..nc) v  (A column-major, leading dimension ld; v, y in smem):
+// each warp owns whole 32-row blocks (no cross-warp reduction, no barrier inside).
+__device__ __forceinline__ void cta_gemv_rows(const double* A, int ld, int nr, int nc, const double* v, double* y,
+                                              double (*)[33]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int rb = warp * 32; rb < nr; rb += 256) {
+    const int i = rb + lane;
+    const double t = row_dot(A, ld, i, i < nr, 0, nc, 1, v);
+    if (i < nr) y[i] = t;
+  }
+  __syncthreads();
 }
 
 __global__ void __launch_bounds__(256) k_solve(SolveDev a) {
@@ -137,8 +155,7 @@ __global__ void __launch_bounds__(256) k_solve(SolveDev a) {
       __syncthreads();
       const double* LR = a.LR + a.lr_off[s];
       for (int j = warp; j < w; j += 8) {
-        double v = 0.0;
-        for (int i = lane; i < r; i += 32) v += LR[i + (size_t)j * r] * fu[i];
+        double v = col_dot(LR + (size_t)j * r, lane, r, fu);
 #pragma unroll
         for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (lane == 0) fv[j] = __ldcg(a.y + c0 + j) - v;
@@ -147,7 +164,7 @@ __global__ void __launch_bounds__(256) k_solve(SolveDev a) {
       const double* Li = a.Linv + a.linv_off[s];
       for (int i = warp; i < w; i += 8) {
         double v = 0.0;
-        for (int j = i + lane; j < w; j += 32) v += Li[j + (size_t)i * w] * fv[j];
+        v = col_dot(Li + (size_t)i * w, i + lane, w, fv);
 #pragma unroll
         for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (lane == 0) a.x[c0 + i] = v;
@@ -181,22 +198,9 @@ __global__ void __launch_bounds__(256) k_solve(SolveDev a) {
       const int i = blk * 32 + lane;
       const int ld = nrows;
       const double* A = (type == IT_FA ? a.Linv + a.linv_off[s] : a.LR + a.lr_off[s]) + (size_t)lo * ld;
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      if (i < nrows) {
-        // warp covers columns warp*32 .. warp*32+31 of the tile
-        const int j0 = warp * 32, j1 = min(ncols, j0 + 32);
-        int j = j0;
-        for (; j + 4 <= j1; j += 4) {
-          const double x0 = A[i + (size_t)(j + 0) * ld], x1 = A[i + (size_t)(j + 1) * ld];
-          const double x2 = A[i + (size_t)(j + 2) * ld], x3 = A[i + (size_t)(j + 3) * ld];
-          acc[0] += x0 * vs[j + 0];
-          acc[1] += x1 * vs[j + 1];
-          acc[2] += x2 * vs[j + 2];
-          acc[3] += x3 * vs[j + 3];
-        }
-        for (; j < j1; ++j) acc[0] += A[i + (size_t)j * ld] * vs[j];
-      }
-      part[warp][lane] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+      // warp covers columns warp*32 .. warp*32+31 of the tile
+      const int j0 = warp * 32, j1 = min(ncols, j0 + 32);
+      part[warp][lane] = row_dot(A, ld, i, i < nrows, j0, j1, 1, vs);
       __syncthreads();
       if (warp == 0) {
         double v = 0.0;
@@ -221,14 +225,7 @@ __global__ void __launch_bounds__(256) k_solve(SolveDev a) {
         double v = 0.0;
         if (col < w) {
           const double* Ac = A + (size_t)col * ld + lo;
-          double v0 = 0.0, v1 = 0.0;
-          int q = lane;
-          for (; q + 32 < nr; q += 64) {
-            v0 += Ac[q] * vs[q];
-            v1 += Ac[q + 32] * vs[q + 32];
-          }
-          if (q < nr) v0 += Ac[q] * vs[q];
-          v = v0 + v1;
+          v = col_dot(Ac, lane, nr, vs);
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -347,9 +347,17 @@ __global__ void k_celem(int mode, const double* __restrict__ A, const double* __
   const int kidx = ekidx[e];
   const double* K = kidx >= 0 ? Kcut + (size_t)kidx * nb * nb : Kref;
   for (int r = i; r < nb; r += tpe) {
-    double s = 0.0;
-    for (int j = 0; j < nb; ++j) s += K[(size_t)j * nb + r] * w[j];
-    Y[(size_t)e * nb + r] = s;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    int j = 0;
+    for (; j + 8 <= nb; j += 8) {   // 8 independent loads in flight (HBM-bound GEMV)
+      double x[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = __ldg(K + (size_t)(j + k) * nb + r);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k & 3] += x[k] * w[j + k];
+    }
+    for (; j < nb; ++j) acc[0] += __ldg(K + (size_t)j * nb + r) * w[j];
+    Y[(size_t)e * nb + r] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
   }
 }
 
