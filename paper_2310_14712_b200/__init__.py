@@ -52,7 +52,8 @@ class sc_info(ctypes.Structure):
                 ("dt", ctypes.c_double), ("dt_crit_uncut", ctypes.c_double), ("step", ctypes.c_int64),
                 ("bytes_per_step", ctypes.c_double), ("bytes_explicit_per_step", ctypes.c_double),
                 ("kernels_per_step", ctypes.c_int32), ("lattice_nodes", ctypes.c_int64),
-                ("setup_seconds", ctypes.c_double)]
+                ("setup_seconds", ctypes.c_double), ("n_near", ctypes.c_int64),
+                ("bytes_solve_per_step", ctypes.c_double), ("bytes_celem_per_step", ctypes.c_double)]
 
 
 EXPORTS = ("sc_setup", "sc_set_state", "sc_step", "sc_sync", "sc_read", "sc_read_c_state", "sc_query",

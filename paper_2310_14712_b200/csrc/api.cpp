@@ -1,6 +1,8 @@
 // C ABI entry points of libsc (include/sc.h).
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "sc_internal.h"
@@ -13,24 +15,49 @@ static sc_status fail(sc_ctx* c, const ScError& e) {
   return e.st;
 }
 
+// SC_TRACE=path: dump the last solve launch's item timeline (debug instrumentation)
+static void dump_trace(sc_ctx* c) {
+  const char* path = getenv("SC_TRACE");
+  if (!path || !c->d_trace || c->n_items == 0) return;
+  std::vector<unsigned long long> t(3 * (size_t)c->n_items);
+  if (cudaMemcpy(t.data(), c->d_trace, sizeof(unsigned long long) * t.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return;
+  FILE* f = fopen(path, "wb");
+  if (!f) return;
+  const int32_t hdr[2] = {c->n_items, c->n_sn};
+  fwrite(hdr, sizeof(int32_t), 2, f);
+  fwrite(c->h_items.data(), sizeof(int32_t), c->h_items.size(), f);
+  fwrite(t.data(), sizeof(unsigned long long), t.size(), f);
+  std::vector<int32_t> wr(3 * (size_t)c->n_sn);
+  cudaMemcpy(wr.data(), c->d_sn_w, sizeof(int32_t) * c->n_sn, cudaMemcpyDeviceToHost);
+  cudaMemcpy(wr.data() + c->n_sn, c->d_sn_r, sizeof(int32_t) * c->n_sn, cudaMemcpyDeviceToHost);
+  cudaMemcpy(wr.data() + 2 * c->n_sn, c->d_parent, sizeof(int32_t) * c->n_sn, cudaMemcpyDeviceToHost);
+  fwrite(wr.data(), sizeof(int32_t), wr.size(), f);
+  fclose(f);
+}
+
 static void free_ctx(sc_ctx* c) {
   if (!c) return;
   int cur = -1;
   cudaGetDevice(&cur);
   cudaSetDevice(c->device);
+  dump_trace(c);
   for (int i = 0; i < 2; ++i)
     if (c->graph[i]) cudaGraphExecDestroy(c->graph[i]);
   void* ptrs[] = {c->d_voids, c->d_u[0], c->d_u[1], c->d_ntype, c->d_cell_class, c->d_dof_lat, c->d_out,
                   c->d_ft, c->d_step, c->d_flag, c->d_irr_lat, c->d_irr_invm, c->d_irr_fx, c->d_Kref,
-                  c->d_c_lat, c->d_vc, c->d_ac, c->d_fxc, c->d_b, c->d_y, c->d_x, c->d_z, c->d_U,
+                  c->d_c_lat, c->d_vc, c->d_ac, c->d_fxc, c->d_b, c->d_q, c->d_x, c->d_U,
                   c->d_celem_cell, c->d_celem_kidx, c->d_celem_cidx, c->d_Kcut, c->d_Y, c->d_rhs_ptr,
-                  c->d_rhs_idx, c->d_sn_c0, c->d_sn_w, c->d_sn_r, c->d_sn_linv, c->d_sn_lr, c->d_sn_roff,
-                  c->d_sn_uoff, c->d_sn_goff, c->d_R, c->d_gptr, c->d_gidx, c->d_items, c->fS.Linv, c->fS.LR,
-                  c->fM.Linv, c->fM.LR, c->fS.d, c->fM.d, c->d_tmp, c->d_nitem, c->d_chptr, c->d_chidx, c->d_parent, c->d_solve_cnt,
-                  c->d_part};
+                  c->d_rhs_idx, c->d_sn_c0, c->d_sn_w, c->d_sn_r, c->d_sn_aoff, c->d_sn_roff,
+                  c->d_sn_uoff, c->d_sn_goff, c->d_R, c->d_gptr, c->d_gidx, c->d_items, c->fS.A,
+                  c->fM.A, c->fS.d, c->fM.d, c->d_tmp, c->d_nitem, c->d_chptr, c->d_chidx, c->d_parent, c->d_solve_cnt,
+                  c->d_part, c->d_trace, c->d_near_tiles, c->d_qmeta};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  if (c->s_hi) cudaStreamDestroy(c->s_hi);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (cur >= 0) cudaSetDevice(cur);
   delete c;
 }
@@ -133,6 +160,7 @@ extern "C" sc_status sc_setup(const sc_grid* grid, int32_t p, double alpha, cons
     device_upload_reference(c);
     setup_device_geometry(c);
     setup_factor(c, {});
+    setup_step_structures(c);
     // state buffers
     const size_t latb = sizeof(double) * c->n_lat;
     SC_CUDA(cudaMalloc(&c->d_u[0], latb));
@@ -148,14 +176,18 @@ extern "C" sc_status sc_setup(const sc_grid* grid, int32_t p, double alpha, cons
     // algorithmic bytes per step
     {
       const double nbd = (double)c->nb;
-      double ex = 24.0 * (double)(c->n_d - c->n_irr);  // tensor-d: read u_n, u_{n-1}; write u_{n+1}
-      double b = ex;
-      b += 24.0 * (double)c->n_irr;
-      b += 8.0 * (double)c->n_cut * nbd * nbd;         // dense cut K_e
-      b += 48.0 * (double)c->n_c;                      // c state read/write (u, v, a)
-      b += 8.0 * (double)c->nnz_factor * 2.0;          // two sweeps... forward reads both, backward both
+      // far tensor-d nodes (the dominant explicit launch): read u_n, u_{n-1}; write u_{n+1}
+      const double ex = 24.0 * (double)(c->n_d - c->n_irr - c->n_near);
+      // c-element products: dense cut K_e once, w gathered and Y written per element node
+      const double ce = 8.0 * (double)c->n_cut * nbd * nbd + 16.0 * (double)c->n_celem * nbd;
+      // solve: forward streams every panel [D_s; G_s], backward G_s again; b, q, x vectors
+      // and the update vectors U (written once, read once)
+      const double so = 8.0 * (double)(c->nnz_factor + c->nnz_G) + 32.0 * (double)c->n_c + 16.0 * (double)c->sum_r;
       c->bytes_explicit = ex;
-      c->bytes_per_step = b;
+      c->bytes_celem = ce;
+      c->bytes_solve = so;
+      c->bytes_per_step = ex + 24.0 * (double)(c->n_near + c->n_irr) + ce + so +
+                          56.0 * (double)c->n_c;   // r^c gather + corrector state (u, v, a, x)
     }
     if (u0 || v0) {
       double *du = nullptr, *dv = nullptr;
@@ -221,6 +253,7 @@ extern "C" sc_status sc_step(sc_ctx* c, int64_t n) {
   }
   try {
     SC_CUDA(cudaSetDevice(c->device));
+    if (n > 0) enqueue_far_prologue(c);
     for (int64_t i = 0; i < n; ++i) {
       SC_CUDA(cudaGraphLaunch(c->graph[c->cur], c->stream));
       c->cur ^= 1;
@@ -310,6 +343,9 @@ extern "C" sc_status sc_query(sc_ctx* c, sc_info* o) {
   o->kernels_per_step = c->kernels_per_step;
   o->lattice_nodes = c->n_lat;
   o->setup_seconds = c->setup_seconds;
+  o->n_near = c->n_near;
+  o->bytes_solve_per_step = c->bytes_solve;
+  o->bytes_celem_per_step = c->bytes_celem;
   return SC_OK;
 }
 
@@ -354,8 +390,8 @@ extern "C" void sc_destroy(sc_ctx* c) { free_ctx(c); }
 
 extern "C" sc_status sc_profile(sc_ctx* c, int32_t which, int64_t n) {
   if (!c) return SC_ERR_STATE;
-  if (which < 0 || which > 2 || n < 0) {
-    c->err = "sc_profile: which in {0,1,2}, n >= 0";
+  if (which < 0 || which > 3 || n < 0) {
+    c->err = "sc_profile: which in {0,1,2,3}, n >= 0";
     return SC_ERR_CONFIG;
   }
   try {

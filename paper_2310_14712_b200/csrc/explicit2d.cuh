@@ -19,7 +19,8 @@ __global__ void __launch_bounds__(NT) k_explicit_2d(const double* __restrict__ U
   const int tid = threadIdx.x;
   const int Nx = e.N[0], Ny = e.N[1];
   const int nx = e.nl[0];
-  const int ex0 = blockIdx.x * EX, ey0 = blockIdx.y * EY;
+  const int3 tb = tile_of(e);
+  const int ex0 = tb.x * EX, ey0 = tb.y * EY;
   const int ex1 = min(ex0 + EX, Nx), ey1 = min(ey0 + EY, Ny);
   const int nEX = ex1 - ex0, nEY = ey1 - ey0;
   const int xr0 = (ex0 - 1) * P, yr0 = (ey0 - 1) * P;
@@ -119,7 +120,7 @@ __global__ void __launch_bounds__(NT) k_explicit_2d(const double* __restrict__ U
           double rr = r[l];
           if (l == 0 && (exl > 1 || ex0 > 0)) rr += left;
           const size_t g = gx + (size_t)nx * gy;
-          if (nt[g] == 1) {
+          if (nt[g] == e.want) {
             const double uu = SU[(oy + P) * RX + exl * P + l];
             const double res = e.a1 * uu + e.a2 * Pv[g] - cy * inv_wt(gx, Nx, P) * rr;
             out[g] = res;

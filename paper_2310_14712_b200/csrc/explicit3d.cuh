@@ -62,7 +62,8 @@ __global__ void __launch_bounds__(NT, MINB) k_explicit_3d(const double* __restri
   const int Nx = e.N[0], Ny = e.N[1], Nz = e.N[2];
   const int nx = e.nl[0], ny = e.nl[1];
   const size_t pl = (size_t)nx * ny;
-  const int ex0 = blockIdx.x * EX, ey0 = blockIdx.y * EY, ez0 = blockIdx.z * EZ;
+  const int3 tb = tile_of(e);
+  const int ex0 = tb.x * EX, ey0 = tb.y * EY, ez0 = tb.z * EZ;
   const int ex1 = min(ex0 + EX, Nx), ey1 = min(ey0 + EY, Ny), ez1 = min(ez0 + EZ, Nz);
   const int nEX = ex1 - ex0, nEY = ey1 - ey0;
   const int xr0 = (ex0 - 1) * P, yr0 = (ey0 - 1) * P;
@@ -236,7 +237,7 @@ __global__ void __launch_bounds__(NT, MINB) k_explicit_3d(const double* __restri
           const double cyz = e.coefR * inv_wt(gy, Ny, P) * iwz;
 #pragma unroll
           for (int l = 0; l < P1; ++l) {
-            if (ntc[q][l] == 1) {
+            if (ntc[q][l] == e.want) {
               const int gx = (ex0 - 1 + exl) * P + l;
               double rr = r[l];
               if (l == 0 && (exl > 1 || ex0 > 0)) rr += left;

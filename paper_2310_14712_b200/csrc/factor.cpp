@@ -148,6 +148,41 @@ void tri_inverse(const double* L, int n, int w, double* X) {
   }
 }
 
+// Stacked device panel of one supernode from its factored front F (n x n, ld n, lower;
+// columns 0..w-1 hold L_ss over L_Rs):  rows [0, w) = D_s = L_ss^{-T} L_ss^{-1} (full),
+// rows [wp, wp + r) = G_s = L_Rs L_ss^{-1}, zero padding rows in between / below, with
+// wp = w rounded up to even and ld = wp + (r rounded up to even) (panel_ld): every column
+// segment the device copies with bulk (TMA) copies is then 16-byte aligned.  Column-major.
+int panel_wp(int w) { return (w + 1) & ~1; }
+int panel_ld(int w, int r) { return panel_wp(w) + ((r + 1) & ~1); }
+
+void make_panel(const double* F, int n, int w, double* P) {
+  const int r = n - w, wp = panel_wp(w), ld = panel_ld(w, r);
+  std::fill(P, P + (size_t)ld * w, 0.0);
+  std::vector<double> X((size_t)w * w);
+  tri_inverse(F, n, w, X.data());   // X = L_ss^{-1}, lower, column-major (ld w)
+  for (int j = 0; j < w; ++j) {
+    const double* xj = X.data() + (size_t)j * w;
+    for (int i = j; i < w; ++i) {
+      const double* xi = X.data() + (size_t)i * w;
+      double s = 0.0;
+      for (int k = i; k < w; ++k) s += xi[k] * xj[k];   // (X^T X)_{ij}, k >= max(i, j) = i
+      P[(size_t)j * ld + i] = s;
+      P[(size_t)i * ld + j] = s;
+    }
+  }
+  for (int j = 0; j < w; ++j) {
+    double* g = P + (size_t)j * ld + wp;
+    const double* xj = X.data() + (size_t)j * w;
+    for (int k = j; k < w; ++k) {
+      const double f = xj[k];
+      if (f == 0.0) continue;
+      const double* lk = F + (size_t)k * n + w;   // column k of L_Rs
+      for (int i = 0; i < r; ++i) g[i] += lk[i] * f;
+    }
+  }
+}
+
 }  // namespace
 
 // Nested dissection of one component (local node ids into b.clat, canonical indices).
@@ -434,6 +469,30 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
     }
     for (int loc = 0; loc < nb; ++loc) b.celem_cidx[(size_t)e * nb + loc] = cidx_of(elem_node(g, ci, loc, n1));
   }
+  // near-d nodes (type 4): tensor-d nodes of uncut c elements, i.e. d nodes whose residual
+  // reads a c value; the step pipeline updates them after the c part (step.cu)
+  c->n_near = 0;
+  for (int e = 0; e < ne; ++e) {
+    if (b.celem_kidx[e] >= 0) continue;   // cut cell: all its nodes are c
+    int64_t ci[3];
+    int64_t t = b.celem_cell[e];
+    for (int k = 0; k < 3; ++k) {
+      if (k < g.dim) {
+        ci[k] = t % g.N[k];
+        t /= g.N[k];
+      } else {
+        ci[k] = 0;
+      }
+    }
+    for (int loc = 0; loc < nb; ++loc) {
+      const int64_t L = elem_node(g, ci, loc, n1);
+      if (c->ntype[L] == 1) {
+        c->ntype[L] = 4;
+        ++c->n_near;
+      }
+    }
+  }
+  if (c->n_near) SC_CUDA(cudaMemcpy(c->d_ntype, c->ntype.data(), c->n_lat, cudaMemcpyHostToDevice));
   // node -> (e, loc) lists, canonical order
   b.node_eptr.assign(nc + 1, 0);
   for (size_t q = 0; q < b.celem_cidx.size(); ++q)
@@ -552,13 +611,18 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
     dS[i] = 1.0 / std::sqrt(dS[i]);
     dM[i] = 1.0 / std::sqrt(dM[i]);
   }
-  std::vector<int64_t> linv_off(nsn + 1, 0), lr_off(nsn + 1, 0);
+  std::vector<int64_t> a_off(nsn + 1, 0);
+  for (int s = 0; s < nsn; ++s)
+    a_off[s + 1] = a_off[s] + (int64_t)b.sn[s].w * panel_ld(b.sn[s].w, (int)b.sn[s].R.size());
+  c->nnz_factor = 0;
+  c->nnz_G = 0;
+  c->sum_r = 0;
   for (int s = 0; s < nsn; ++s) {
-    linv_off[s + 1] = linv_off[s] + (int64_t)b.sn[s].w * b.sn[s].w;
-    lr_off[s + 1] = lr_off[s] + (int64_t)b.sn[s].w * (int64_t)b.sn[s].R.size();
+    c->nnz_factor += (int64_t)b.sn[s].w * (b.sn[s].w + (int64_t)b.sn[s].R.size());
+    c->nnz_G += (int64_t)b.sn[s].w * (int64_t)b.sn[s].R.size();
+    c->sum_r += (int64_t)b.sn[s].R.size();
   }
-  c->nnz_factor = linv_off[nsn] + lr_off[nsn];
-  std::vector<double> hLinvS(linv_off[nsn]), hLRS(lr_off[nsn]), hLinvM(linv_off[nsn]), hLRM(lr_off[nsn]);
+  std::vector<double> hAS(a_off[nsn]), hAM(a_off[nsn]);
   int fail_comp = -1, fail_row = -1, fail_which = 0;
   const double* Kref = c->Kref.data();
   const double* Mref = c->Mref.data();
@@ -616,11 +680,7 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
           }
           break;
         }
-        double* Linv = (which == 0 ? hLinvS.data() : hLinvM.data()) + linv_off[s];
-        double* LR = (which == 0 ? hLRS.data() : hLRM.data()) + lr_off[s];
-        tri_inverse(F.data(), n, w, Linv);
-        for (int j = 0; j < w; ++j)
-          for (int i = 0; i < r; ++i) LR[(size_t)j * r + i] = F[(size_t)j * n + w + i];
+        make_panel(F.data(), n, w, (which == 0 ? hAS.data() : hAM.data()) + a_off[s]);
         std::vector<double> U((size_t)r * r);
         for (int j = 0; j < r; ++j)
           for (int i = j; i < r; ++i) U[(size_t)j * r + i] = F[(size_t)(w + j) * n + w + i];
@@ -638,13 +698,12 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   for (auto& S : b.sn) H = std::max(H, S.height);
   c->height = nsn ? H + 1 : 0;
   std::vector<int32_t> c0(nsn), wv(nsn), rv(nsn), roff(nsn + 1, 0), uoff(nsn + 1, 0), goff(nsn + 1, 0);
-  std::vector<int64_t> li(nsn), lr(nsn);
+  std::vector<int64_t> ao(nsn);
   for (int s = 0; s < nsn; ++s) {
     c0[s] = b.sn[s].c0;
     wv[s] = b.sn[s].w;
     rv[s] = (int)b.sn[s].R.size();
-    li[s] = linv_off[s];
-    lr[s] = lr_off[s];
+    ao[s] = a_off[s];
     roff[s + 1] = roff[s] + rv[s];
     uoff[s + 1] = uoff[s] + rv[s];
     goff[s + 1] = goff[s] + wv[s] + rv[s];
@@ -673,71 +732,108 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
     gptr[t + 1] = gptr[t] + (int32_t)gl[t].size();
     gidx.insert(gidx.end(), gl[t].begin(), gl[t].end());
   }
-  // persistent-solve work list in topological order (solve.cu):
-  //  forward, heights ascending:  fA items (32 rows of L_ss^{-1}) then fB items (32 rows of L_R)
-  //  backward, heights descending: bA items (8 columns) then bB items (8 outputs)
-  // tiles (solve.cu): 32-wide output blocks x 256-long reduction tiles; per tile two int4:
-  // (type, s, block, tile) (ntiles, partial slot, ticket counter, first col/row of tile)
-  const int TILE = 256;
+  // persistent-solve work list (solve.cu).  Items of a phase cover the supernode's panel in
+  // tiles that fill one staging buffer of SOLVE_STAGE doubles:
+  //  forward  F: panel rows [r0, r0 + nr) x columns [c0, c0 + nc); C = min(w, SOLVE_TILE)
+  //              columns per tile, R = 32 * 2^k rows (as many as fit, >= 32)
+  //  backward B: G_s columns [c0, c0 + nc) (nc <= 32) x G_s rows [r0, r0 + nr), rows as
+  //              many as fit (<= SOLVE_BROWS)
+  // A tile group (same rows for F / same columns for B) whose reduction spans ntb > 1 tiles
+  // writes partials (slot pslot, ticket bctr).  Per item 20 int32 (everything the item
+  // needs, one load): (type, s, t, ntb) (pslot, bctr, r0, nr) (col0, nc, dof0, w)
+  // (r, goff, uoff, roff) (aoff lo, aoff hi, ld, wp).
+  const int TILE = SOLVE_TILE;
   std::vector<int32_t> items;
-  std::vector<int32_t> nblk(4 * (size_t)nsn, 0);
+  std::vector<int32_t> nblk(2 * (size_t)nsn, 0);
   std::vector<std::vector<int>> by_h(c->height);
   for (int s = 0; s < nsn; ++s) by_h[b.sn[s].height].push_back(s);
   int64_t pslot = 0;
   int n_bctr = 0;
-  // one 32-block of phase `type` of supernode s whose reduction range is [r0, r1)
-  auto block = [&](int type, int s, int blk, int r0, int r1) {
-    const int ntb = std::max(1, (r1 - r0 + TILE - 1) / TILE);
-    for (int t = 0; t < ntb; ++t)
-      items.insert(items.end(), {type, s, blk, t, ntb, (int32_t)pslot, n_bctr, r0 + t * TILE});
-    if (pslot + (int64_t)ntb * 32 > INT32_MAX) throw ScError(SC_ERR_CONFIG, "solve partial buffer too large");
-    pslot += (int64_t)ntb * 32;
-    ++n_bctr;
-    ++nblk[(size_t)type * nsn + s];
+  auto group = [&](int ph, int s, int ntb, int outs, auto&& geom) {   // one output group
+    for (int t = 0; t < ntb; ++t) {
+      int r0, nr, c0_, nc;
+      geom(t, r0, nr, c0_, nc);
+      const int64_t ao = a_off[s];
+      items.insert(items.end(), {ph, s, t, ntb, (int32_t)pslot, ntb > 1 ? n_bctr : 0, r0, nr, c0_, nc,
+                                 c0[s], wv[s], rv[s], goff[s], uoff[s], roff[s], (int32_t)(ao & 0xffffffff),
+                                 (int32_t)(ao >> 32), panel_ld(wv[s], rv[s]), panel_wp(wv[s])});
+    }
+    if (ntb > 1) {
+      if (pslot + (int64_t)ntb * outs > INT32_MAX) throw ScError(SC_ERR_CONFIG, "solve partial buffer too large");
+      pslot += (int64_t)ntb * outs;
+      ++n_bctr;
+    }
+    ++nblk[(size_t)ph * nsn + s];
   };
-  auto fused = [&](int s) {
-    return wv[s] <= FUSE_W && rv[s] <= FUSE_R && (int64_t)wv[s] * (wv[s] + rv[s]) <= FUSE_ENTRIES;
+  auto fwd_items = [&](int s) {
+    const int w = wv[s], ld = panel_ld(w, rv[s]);
+    const int C = std::min(w, TILE);
+    int R = 32;
+    while (2 * R * C <= SOLVE_STAGE && R < ((ld + 31) / 32) * 32) R *= 2;
+    const int ntb = (w + C - 1) / C;
+    for (int r0 = 0; r0 < ld; r0 += R)
+      group(0, s, ntb, R, [&](int t, int& rr, int& nr, int& cc, int& nc) {
+        rr = r0;
+        nr = std::min(R, ld - r0);
+        cc = t * C;
+        nc = std::min(C, w - t * C);
+      });
   };
-  auto fused_item = [&](int type, int s) {  // one CTA does both phases of the sweep
-    items.insert(items.end(), {type, s, 0, 0, 1, 0, 0, 0});
-    const int p0 = type == 4 ? 0 : 2;
-    nblk[(size_t)p0 * nsn + s] = 1;
-    nblk[(size_t)(p0 + 1) * nsn + s] = 1;
+  auto bwd_items = [&](int s) {
+    const int w = wv[s], rp = (rv[s] + 1) & ~1;
+    const int NC = std::min(32, w);
+    int RR = std::min(SOLVE_BROWS, (SOLVE_STAGE / NC) & ~1);
+    RR = std::max(2, std::min(RR, std::max(rp, 2)));
+    const int ntb = std::max(1, (rp + RR - 1) / RR);
+    for (int o0 = 0; o0 < w; o0 += 32)
+      group(1, s, ntb, 32, [&](int t, int& rr, int& nr, int& cc, int& nc) {
+        rr = t * RR;
+        nr = std::max(0, std::min(RR, rp - t * RR));
+        cc = o0;
+        nc = std::min(32, w - o0);
+      });
   };
-  for (int h = 0; h < c->height; ++h) {
-    for (int s : by_h[h])
-      if (fused(s)) fused_item(4, s);
-    for (int s : by_h[h])  // fA: rows of L_ss^{-1}; columns 0 .. block end (lower triangle)
-      if (!fused(s))
-        for (int rb = 0; rb * 32 < wv[s]; ++rb) block(0, s, rb, 0, std::min(wv[s], rb * 32 + 32));
-    for (int s : by_h[h])  // fB: rows of L_R; all w columns
-      if (!fused(s))
-        for (int rb = 0; rb * 32 < rv[s]; ++rb) block(1, s, rb, 0, wv[s]);
-  }
-  for (int h = c->height - 1; h >= 0; --h) {
-    for (int s : by_h[h])
-      if (fused(s)) fused_item(5, s);
-    for (int s : by_h[h])  // bA: columns of L_R; all r rows
-      if (!fused(s))
-        for (int cb = 0; cb * 32 < wv[s]; ++cb) block(2, s, cb, 0, rv[s]);
-    for (int s : by_h[h])  // bB: columns i of L_ss^{-1}; rows j >= block start
-      if (!fused(s))
-        for (int ob = 0; ob * 32 < wv[s]; ++ob) block(3, s, ob, ob * 32, wv[s]);
-  }
-  c->n_items = (int)(items.size() / 8);
+  // items of one phase of one supernode are contiguous: [item_first, item_first + item_cnt)
+  std::vector<int32_t> item_first(2 * (size_t)nsn, 0), item_cnt(2 * (size_t)nsn, 0);
+  for (int h = 0; h < c->height; ++h)
+    for (int s : by_h[h]) {
+      item_first[s] = (int32_t)(items.size() / 20);
+      fwd_items(s);
+      item_cnt[s] = (int32_t)(items.size() / 20) - item_first[s];
+    }
+  for (int h = c->height - 1; h >= 0; --h)
+    for (int s : by_h[h]) {
+      item_first[nsn + s] = (int32_t)(items.size() / 20);
+      bwd_items(s);
+      item_cnt[nsn + s] = (int32_t)(items.size() / 20) - item_first[nsn + s];
+    }
+  c->n_items = (int)(items.size() / 20);
+  // ready-queue metadata (solve.cu): the forward items of the leaves are ready at launch;
+  // every other phase is pushed by the CTA that completes its last dependency
+  std::vector<int32_t> qmeta;
+  qmeta.insert(qmeta.end(), item_first.begin(), item_first.end());
+  qmeta.insert(qmeta.end(), item_cnt.begin(), item_cnt.end());
+  for (int s = 0; s < nsn; ++s) qmeta.push_back((int32_t)b.sn[s].children.size());
+  c->n_init = 0;
+  for (int s = 0; s < nsn; ++s)
+    if (b.sn[s].children.empty())
+      for (int k = 0; k < item_cnt[s]; ++k) {
+        qmeta.push_back(item_first[s] + k);
+        ++c->n_init;
+      }
   if (getenv("SC_DEBUG")) {
-    int64_t nf = 0, ef = 0, nt = 0, et = 0, maxw = 0, maxr = 0;
+    int64_t maxw = 0, maxr = 0;
     for (int s = 0; s < nsn; ++s) {
-      const int64_t ent = (int64_t)wv[s] * (wv[s] + rv[s]);
-      if (fused(s)) { ++nf; ef += ent; } else { ++nt; et += ent; }
       maxw = std::max<int64_t>(maxw, wv[s]);
       maxr = std::max<int64_t>(maxr, rv[s]);
     }
-    fprintf(stderr, "[sc] supernodes %d (fused %lld, %.3g entries; tiled %lld, %.3g entries) max w %lld max r %lld "
-            "height %d items %d components %lld\n", nsn, (long long)nf, (double)ef, (long long)nt, (double)et,
+    fprintf(stderr, "[sc] supernodes %d max w %lld max r %lld height %d items %d components %lld\n", nsn,
             (long long)maxw, (long long)maxr, c->height, c->n_items, (long long)c->n_components);
   }
-  c->n_counters = 4 * (size_t)nsn + n_bctr + 1;
+  // per-launch counters (zeroed by launch_solve): phase block counts [2 nsn], finished
+  // children [nsn], tile tickets [n_bctr], ready slots [n_items], head, tail
+  c->n_counters = 3 * (size_t)nsn + n_bctr + (size_t)c->n_items + 2;
+  c->h_items = items;
   std::vector<int32_t> chptr(nsn + 1, 0), chidx, parent(nsn, -1);
   for (int s = 0; s < nsn; ++s) {
     for (int ch : b.sn[s].children) chidx.push_back(ch);
@@ -759,8 +855,7 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   up32(&c->d_sn_c0, c0);
   up32(&c->d_sn_w, wv);
   up32(&c->d_sn_r, rv);
-  up64(&c->d_sn_linv, li);
-  up64(&c->d_sn_lr, lr);
+  up64(&c->d_sn_aoff, ao);
   up32(&c->d_sn_roff, roff);
   up32(&c->d_sn_uoff, uoff);
   up32(&c->d_sn_goff, goff);
@@ -769,15 +864,14 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   up32(&c->d_gidx, gidx);
   up32(&c->d_items, items);
   up32(&c->d_nitem, nblk);
+  up32(&c->d_qmeta, qmeta);
   SC_CUDA(cudaMalloc(&c->d_part, sizeof(double) * std::max<int64_t>(1, pslot)));
   up32(&c->d_chptr, chptr);
   up32(&c->d_chidx, chidx);
   up32(&c->d_parent, parent);
   SC_CUDA(cudaMalloc(&c->d_solve_cnt, sizeof(int) * c->n_counters));
-  upd_(&c->fS.Linv, hLinvS);
-  upd_(&c->fS.LR, hLRS);
-  upd_(&c->fM.Linv, hLinvM);
-  upd_(&c->fM.LR, hLRM);
+  upd_(&c->fS.A, hAS);
+  upd_(&c->fM.A, hAM);
   SC_CUDA(cudaMalloc(&c->d_U, sizeof(double) * std::max<int32_t>(1, uoff[nsn])));
   // c element tables
   std::vector<int32_t> cell32(ne), kidx32(ne);
@@ -814,9 +908,8 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   SC_CUDA(cudaMalloc(&c->d_vc, sizeof(double) * ncs));
   SC_CUDA(cudaMalloc(&c->d_ac, sizeof(double) * ncs));
   SC_CUDA(cudaMalloc(&c->d_b, sizeof(double) * ncs));
-  SC_CUDA(cudaMalloc(&c->d_y, sizeof(double) * ncs));
+  SC_CUDA(cudaMalloc(&c->d_q, sizeof(double) * ncs));
   SC_CUDA(cudaMalloc(&c->d_x, sizeof(double) * ncs));
-  SC_CUDA(cudaMalloc(&c->d_z, sizeof(double) * ncs));
   SC_CUDA(cudaMalloc(&c->d_Y, sizeof(double) * std::max<size_t>(1, (size_t)ne * nb)));
   SolveDev& sd = c->solve_dev;
   sd.items = reinterpret_cast<const int4*>(c->d_items);
@@ -831,8 +924,7 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   sd.uoff = c->d_sn_uoff;
   sd.roff = c->d_sn_roff;
   sd.R = c->d_R;
-  sd.linv_off = c->d_sn_linv;
-  sd.lr_off = c->d_sn_lr;
+  sd.aoff = c->d_sn_aoff;
   sd.nblk = c->d_nitem;
   sd.part = c->d_part;
   sd.chptr = c->d_chptr;
@@ -840,12 +932,26 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   sd.parent = c->d_parent;
   sd.U = c->d_U;
   sd.b = c->d_b;
-  sd.y = c->d_y;
+  sd.q = c->d_q;
   sd.x = c->d_x;
-  sd.z = c->d_z;
   sd.cnt = c->d_solve_cnt;
-  sd.bcnt = c->d_solve_cnt + 4 * (size_t)nsn;
-  sd.head = c->d_solve_cnt + c->n_counters - 1;
+  sd.done_ch = c->d_solve_cnt + 2 * (size_t)nsn;
+  sd.bcnt = c->d_solve_cnt + 3 * (size_t)nsn;
+  sd.ready = sd.bcnt + n_bctr;
+  sd.head = c->d_solve_cnt + c->n_counters - 2;
+  sd.tail = c->d_solve_cnt + c->n_counters - 1;
+  sd.item_first = c->d_qmeta;
+  sd.item_cnt = c->d_qmeta + 2 * (size_t)nsn;
+  sd.nch = c->d_qmeta + 4 * (size_t)nsn;
+  sd.init = c->d_qmeta + 5 * (size_t)nsn;
+  sd.n_init = c->n_init;
+  sd.tile = TILE;
+  sd.prefetch = getenv("SC_SOLVE_PREFETCH") ? atoi(getenv("SC_SOLVE_PREFETCH")) : 0;
+  sd.trace = nullptr;
+  if (getenv("SC_TRACE")) {
+    SC_CUDA(cudaMalloc(&c->d_trace, sizeof(unsigned long long) * 3 * std::max(1, c->n_items)));
+    sd.trace = c->d_trace;
+  }
   c->Kcut_host.clear();
   c->Kcut_host.shrink_to_fit();
   c->Mcut_host.clear();

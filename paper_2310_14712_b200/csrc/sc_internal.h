@@ -10,11 +10,11 @@
 
 #define SC_MAXP1 9            // p <= 8
 #define SC_MAX_VOIDS 4096
-// supernodes with w <= FUSE_W, r <= FUSE_R and (w*w + r*w) <= FUSE_ENTRIES are solved by a
-// single CTA per sweep (solve.cu); larger ones are tiled
-#define FUSE_W 128
-#define FUSE_R 1024
-#define FUSE_ENTRIES 16384
+// solve work items (solve.cu, factor.cpp): one staging buffer of SOLVE_STAGE doubles per CTA;
+// forward tiles have at most SOLVE_TILE columns, backward tiles at most SOLVE_BROWS rows
+#define SOLVE_TILE 128
+#define SOLVE_STAGE 4096
+#define SOLVE_BROWS 1024
 
 // ---------------------------------------------------------------- device-side data
 struct DVoid {
@@ -37,23 +37,36 @@ struct GridP {
 
 // device view of the supernodal factor structure + persistent-solve work list (solve.cu)
 struct SolveDev {
-  const int4* items;           // 2 x int4 per tile: (type, s, block, tile) (ntiles, pslot, bctr, lo)
+  const int4* items;           // 5 x int4 per item (factor.cpp)
   int n_items, n_sn;
   const int32_t *w, *r, *c0, *goff, *gptr, *gidx, *uoff, *roff, *R;
-  const int64_t *linv_off, *lr_off;
-  const int32_t *nblk;         // [4][n_sn] 32-blocks per phase
+  const int64_t* aoff;         // per supernode offset of its stacked [D_s; G_s] panel
+  const int32_t *nblk;         // [2][n_sn] 32-blocks per phase (0 forward, 1 backward)
   const int32_t *chptr, *chidx, *parent;
-  const double *Linv, *LR;
-  double *U, *b, *y, *x, *z;
+  const double* A;             // stacked panels, ld x w column-major each (factor.cpp panel_ld)
+  double *U, *b, *q, *x;
   double* part;                // tile partial sums
-  int* cnt;                    // [4][n_sn] completed blocks per phase
+  int* cnt;                    // [2][n_sn] completed blocks per phase
+  int* done_ch;                // [n_sn] children whose forward phase is complete
   int* bcnt;                   // per block: tiles done (ticket)
-  int* head;                   // dequeue counter
+  int* ready;                  // ready queue slots: item + 1 (0 = not yet pushed)
+  int* head;                   // ready-queue consumer counter
+  int* tail;                   // ready-queue producer counter
+  const int32_t *item_first, *item_cnt;   // [2][n_sn] item range of each phase
+  const int32_t* nch;          // [n_sn] number of children
+  const int32_t* init;         // forward items of the leaves (ready at launch)
+  int n_init;
+  int tile;                    // reduction-tile length (SOLVE_TILE)
+  int prefetch;                // SC_SOLVE_PREFETCH=1: L2 bulk prefetch of a phase's panel at push
+  unsigned long long* trace;   // optional (SC_TRACE): per item [dequeued, deps met, done] ns
 };
 
-struct Factor {          // device factor of one SPD matrix (S or M^cc), shared symbolic
-  double* Linv = nullptr;  // per supernode w x w column-major inverse of L_ss (lower)
-  double* LR = nullptr;    // per supernode r x w column-major L_{R_s, s}
+// Device factor of one SPD matrix (S or M^cc), shared symbolic structure.  For supernode s
+// with L = [L_ss 0; L_Rs L_RR] the panel stores D_s = (L_ss L_ss^T)^{-1} (w x w, full) on
+// top of G_s = L_Rs L_ss^{-1} (r x w): forward  q_s = D_s v_s, U_s = G_s v_s (+ children);
+// backward x_s = q_s - G_s^T x_R  (solve.cu).
+struct Factor {
+  double* A = nullptr;     // stacked panels [D_s; 0; G_s; 0], column-major (factor.cpp make_panel)
   double* d = nullptr;     // Jacobi scaling: the factor is of D A D, D = diag(A)^{-1/2}
 };
 
@@ -72,9 +85,10 @@ struct sc_ctx {
   double dt_crit_uncut = 0;
   // ---- classification (host copies)
   std::vector<int8_t> cell_class;     // 0 uncut 1 cut 2 empty
-  std::vector<uint8_t> ntype;         // per lattice node: 0 hole 1 tensor-d 2 irregular-d 3 c
+  std::vector<uint8_t> ntype;         // per lattice node: 0 hole 1 tensor-d far from c 2 irregular-d 3 c
+                                      // 4 tensor-d sharing an element with a c node ("near")
   std::vector<int64_t> dof_lat;       // canonical DOFs -> lattice index
-  int64_t n_dof = 0, n_d = 0, n_c = 0, n_irr = 0;
+  int64_t n_dof = 0, n_d = 0, n_c = 0, n_irr = 0, n_near = 0;
   int64_t cells_uncut = 0, cells_cut = 0, cells_empty = 0;
   // c numbering: ND order (new index) -> lattice index; canonical c order map
   std::vector<int64_t> c_lat;         // ND order
@@ -103,7 +117,7 @@ struct sc_ctx {
   // c state (ND order)
   int32_t* d_c_lat = nullptr;
   double *d_vc = nullptr, *d_ac = nullptr, *d_fxc = nullptr;
-  double *d_b = nullptr, *d_y = nullptr, *d_x = nullptr, *d_z = nullptr, *d_U = nullptr;
+  double *d_b = nullptr, *d_q = nullptr, *d_x = nullptr, *d_U = nullptr;
   // c elements
   int64_t n_celem = 0, n_cut = 0;
   int32_t* d_celem_cell = nullptr;   // cell index of each c-element
@@ -115,24 +129,36 @@ struct sc_ctx {
   // factor structure (shared by S and M^cc)
   int n_sn = 0, height = 0;
   int32_t *d_sn_c0 = nullptr, *d_sn_w = nullptr, *d_sn_r = nullptr;
-  int64_t *d_sn_linv = nullptr, *d_sn_lr = nullptr;
+  int64_t* d_sn_aoff = nullptr;
   int32_t *d_sn_roff = nullptr, *d_sn_uoff = nullptr, *d_sn_goff = nullptr;
   int32_t* d_R = nullptr;             // row structures (ND c indices)
   int32_t *d_gptr = nullptr, *d_gidx = nullptr;
   int32_t* d_items = nullptr;         // int4 work items
   int32_t *d_nitem = nullptr, *d_chptr = nullptr, *d_chidx = nullptr, *d_parent = nullptr;
-  int* d_solve_cnt = nullptr;         // [4*n_sn] phase counters, [n_bctr] tickets, head
+  int32_t* d_qmeta = nullptr;         // ready-queue metadata (solve.cu)
+  int n_init = 0;
+  int* d_solve_cnt = nullptr;         // [2*n_sn] phase counters, [n_bctr] tickets, head
   double* d_part = nullptr;           // tile partials
   int n_items = 0, solve_grid = 0;
+  unsigned long long* d_trace = nullptr;   // SC_TRACE: solve item timeline (debug)
+  std::vector<int32_t> h_items;            // host copy of the work list (debug)
   size_t n_counters = 0;
   SolveDev solve_dev{};
   Factor fS, fM;
-  int64_t nnz_factor = 0;
+  int64_t nnz_factor = 0;   // sum_s w_s (w_s + r_s): stored panel entries
+  int64_t nnz_G = 0;        // sum_s r_s w_s (re-read by the backward sweep)
+  int64_t sum_r = 0;        // sum_s r_s (update-vector entries)
   int64_t n_components = 0;
-  // graphs
+  // near-d tiles of the explicit kernel (tile ids, x fastest)
+  int* d_near_tiles = nullptr;
+  int n_near_tiles = 0;
+  // graphs and the step pipeline (step.cu)
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  cudaStream_t s_hi = nullptr;             // high-priority stream of the c part
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool far_ready = false;                  // far-d update of the current step already enqueued
   int kernels_per_step = 0;
-  double bytes_per_step = 0, bytes_explicit = 0;
+  double bytes_per_step = 0, bytes_explicit = 0, bytes_solve = 0, bytes_celem = 0;
   double setup_seconds = 0;
   // setup scratch
   int src_kind = 0;
@@ -174,10 +200,12 @@ void setup_device_geometry(sc_ctx* c);
 void setup_factor(sc_ctx* c, const std::vector<double>& Mcut_host);
 // step (step.cu)
 void setup_step_structures(sc_ctx* c);
+void explicit_tiling(const GridP& g, int ext[3], int tg[3]);
 void build_graphs(sc_ctx* c);
 void run_startup(sc_ctx* c, const double* u0, const double* v0);
-void enqueue_step(sc_ctx* c, int parity);
-void launch_solve(sc_ctx* c, const Factor& f);
+void enqueue_step(sc_ctx* c, int parity, cudaStream_t st);
+void enqueue_far_prologue(sc_ctx* c);
+void launch_solve(sc_ctx* c, const Factor& f, cudaStream_t st);
 void device_upload_reference(sc_ctx* c);
 void gather_dofs(sc_ctx* c, const double* d_lat, double* d_out);
 void profile_launch(sc_ctx* c, int which);

@@ -2,28 +2,49 @@
 // ("triangular matrix system with the factorized system
 // matrix S" each step).  The factor is of the Jacobi-scaled matrix D S D (factor.cpp).
 //
-// One persistent kernel performs both sweeps.  Every supernode GEMV is cut into tiles
-// (forward: 32 rows x 256 columns, backward: 32 outputs x 256 rows); a tile writes its 32
-// partial sums to a private slot, and the LAST tile of each 32-wide block (atomic ticket)
-// sums the block's partials in fixed tile order -> deterministic results.  Tiles are stored
-// in a topological order (forward by supernode height, backward by height descending);
-// CTAs dequeue them from a global counter and spin until the phase counters they depend
-// on are complete.  Every dependency points to an EARLIER tile and tiles are only dequeued
-// by running CTAs, so all producers are resident: no deadlock, no cooperative launch.
-// Producer: partials / results, __threadfence, atomicAdd.  Consumer: spin, __threadfence,
-// reads of produced data with ld.global.cg (L1 bypass).
+// Supernodal block substitution with each supernode's triangular solves folded into its
+// panel (factor.cpp make_panel): with L = [L_ss 0; L_Rs L_RR],
+//   forward   v_s = b_s - (updates of the children),  q_s = D_s v_s,  U_s = G_s v_s (+ children)
+//   backward  x_s = q_s - G_s^T x_R
+// where D_s = (L_ss L_ss^T)^{-1} and G_s = L_Rs L_ss^{-1}; this equals L_ss^{-T}(L_ss^{-1} v_s
+// - L_Rs^T x_R), i.e. the two triangular solves of the block algorithm, so each supernode has
+// ONE dependent phase per sweep (the critical path is the elimination-tree height, once per
+// sweep) and one stacked GEMV [D_s; G_s] v_s per forward phase.
 //
-// Phases per supernode s (w columns, r rows below, c0 first column):
-//  fA: y_s = L_ss^{-1} (b_s - child updates)            tiles over (row block, column tile)
-//  fB: U_s = child updates + L_{R,s} y_s                  tiles over (row block, column tile)
-//  bA: z_s = y_s - L_{R,s}^T x[R_s]                       tiles over (column block, row tile)
-//  bB: x_s = L_ss^{-T} z_s                                tiles over (output block, row tile)
+// One persistent kernel performs both sweeps, driven by a READY QUEUE of work items: the
+// forward items of the leaves are ready at launch; the CTA that completes the last block of a
+// phase pushes the items that this completion makes ready (forward of the parent once all its
+// children are done; backward of the root after its forward; backward of the children after a
+// backward).  A CTA therefore only ever holds a ready item: no CTA waits on dependencies while
+// holding an item, all resident CTAs work.  Per item: take the next queue slot, stream the
+// item's panel tile into shared memory with bulk (TMA) copies completing on an mbarrier,
+// gather the produced vector entries meanwhile, contract, publish.
+// Tiles: forward 32 panel rows x SOLVE_TILE columns, backward 32 outputs x SOLVE_TILE rows.  A
+// block whose reduction spans several tiles writes per-tile partials; the LAST tile (atomic
+// ticket) sums them in fixed tile order -> deterministic results regardless of the schedule.
+// Small supernodes (whole panel <= one staging buffer) are one item per phase.
+// Progress: a slot is only awaited by a CTA that holds no item; if every CTA waits, every
+// pushed item is finished and its completion pushed its dependents, so the queue advances
+// until all n_items slots are filled.  Publication: results, __threadfence, counter atomics
+// (release); the pusher fences after observing the final count and then stores the slots
+// (fence + relaxed store = release); the consumer acquire-loads the slot.
+#include <cstdlib>
+
 #include "sc_internal.h"
 
 namespace {
 
-enum { IT_FA = 0, IT_FB = 1, IT_BA = 2, IT_BB = 3, IT_FF = 4, IT_BF = 5 };
-constexpr int TILE = 256;  // columns (forward) / rows (backward) per tile
+enum { IT_F = 0, IT_B = 1 };
+constexpr int NT = 256;               // threads per CTA
+constexpr int NW = NT / 32;
+constexpr int STAGE = SOLVE_STAGE;    // staging buffer (doubles)
+constexpr int VS = SOLVE_BROWS > SOLVE_TILE ? SOLVE_BROWS : SOLVE_TILE;   // gathered vector
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -41,245 +62,316 @@ __device__ __forceinline__ void wait_ge(const int* p, int target) {
   }
 }
 
-// sum_{j in [j0, j1) step js} A[i + j ld] v[j] for one row per lane, 8 loads in flight
-__device__ __forceinline__ double row_dot(const double* A, size_t ld, int i, bool ok, int j0, int j1, int js,
-                                          const double* v) {
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  if (ok) {
-    int j = j0;
-    for (; j + 7 * js < j1; j += 8 * js) {
-      double x[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) x[k] = A[i + (size_t)(j + k * js) * ld];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) acc[k & 3] += x[k] * v[j + k * js];
+__device__ __forceinline__ void st_relaxed(int* p, int v) {
+  asm volatile("st.relaxed.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// L2 prefetch (TMA bulk prefetch) of the panel data of phase ph of supernode s (warp), so the
+// items' staging copies hit L2: forward streams the whole panel, backward the G_s parts
+__device__ __forceinline__ void prefetch_phase(const SolveDev& a, int ph, int s, int lane) {
+  const int first = a.item_first[ph * a.n_sn + s];
+  const int4 d2 = a.items[5 * (size_t)first + 2], d3 = a.items[5 * (size_t)first + 3],
+             d4 = a.items[5 * (size_t)first + 4];
+  const int w = d2.w, r = d3.x, ld = d4.z, wp = d4.w;
+  const double* Ap = a.A + ((int64_t)(uint32_t)d4.x | ((int64_t)d4.y << 32));
+  if (ph == 0) {
+    const size_t bytes = (size_t)ld * w * 8;
+    for (size_t o = (size_t)lane << 16; o < bytes; o += (size_t)32 << 16)
+      bulk_prefetch_l2(reinterpret_cast<const char*>(Ap) + o, (unsigned)min((size_t)1 << 16, bytes - o));
+  } else if (r > 0) {
+    const unsigned bytes = (unsigned)(((r + 1) & ~1) * 8);
+    for (int j = lane; j < w; j += 32) bulk_prefetch_l2(Ap + (size_t)j * ld + wp, bytes);
+  }
+}
+
+// make the items of phase ph of supernode s ready (warp 0; the caller fenced after observing
+// the completion it reacts to, so relaxed slot stores publish everything before the fence)
+__device__ __forceinline__ void push_phase(const SolveDev& a, int ph, int s, int lane) {
+  const int first = a.item_first[ph * a.n_sn + s], cnt = a.item_cnt[ph * a.n_sn + s];
+  int slot = 0;
+  if (lane == 0) slot = atomicAdd(a.tail, cnt);
+  slot = __shfl_sync(0xffffffffu, slot, 0);
+  for (int k = lane; k < cnt; k += 32) st_relaxed(a.ready + slot + k, first + k + 1);
+  if (a.prefetch) prefetch_phase(a, ph, s, lane);
+}
+
+// one block of phase ph of supernode s is published (warp 0, after the block's results were
+// written and fenced); the warp completing the phase pushes its dependents
+__device__ __forceinline__ void complete_block(const SolveDev& a, int ph, int s, int lane) {
+  const int n_sn = a.n_sn;
+  int act = 0;   // 0 nothing, 1 phase complete (forward: 2 parent ready, 3 root)
+  if (lane == 0) {
+    __threadfence();
+    if (atomicAdd(a.cnt + ph * n_sn + s, 1) == a.nblk[ph * n_sn + s] - 1) {
+      __threadfence();
+      act = 1;
+      if (ph == 0) {
+        const int p = a.parent[s];
+        if (p < 0) {
+          act = 3;
+        } else if (atomicAdd(a.done_ch + p, 1) == a.nch[p] - 1) {
+          __threadfence();
+          act = 2;
+        }
+      }
     }
-    for (; j < j1; j += js) acc[0] += A[i + (size_t)j * ld] * v[j];
   }
-  return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  act = __shfl_sync(0xffffffffu, act, 0);
+  if (!act) return;
+  if (ph == 0) {
+    if (act == 3) push_phase(a, 1, s, lane);
+    else if (act == 2) push_phase(a, 0, a.parent[s], lane);
+  } else {
+    for (int q = a.chptr[s]; q < a.chptr[s + 1]; ++q) push_phase(a, 1, a.chidx[q], lane);
+  }
 }
 
-// sum_{q in [q0, q1) step 32} Ac[q] v[q] by one lane (column dot product, 8 loads in flight)
-__device__ __forceinline__ double col_dot(const double* Ac, int q0, int q1, const double* v) {
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  int q = q0;
-  for (; q + 7 * 32 < q1; q += 256) {
-    double x[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) x[k] = Ac[q + 32 * k];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) acc[k & 3] += x[k] * v[q + 32 * k];
-  }
-  for (; q < q1; q += 32) acc[0] += Ac[q] * v[q];
-  return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, unsigned phase) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+// global -> shared bulk copy (TMA engine); bytes and both addresses multiples of 16
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 
-// y[0..nr) = A[0..nr, 0..nc) v  (A column-major, leading dimension ld; v, y in smem):
-// each warp owns whole 32-row blocks (no cross-warp reduction, no barrier inside).
-__device__ __forceinline__ void cta_gemv_rows(const double* A, int ld, int nr, int nc, const double* v, double* y,
-                                              double (*)[33]) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int rb = warp * 32; rb < nr; rb += 256) {
-    const int i = rb + lane;
-    const double t = row_dot(A, ld, i, i < nr, 0, nc, 1, v);
-    if (i < nr) y[i] = t;
-  }
-  __syncthreads();
+struct Item {
+  int type, s, t, ntb, pslot, bctr, r0, nr, c0, nc;   // see factor.cpp (fat items)
+  int dof0, w, r, goff, uoff, roff, ld, wp;
+  int64_t aoff;
+};
+
+__device__ __forceinline__ Item load_item(const SolveDev& a, int it) {
+  const int4* d = a.items + 5 * (size_t)it;
+  const int4 d0 = d[0], d1 = d[1], d2 = d[2], d3 = d[3], d4 = d[4];
+  Item m;
+  m.type = d0.x;
+  m.s = d0.y;
+  m.t = d0.z;
+  m.ntb = d0.w;
+  m.pslot = d1.x;
+  m.bctr = d1.y;
+  m.r0 = d1.z;
+  m.nr = d1.w;
+  m.c0 = d2.x;
+  m.nc = d2.y;
+  m.dof0 = d2.z;
+  m.w = d2.w;
+  m.r = d3.x;
+  m.goff = d3.y;
+  m.uoff = d3.z;
+  m.roff = d3.w;
+  m.aoff = (int64_t)(uint32_t)d4.x | ((int64_t)d4.y << 32);
+  m.ld = d4.z;
+  m.wp = d4.w;
+  return m;
 }
 
-__global__ void __launch_bounds__(256) k_solve(SolveDev a) {
-  __shared__ double vs[TILE];
-  __shared__ double part[8][33];
-  __shared__ double fv[FUSE_W], fy[FUSE_W], fu[FUSE_R];   // fused small-supernode phases
+// issue the bulk copies of item m's panel tile into `st` (warp 0): one column segment per
+// staged column; lane 0 arms `bar` with the byte count first.  Staged layout: column j of
+// the tile at st + j * nr (F: panel rows r0.., B: G rows r0..).
+__device__ __forceinline__ void stage_item(const SolveDev& a, const Item& m, double* st, uint64_t* bar, int lane) {
+  const double* Ap = a.A + m.aoff;
+  const int nr = m.nr;
+  if (lane == 0) mbar_expect(bar, (unsigned)(m.nc * nr * 8));
+  __syncwarp();
+  if (nr == 0) return;
+  const size_t row0 = (m.type == IT_F) ? (size_t)m.r0 : (size_t)m.wp + m.r0;
+  for (int j = lane; j < m.nc; j += 32)
+    bulk_g2s(st + j * nr, Ap + (size_t)(m.c0 + j) * m.ld + row0, nr * 8, bar);
+}
+
+__global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
+  extern __shared__ __align__(128) double stg[];   // STAGE doubles
+  __shared__ double vs[VS];
+  __shared__ double red[NT];
+  __shared__ __align__(8) uint64_t bar;
   __shared__ int s_item, s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) mbar_init(&bar);
+  unsigned phase = 0;
   while (true) {
-    if (tid == 0) s_item = atomicAdd(a.head, 1);
+    __syncthreads();   // previous item fully consumed (stage buffer and vs free)
+    if (tid == 0) {
+      const int h = atomicAdd(a.head, 1);
+      int itm = -1;
+      if (h < a.n_items) {
+        if (h < a.n_init) {
+          itm = a.init[h];
+        } else {
+          const int* slot = a.ready + (h - a.n_init);
+          int v;
+          unsigned ns = 32;
+          while ((v = ld_acquire(slot)) == 0) {
+            __nanosleep(ns);
+            if (ns < 256) ns <<= 1;
+          }
+          itm = v - 1;
+        }
+      }
+      s_item = itm;
+    }
     __syncthreads();
     const int it = s_item;
-    if (it >= a.n_items) return;
-    const int4 d0 = a.items[2 * it], d1 = a.items[2 * it + 1];
-    const int type = d0.x, s = d0.y, blk = d0.z, t = d0.w;   // blk: 32-block, t: tile in block
-    const int ntb = d1.x, pslot = d1.y, bctr = d1.z, lo = d1.w;  // lo: first column/row of tile
-    const int w = a.w[s], r = a.r[s], c0 = a.c0[s];
-    const int n_sn = a.n_sn;
-    // ---- dependencies
-    if (tid == 0) {
-      if (type == IT_FA || type == IT_FF) {
-        for (int q = a.chptr[s]; q < a.chptr[s + 1]; ++q) {
-          const int c = a.chidx[q];
-          wait_ge(a.cnt + 1 * n_sn + c, a.nblk[1 * n_sn + c]);
-        }
-      } else if (type == IT_FB) {
-        wait_ge(a.cnt + 0 * n_sn + s, a.nblk[0 * n_sn + s]);
-      } else if (type == IT_BA || type == IT_BF) {
-        const int p = a.parent[s];
-        if (p >= 0) wait_ge(a.cnt + 3 * n_sn + p, a.nblk[3 * n_sn + p]);
-        wait_ge(a.cnt + 0 * n_sn + s, a.nblk[0 * n_sn + s]);
-      } else {
-        wait_ge(a.cnt + 2 * n_sn + s, a.nblk[2 * n_sn + s]);
-      }
-      __threadfence();
-    }
-    __syncthreads();
-    if (type == IT_FF) {
-      // ---- fused forward phase of a small supernode (one CTA)
-      const int go = a.goff[s];
-      for (int j = tid; j < w; j += 256) {
-        double v = a.b[c0 + j];
-        for (int q = a.gptr[go + j]; q < a.gptr[go + j + 1]; ++q) v -= __ldcg(a.U + a.gidx[q]);
-        fv[j] = v;
-      }
-      __syncthreads();
-      cta_gemv_rows(a.Linv + a.linv_off[s], w, w, w, fv, fy, part);
-      for (int j = tid; j < w; j += 256) a.y[c0 + j] = fy[j];
-      if (r > 0) {
-        cta_gemv_rows(a.LR + a.lr_off[s], r, r, w, fy, fu, part);
-        for (int i = tid; i < r; i += 256) {
-          double v = fu[i];
-          for (int q = a.gptr[go + w + i]; q < a.gptr[go + w + i + 1]; ++q) v += __ldcg(a.U + a.gidx[q]);
-          a.U[a.uoff[s] + i] = v;
-        }
-      }
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) {
-        atomicAdd(a.cnt + 0 * n_sn + s, 1);
-        atomicAdd(a.cnt + 1 * n_sn + s, 1);
-      }
-      continue;
-    }
-    if (type == IT_BF) {
-      // ---- fused backward phase of a small supernode (one CTA)
-      for (int i = tid; i < r; i += 256) fu[i] = __ldcg(a.x + a.R[a.roff[s] + i]);
-      __syncthreads();
-      const double* LR = a.LR + a.lr_off[s];
-      for (int j = warp; j < w; j += 8) {
-        double v = col_dot(LR + (size_t)j * r, lane, r, fu);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) fv[j] = __ldcg(a.y + c0 + j) - v;
-      }
-      __syncthreads();
-      const double* Li = a.Linv + a.linv_off[s];
-      for (int i = warp; i < w; i += 8) {
-        double v = 0.0;
-        v = col_dot(Li + (size_t)i * w, i + lane, w, fv);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) a.x[c0 + i] = v;
-      }
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) {
-        atomicAdd(a.cnt + 2 * n_sn + s, 1);
-        atomicAdd(a.cnt + 3 * n_sn + s, 1);
-      }
-      continue;
-    }
-    double* P = a.part + pslot;   // this block's partials: [ntb][32]
-    if (type == IT_FA || type == IT_FB) {
-      // ---- row-oriented tile: rows blk*32 + lane, columns [lo, hi)
-      const int nrows = (type == IT_FA) ? w : r;
-      const int hi = (type == IT_FA) ? min(min(w, blk * 32 + 32), lo + TILE) : min(w, lo + TILE);
-      const int ncols = hi - lo;
-      const int go = a.goff[s];
-      for (int j = tid; j < ncols; j += 256) {
-        double v;
-        if (type == IT_FA) {
-          v = a.b[c0 + lo + j];
-          for (int q = a.gptr[go + lo + j]; q < a.gptr[go + lo + j + 1]; ++q) v -= __ldcg(a.U + a.gidx[q]);
-        } else {
-          v = __ldcg(a.y + c0 + lo + j);
-        }
+    if (it < 0) return;
+    const Item m = load_item(a, it);
+    const bool fwd = (m.type == IT_F);
+    if (a.trace && tid == 0) a.trace[3 * (size_t)it] = gtimer();
+    // ---- stream the panel tile (TMA) and gather the input vector meanwhile (every producer
+    // of it completed before this item was pushed; L1 bypass)
+    if (warp == 0) stage_item(a, m, stg, &bar, lane);
+    const int go = m.goff;
+    if (fwd) {
+      // v_j = b_j - sum of the children's update entries at column position j
+      for (int j = tid; j < m.nc; j += NT) {
+        const int pj = m.c0 + j;
+        double v = a.b[m.dof0 + pj];
+        for (int q = a.gptr[go + pj]; q < a.gptr[go + pj + 1]; ++q) v -= __ldcg(a.U + a.gidx[q]);
         vs[j] = v;
       }
-      __syncthreads();
-      const int i = blk * 32 + lane;
-      const int ld = nrows;
-      const double* A = (type == IT_FA ? a.Linv + a.linv_off[s] : a.LR + a.lr_off[s]) + (size_t)lo * ld;
-      // warp covers columns warp*32 .. warp*32+31 of the tile
-      const int j0 = warp * 32, j1 = min(ncols, j0 + 32);
-      part[warp][lane] = row_dot(A, ld, i, i < nrows, j0, j1, 1, vs);
-      __syncthreads();
-      if (warp == 0) {
-        double v = 0.0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v += part[k][lane];
-        P[t * 32 + lane] = v;
+    } else {
+      const int rr = min(m.nr, m.r - m.r0);   // real (unpadded) rows of this tile
+      for (int i = tid; i < rr; i += NT) vs[i] = __ldcg(a.x + a.R[m.roff + m.r0 + i]);
+      if (tid == 0 && rr < m.nr && rr >= 0) vs[rr] = 0.0;   // padding row
+    }
+    if (a.trace && tid == 0) a.trace[3 * (size_t)it + 1] = gtimer();
+    while (!mbar_try(&bar, phase)) {
+    }
+    phase ^= 1;
+    __syncthreads();
+    // panel row i of the forward phase -> q_s or U_s (children's contributions added)
+    auto emit_f = [&](int i, double v) {
+      if (i < m.w) {
+        a.q[m.dof0 + i] = v;
+      } else if (i >= m.wp && i < m.wp + m.r) {
+        const int k = i - m.wp;
+        for (int q = a.gptr[go + m.w + k]; q < a.gptr[go + m.w + k + 1]; ++q) v += __ldcg(a.U + a.gidx[q]);
+        a.U[m.uoff + k] = v;
+      }
+    };
+    auto emit_b = [&](int j, double v) {   // j: G column (output) index
+      if (j < m.w) a.x[m.dof0 + j] = __ldcg(a.q + m.dof0 + j) - v;
+    };
+    double* P = a.part + m.pslot;
+    bool last = true;
+    if (fwd) {
+      // rows i of the tile: nr rows, nc columns; G threads per row when nr < NT
+      const int nr = m.nr, nc = m.nc;
+      if (nr >= NT) {
+        for (int i = tid; i < nr; i += NT) {
+          double a0 = 0.0, a1 = 0.0;
+          int j = 0;
+          for (; j + 1 < nc; j += 2) {
+            a0 += stg[j * nr + i] * vs[j];
+            a1 += stg[(j + 1) * nr + i] * vs[j + 1];
+          }
+          if (j < nc) a0 += stg[j * nr + i] * vs[j];
+          if (m.ntb == 1) emit_f(m.r0 + i, a0 + a1);
+          else P[m.t * nr + i] = a0 + a1;
+        }
+      } else {
+        const int G = NT / nr;   // nr >= 2
+        const int i = tid % nr, g = tid / nr;
+        double acc = 0.0;
+        if (g < G)
+          for (int j = g; j < nc; j += G) acc += stg[j * nr + i] * vs[j];
+        red[tid] = acc;
+        __syncthreads();
+        if (tid < nr) {
+          double v = 0.0;
+          for (int k = 0; k < G; ++k) v += red[k * nr + tid];
+          if (m.ntb == 1) emit_f(m.r0 + tid, v);
+          else P[m.t * nr + tid] = v;
+        }
       }
     } else {
-      // ---- column-oriented tile: outputs (columns) blk*32 + o, rows [lo, hi)
-      const int o0 = blk * 32;
-      const int hi = (type == IT_BA) ? min(r, lo + TILE) : min(w, lo + TILE);
-      const int nr = hi - lo;
-      for (int j = tid; j < nr; j += 256)
-        vs[j] = (type == IT_BA) ? __ldcg(a.x + a.R[a.roff[s] + lo + j]) : __ldcg(a.z + c0 + lo + j);
-      __syncthreads();
-      const int ld = (type == IT_BA) ? r : w;
-      const double* A = (type == IT_BA ? a.LR + a.lr_off[s] : a.Linv + a.linv_off[s]);
-      // warp handles 4 output columns; lanes stride rows
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        const int col = o0 + warp * 4 + cc;
-        double v = 0.0;
-        if (col < w) {
-          const double* Ac = A + (size_t)col * ld + lo;
-          v = col_dot(Ac, lane, nr, vs);
+      // outputs: nc columns of G_s, warp w handles columns w, w + NW, ...; lanes stride rows
+      const int nr = m.nr;
+      for (int cc = warp; cc < m.nc; cc += NW) {
+        double v0 = 0.0, v1 = 0.0;
+        int i = lane;
+        for (; i + 32 < nr; i += 64) {
+          v0 += stg[cc * nr + i] * vs[i];
+          v1 += stg[cc * nr + i + 32] * vs[i + 32];
         }
+        if (i < nr) v0 += stg[cc * nr + i] * vs[i];
+        double v = v0 + v1;
 #pragma unroll
         for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) P[t * 32 + warp * 4 + cc] = v;
-      }
-    }
-    // ---- last tile of the block reduces the partials in tile order
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) s_last = (atomicAdd(a.bcnt + bctr, 1) == ntb - 1);
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      if (tid < 32) {
-        const int o = blk * 32 + tid;
-        double v = 0.0;
-        for (int k = 0; k < ntb; ++k) v += __ldcg(P + k * 32 + tid);
-        if (type == IT_FA) {
-          if (o < w) a.y[c0 + o] = v;
-        } else if (type == IT_FB) {
-          if (o < r) {
-            const int go = a.goff[s];
-            for (int q = a.gptr[go + w + o]; q < a.gptr[go + w + o + 1]; ++q) v += __ldcg(a.U + a.gidx[q]);
-            a.U[a.uoff[s] + o] = v;
-          }
-        } else if (type == IT_BA) {
-          if (o < w) a.z[c0 + o] = __ldcg(a.y + c0 + o) - v;
-        } else {
-          if (o < w) a.x[c0 + o] = v;
+        if (lane == 0) {
+          if (m.ntb == 1) emit_b(m.c0 + cc, v);
+          else P[m.t * 32 + cc] = v;
         }
       }
+    }
+    if (m.ntb > 1) {
+      // partials of this tile written; the last tile of the group sums them in tile order
       __threadfence();
       __syncthreads();
-      if (tid == 0) atomicAdd(a.cnt + type * n_sn + s, 1);
+      if (tid == 0) s_last = (atomicAdd(a.bcnt + m.bctr, 1) == m.ntb - 1);
+      __syncthreads();
+      last = s_last;
+      if (last) {
+        __threadfence();
+        const int outs = fwd ? m.nr : m.nc;
+        const int stride = fwd ? m.nr : 32;
+        for (int o = tid; o < outs; o += NT) {
+          double v = 0.0;
+          for (int k = 0; k < m.ntb; ++k) v += __ldcg(P + k * stride + o);
+          if (fwd) emit_f(m.r0 + o, v);
+          else emit_b(m.c0 + o, v);
+        }
+      }
     }
-    __syncthreads();
+    if (last) {
+      __syncthreads();   // the CTA's result stores precede lane 0's releasing fence (cumulative)
+      if (warp == 0) complete_block(a, fwd ? 0 : 1, m.s, lane);
+    }
+    if (a.trace && tid == 0) a.trace[3 * (size_t)it + 2] = gtimer();
   }
 }
 
 }  // namespace
 
-void launch_solve(sc_ctx* c, const Factor& f) {
+void launch_solve(sc_ctx* c, const Factor& f, cudaStream_t st) {
   if (c->n_c == 0 || c->n_items == 0) return;
   SolveDev a = c->solve_dev;
-  a.Linv = f.Linv;
-  a.LR = f.LR;
-  SC_CUDA(cudaMemsetAsync(c->d_solve_cnt, 0, sizeof(int) * c->n_counters, c->stream));
+  a.A = f.A;
+  const int smem = (int)(sizeof(double) * STAGE);
   if (c->solve_grid == 0) {
+    SC_CUDA(cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int per_sm = 0, sms = 0, dev = 0;
     SC_CUDA(cudaGetDevice(&dev));
     SC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve, 256, 0));
+    SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve, NT, smem));
+    // SC_SOLVE_CTAS_PER_SM caps the resident solve CTAs (room for the concurrent far-d update)
+    if (const char* v = getenv("SC_SOLVE_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, atoi(v)));
     c->solve_grid = std::max(1, std::min(c->n_items, per_sm * sms));
   }
-  k_solve<<<c->solve_grid, 256, 0, c->stream>>>(a);
+  SC_CUDA(cudaMemsetAsync(c->d_solve_cnt, 0, sizeof(int) * c->n_counters, st));
+  k_solve<<<c->solve_grid, NT, smem, st>>>(a);
   SC_CUDA(cudaGetLastError());
 }

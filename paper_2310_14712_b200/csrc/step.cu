@@ -12,6 +12,7 @@
 // writes u_{n+1} into d_u[cur^1] (d nodes by (a2), c nodes by (a6)) and flips cur.
 #include <algorithm>
 #include <cmath>
+#include <vector>
 
 #include "sc_internal.h"
 
@@ -26,7 +27,17 @@ struct ExpP {
   int N[3];
   double s[3];      // (2/h_k)^2
   double a1, a2, coefR;  // out = a1 u + a2 P - coefR * r' / prod(wt)
+  int want;         // node type updated by this launch (1 tensor-d far from c, 4 tensor-d near c)
+  int tg[2];        // tile-grid extents in x, y (tile-list launches)
+  const int* tiles; // nullable: tile ids (x fastest) of a tile-list launch, one per block
 };
+
+// tile coordinates of this block: from the tile list if any, else from blockIdx
+__device__ __forceinline__ int3 tile_of(const ExpP& e) {
+  if (!e.tiles) return make_int3(blockIdx.x, blockIdx.y, blockIdx.z);
+  const int id = e.tiles[blockIdx.x];
+  return make_int3(id % e.tg[0], (id / e.tg[0]) % e.tg[1], id / (e.tg[0] * e.tg[1]));
+}
 
 namespace {
 
@@ -64,168 +75,12 @@ template <int P>
 __global__ void k_explicit_1d(const double* __restrict__ U, const double* Pv, double* out,
                               const uint8_t* __restrict__ nt, ExpP e, int* flag) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= e.nl[0] || nt[i] != 1) return;
+  if (i >= e.nl[0] || nt[i] != e.want) return;
   const double r = e.s[0] * op1d<P>(c_Kh, i, e.N[0], [&](int k) { return U[k]; });
   const double u = U[i];
   const double res = e.a1 * u + e.a2 * Pv[i] - e.coefR * r / wt(i, e.N[0], P);
   out[i] = res;
   if (!isfinite(res)) atomicExch(flag, 1);
-}
-
-// ------------------------------------------------------------------ 2D
-template <int P, int EX, int EY>
-__global__ void __launch_bounds__(256) k_explicit_2d_v1(const double* __restrict__ U, const double* Pv,
-                                                     double* out, const uint8_t* __restrict__ nt, ExpP e,
-                                                     int* flag) {
-  constexpr int RX = EX * P + P + 1, RY = EY * P + P + 1, TY = EY * P + 1;
-  __shared__ double su[RY][RX];
-  __shared__ double sm[TY][RX];
-  __shared__ double sk[TY][RX];
-  const int nx = e.nl[0], ny = e.nl[1];
-  const int x0 = blockIdx.x * EX * P, y0 = blockIdx.y * EY * P;
-  const int x1 = (x0 + EX * P >= nx - 1) ? nx : x0 + EX * P;
-  const int y1 = (y0 + EY * P >= ny - 1) ? ny : y0 + EY * P;
-  const int xr0 = x0 - P, yr0 = y0 - P;
-  const int RXn = min(x1, nx - 1) - xr0 + 1, RYn = min(y1, ny - 1) - yr0 + 1;
-  for (int t = threadIdx.x; t < RXn * RYn; t += blockDim.x) {
-    const int ix = t % RXn, iy = t / RXn;
-    const int gx = xr0 + ix, gy = yr0 + iy;
-    su[iy][ix] = (gx >= 0 && gy >= 0) ? U[gx + (size_t)nx * gy] : 0.0;
-  }
-  __syncthreads();
-  const int OY = y1 - y0, OX = x1 - x0;
-  for (int t = threadIdx.x; t < OY * RXn; t += blockDim.x) {
-    const int ix = t % RXn, oy = t / RXn;
-    const int gy = y0 + oy;
-    auto col = [&](int k) { return su[k - yr0][ix]; };
-    sm[oy][ix] = op1d<P>(c_Mh, gy, e.N[1], col);
-    sk[oy][ix] = op1d<P>(c_Kh, gy, e.N[1], col);
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < OY * OX; t += blockDim.x) {
-    const int ox = t % OX, oy = t / OX;
-    const int gx = x0 + ox, gy = y0 + oy;
-    const size_t g = gx + (size_t)nx * gy;
-    if (nt[g] != 1) continue;
-    const double r = e.s[0] * op1d<P>(c_Kh, gx, e.N[0], [&](int k) { return sm[oy][k - xr0]; }) +
-                     e.s[1] * op1d<P>(c_Mh, gx, e.N[0], [&](int k) { return sk[oy][k - xr0]; });
-    const double u = su[gy - yr0][gx - xr0];
-    const double res = e.a1 * u + e.a2 * Pv[g] - e.coefR * r / (wt(gx, e.N[0], P) * wt(gy, e.N[1], P));
-    out[g] = res;
-    if (!isfinite(res)) atomicExch(flag, 1);
-  }
-}
-
-// ------------------------------------------------------------------ 3D
-// xy tile of EX x EY elements, streaming along z over EZ element layers (plus one warm-up
-// layer below).  z contraction per column in registers; y and x contractions per plane in
-// shared memory.
-template <int P, int EX, int EY, int EZ>
-__global__ void __launch_bounds__(256) k_explicit_3d_v1(const double* __restrict__ U, const double* Pv, double* out,
-                                                        const uint8_t* __restrict__ nt, ExpP e, int* flag) {
-  constexpr int RX = EX * P + P + 1, RY = EY * P + P + 1, TY = EY * P + 1;
-  constexpr int NCOL = (RX * RY + 255) / 256;
-  extern __shared__ double smem[];
-  double* sa = smem;                          // [P+1][RY][RX]
-  double* sb = sa + (P + 1) * RY * RX;        // [P+1][RY][RX]
-  double* sm = sb + (P + 1) * RY * RX;        // [P+1][TY][RX]
-  double* st = sm + (P + 1) * TY * RX;        // [P+1][TY][RX]
-  const int nx = e.nl[0], ny = e.nl[1];
-  const size_t pl = (size_t)nx * ny;
-  const int x0 = blockIdx.x * EX * P, y0 = blockIdx.y * EY * P;
-  const int x1 = (x0 + EX * P >= nx - 1) ? nx : x0 + EX * P;
-  const int y1 = (y0 + EY * P >= ny - 1) ? ny : y0 + EY * P;
-  const int xr0 = x0 - P, yr0 = y0 - P;
-  const int RXn = min(x1, nx - 1) - xr0 + 1, RYn = min(y1, ny - 1) - yr0 + 1;
-  const int OX = x1 - x0, OY = y1 - y0;
-  const int Nz = e.N[2];
-  const int ez0 = blockIdx.z * EZ, ez1 = min(ez0 + EZ, Nz);
-  double carry_a[NCOL], carry_b[NCOL];
-#pragma unroll
-  for (int c = 0; c < NCOL; ++c) carry_a[c] = carry_b[c] = 0.0;
-  for (int ez = max(ez0 - 1, 0); ez < ez1; ++ez) {
-    const bool warm = ez < ez0;
-    const bool top = (ez == Nz - 1);
-#pragma unroll
-    for (int c = 0; c < NCOL; ++c) {
-      const int col = threadIdx.x + c * 256;
-      if (col >= RXn * RYn) continue;
-      const int ix = col % RXn, iy = col / RXn;
-      const int gx = xr0 + ix, gy = yr0 + iy;
-      double u[P + 1];
-      if (gx >= 0 && gy >= 0) {
-        const double* base = U + gx + (size_t)nx * gy + pl * (size_t)(ez * P);
-#pragma unroll
-        for (int k = 0; k <= P; ++k) u[k] = base[pl * k];
-      } else {
-#pragma unroll
-        for (int k = 0; k <= P; ++k) u[k] = 0.0;
-      }
-      double aa[P + 1], bb[P + 1];
-#pragma unroll
-      for (int k = 0; k <= P; ++k) {
-        double s1 = 0.0, s2 = 0.0;
-#pragma unroll
-        for (int m = 0; m <= P; ++m) {
-          s1 += c_Mh[k * (P + 1) + m] * u[m];
-          s2 += c_Kh[k * (P + 1) + m] * u[m];
-        }
-        aa[k] = s1;
-        bb[k] = s2;
-      }
-      if (!warm) {
-        const int o = iy * RX + ix;
-        sa[o] = aa[0] + carry_a[c];
-        sb[o] = bb[0] + carry_b[c];
-#pragma unroll
-        for (int k = 1; k < P; ++k) {
-          sa[k * RY * RX + o] = aa[k];
-          sb[k * RY * RX + o] = bb[k];
-        }
-        if (top) {
-          sa[P * RY * RX + o] = aa[P];
-          sb[P * RY * RX + o] = bb[P];
-        }
-      }
-      carry_a[c] = aa[P];
-      carry_b[c] = bb[P];
-    }
-    if (warm) continue;
-    __syncthreads();
-    const int np = top ? P + 1 : P;
-    // y pass: sm = M_y sa ; st = s1 K_y sa + s2 M_y sb
-    for (int t = threadIdx.x; t < np * OY * RXn; t += blockDim.x) {
-      const int ix = t % RXn;
-      const int rest = t / RXn;
-      const int oy = rest % OY, k = rest / OY;
-      const int gy = y0 + oy;
-      const double* A = sa + k * RY * RX + ix;
-      const double* B = sb + k * RY * RX + ix;
-      auto fa = [&](int j) { return A[(j - yr0) * RX]; };
-      auto fb = [&](int j) { return B[(j - yr0) * RX]; };
-      sm[(k * TY + oy) * RX + ix] = op1d<P>(c_Mh, gy, e.N[1], fa);
-      st[(k * TY + oy) * RX + ix] = e.s[1] * op1d<P>(c_Kh, gy, e.N[1], fa) + e.s[2] * op1d<P>(c_Mh, gy, e.N[1], fb);
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < np * OY * OX; t += blockDim.x) {
-      const int ox = t % OX;
-      const int rest = t / OX;
-      const int oy = rest % OY, k = rest / OY;
-      const int gx = x0 + ox, gy = y0 + oy, gz = ez * P + k;
-      const size_t g = gx + (size_t)nx * gy + pl * gz;
-      if (nt[g] != 1) continue;
-      const double* M = sm + (k * TY + oy) * RX;
-      const double* T = st + (k * TY + oy) * RX;
-      const double r = e.s[0] * op1d<P>(c_Kh, gx, e.N[0], [&](int j) { return M[j - xr0]; }) +
-                       op1d<P>(c_Mh, gx, e.N[0], [&](int j) { return T[j - xr0]; });
-      const double u = U[g];
-      const double res = e.a1 * u + e.a2 * Pv[g] -
-                         e.coefR * r / (wt(gx, e.N[0], P) * wt(gy, e.N[1], P) * wt(gz, Nz, P));
-      out[g] = res;
-      if (!isfinite(res)) atomicExch(flag, 1);
-    }
-    __syncthreads();
-  }
 }
 
 #include "explicit3d.cuh"
@@ -415,19 +270,37 @@ __global__ void k_scatter(const double* __restrict__ in, const int64_t* __restri
 
 // ------------------------------------------------------------------ launch helpers
 template <int P> struct Tile2 { static constexpr int E = P <= 4 ? 8 : 4; };
-constexpr int EX3 = 4, EY3 = 4, EZ3 = 8;
+
+// tile extents (elements) of the explicit kernel for this p / dim: ext[k] elements per tile
+// along k, tg[k] tiles along k
+template <int P>
+void tiling_p(const GridP& g, int ext[3], int tg[3]) {
+  ext[0] = ext[1] = ext[2] = 1;
+  if (g.dim == 2) {
+    ext[0] = ext[1] = Tile2v<P>::E;
+  } else if (g.dim == 3) {
+    if constexpr (P <= 6) {
+      ext[0] = ext[1] = Tile3<P>::E;
+      ext[2] = Tile3<P>::EZ;
+    }
+  }
+  for (int k = 0; k < 3; ++k) tg[k] = (g.N[k] + ext[k] - 1) / ext[k];
+}
 
 template <int P>
-void launch_explicit_p(sc_ctx* c, const double* U, const double* Pv, double* out, const ExpP& e) {
+void launch_explicit_p(sc_ctx* c, const double* U, const double* Pv, double* out, ExpP e, int n_tiles,
+                       cudaStream_t st) {
   const GridP& g = c->g;
+  int ext[3], tg[3];
+  tiling_p<P>(g, ext, tg);
+  e.tg[0] = tg[0];
+  e.tg[1] = tg[1];
   if (g.dim == 1) {
-    k_explicit_1d<P><<<(unsigned)((g.nl[0] + 255) / 256), 256, 0, c->stream>>>(U, Pv, out, c->d_ntype, e,
-                                                                                c->d_flag);
+    k_explicit_1d<P><<<(unsigned)((g.nl[0] + 255) / 256), 256, 0, st>>>(U, Pv, out, c->d_ntype, e, c->d_flag);
   } else if (g.dim == 2) {
     constexpr int E2 = Tile2v<P>::E;
-    dim3 grid((g.N[0] + E2 - 1) / E2, (g.N[1] + E2 - 1) / E2);
-    k_explicit_2d<P, E2, E2, Tile2v<P>::NT><<<grid, Tile2v<P>::NT, 0, c->stream>>>(U, Pv, out, c->d_ntype, e,
-                                                                                   c->d_flag);
+    dim3 grid = e.tiles ? dim3(n_tiles) : dim3(tg[0], tg[1]);
+    k_explicit_2d<P, E2, E2, Tile2v<P>::NT><<<grid, Tile2v<P>::NT, 0, st>>>(U, Pv, out, c->d_ntype, e, c->d_flag);
   } else {
     if constexpr (P <= 6) {
       using T = Tile3<P>;
@@ -437,97 +310,188 @@ void launch_explicit_p(sc_ctx* c, const double* U, const double* Pv, double* out
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::smem);
         attr = true;
       }
-      dim3 grid((g.N[0] + T::E - 1) / T::E, (g.N[1] + T::E - 1) / T::E, (g.N[2] + T::EZ - 1) / T::EZ);
-      kern<<<grid, T::NT, T::smem, c->stream>>>(U, Pv, out, c->d_ntype, e, c->d_flag);
+      dim3 grid = e.tiles ? dim3(n_tiles) : dim3(tg[0], tg[1], tg[2]);
+      kern<<<grid, T::NT, T::smem, st>>>(U, Pv, out, c->d_ntype, e, c->d_flag);
     }
   }
 }
 
-void launch_explicit(sc_ctx* c, const double* U, const double* Pv, double* out, double a1, double a2, double a3) {
+}  // namespace
+
+void explicit_tiling(const GridP& g, int ext[3], int tg[3]) {
+  switch (g.p) {
+    case 1: tiling_p<1>(g, ext, tg); break;
+    case 2: tiling_p<2>(g, ext, tg); break;
+    case 3: tiling_p<3>(g, ext, tg); break;
+    case 4: tiling_p<4>(g, ext, tg); break;
+    case 5: tiling_p<5>(g, ext, tg); break;
+    case 6: tiling_p<6>(g, ext, tg); break;
+    case 7: tiling_p<7>(g, ext, tg); break;
+    case 8: tiling_p<8>(g, ext, tg); break;
+    default: throw ScError(SC_ERR_CONFIG, "p out of range");
+  }
+}
+
+// (a1)+(a2) on the lattice nodes of type `want` (1: tensor-d far from c nodes, 4: tensor-d
+// sharing an element with a c node).  want 4 runs over the near-tile list only.
+void launch_explicit(sc_ctx* c, const double* U, const double* Pv, double* out, double a1, double a2, double a3,
+                     int want, cudaStream_t st) {
   const GridP& g = c->g;
   ExpP e;
-
   for (int k = 0; k < 3; ++k) {
     e.nl[k] = (int)g.nl[k];
     e.N[k] = g.N[k];
     e.s[k] = k < g.dim ? (2.0 / g.h[k]) * (2.0 / g.h[k]) : 0.0;
   }
-
   e.a1 = a1;
   e.a2 = a2;
   e.coefR = a3 * c->c * c->c;
+  e.want = want;
+  e.tiles = nullptr;
+  int n_tiles = 0;
+  if (want == 4) {
+    if (c->n_near == 0) return;
+    if (g.dim > 1) {
+      e.tiles = c->d_near_tiles;
+      n_tiles = c->n_near_tiles;
+    }
+  }
   switch (g.p) {
-    case 1: launch_explicit_p<1>(c, U, Pv, out, e); break;
-    case 2: launch_explicit_p<2>(c, U, Pv, out, e); break;
-    case 3: launch_explicit_p<3>(c, U, Pv, out, e); break;
-    case 4: launch_explicit_p<4>(c, U, Pv, out, e); break;
-    case 5: launch_explicit_p<5>(c, U, Pv, out, e); break;
-    case 6: launch_explicit_p<6>(c, U, Pv, out, e); break;
-    case 7: launch_explicit_p<7>(c, U, Pv, out, e); break;
-    case 8: launch_explicit_p<8>(c, U, Pv, out, e); break;
+    case 1: launch_explicit_p<1>(c, U, Pv, out, e, n_tiles, st); break;
+    case 2: launch_explicit_p<2>(c, U, Pv, out, e, n_tiles, st); break;
+    case 3: launch_explicit_p<3>(c, U, Pv, out, e, n_tiles, st); break;
+    case 4: launch_explicit_p<4>(c, U, Pv, out, e, n_tiles, st); break;
+    case 5: launch_explicit_p<5>(c, U, Pv, out, e, n_tiles, st); break;
+    case 6: launch_explicit_p<6>(c, U, Pv, out, e, n_tiles, st); break;
+    case 7: launch_explicit_p<7>(c, U, Pv, out, e, n_tiles, st); break;
+    case 8: launch_explicit_p<8>(c, U, Pv, out, e, n_tiles, st); break;
     default: throw ScError(SC_ERR_CONFIG, "p out of range");
   }
   SC_CUDA(cudaGetLastError());
 }
 
-}  // namespace
-
-static void launch_celem(sc_ctx* c, int mode, const double* A, const double* B) {
+static void launch_celem(sc_ctx* c, int mode, const double* A, const double* B, cudaStream_t st) {
   if (c->n_celem == 0) return;
   const int nb = c->nb;
   const int tpe = std::min(256, ((nb + 31) / 32) * 32);
   const int epb = 256 / tpe;
   const unsigned blocks = (unsigned)((c->n_celem + epb - 1) / epb);
-  k_celem<<<blocks, epb * tpe, sizeof(double) * epb * nb, c->stream>>>(
+  k_celem<<<blocks, epb * tpe, sizeof(double) * epb * nb, st>>>(
       mode, A, B, c->d_vc, c->d_ac, c->dt, c->d_celem_cell, c->d_celem_kidx, c->d_celem_cidx, c->d_Kcut,
       c->d_Kref, c->d_Y, (int)c->n_celem, nb, tpe, c->g);
   SC_CUDA(cudaGetLastError());
 }
 
 static void launch_irregular(sc_ctx* c, const double* U, const double* Pv, double* out, double a1, double a2,
-                             double a3) {
+                             double a3, cudaStream_t st) {
   if (c->n_irr == 0) return;
-  k_irregular<<<(unsigned)((c->n_irr * 32 + 127) / 128), 128, 0, c->stream>>>(
+  k_irregular<<<(unsigned)((c->n_irr * 32 + 127) / 128), 128, 0, st>>>(
       U, Pv, out, c->d_irr_lat, c->d_irr_invm, c->d_irr_fx, (int)c->n_irr, c->d_cell_class, c->d_Kref, c->g,
       c->d_ft, c->n_t, c->d_step, a1, a2, a3, c->d_flag);
   SC_CUDA(cudaGetLastError());
 }
 
-// one Newmark IMEX step: u_n in d_u[parity], writes u_{n+1} into d_u[parity^1]
-void enqueue_step(sc_ctx* c, int parity) {
-  const double* A = c->d_u[parity];
-  double* B = c->d_u[parity ^ 1];
+// (a3)-(a6) of one step on stream st: predictor fused into the c-element products, r^c,
+// the implicit solve S a^c_{n+1} = r^c, the corrector; then the device step counter.
+static void enqueue_c_part(sc_ctx* c, const double* A, double* B, cudaStream_t st) {
   const double dt = c->dt;
-  // (a1)+(a2): explicit CDM on d DOFs
-  launch_explicit(c, A, B, B, 2.0, -1.0, dt * dt);
-  launch_irregular(c, A, B, B, 2.0, -1.0, dt * dt);
   if (c->n_c > 0) {
-    // (a3)+(a4): predictor fused into the c-element products, then r^c
-    launch_celem(c, 0, A, B);
-    k_crhs<<<(unsigned)((c->n_c + 255) / 256), 256, 0, c->stream>>>(c->d_b, c->d_fxc, c->d_rhs_ptr, c->d_rhs_idx,
-                                                                     c->d_Y, (int)c->n_c, c->d_ft, c->n_t,
-                                                                     c->d_step, 1, c->fS.d);
-    // (a5): S a^c_{n+1} = r^c
-    launch_solve(c, c->fS);
-    // (a6)
-    k_corrector<<<(unsigned)((c->n_c + 255) / 256), 256, 0, c->stream>>>(A, B, c->d_vc, c->d_ac, c->d_x,
-                                                                         c->d_c_lat, (int)c->n_c, dt, c->d_flag, c->fS.d);
+    launch_celem(c, 0, A, B, st);
+    k_crhs<<<(unsigned)((c->n_c + 255) / 256), 256, 0, st>>>(c->d_b, c->d_fxc, c->d_rhs_ptr, c->d_rhs_idx, c->d_Y,
+                                                             (int)c->n_c, c->d_ft, c->n_t, c->d_step, 1, c->fS.d);
+    launch_solve(c, c->fS, st);
+    k_corrector<<<(unsigned)((c->n_c + 255) / 256), 256, 0, st>>>(A, B, c->d_vc, c->d_ac, c->d_x, c->d_c_lat,
+                                                                 (int)c->n_c, dt, c->d_flag, c->fS.d);
   }
-  k_advance<<<1, 1, 0, c->stream>>>(c->d_step);
+  k_advance<<<1, 1, 0, st>>>(c->d_step);
   SC_CUDA(cudaGetLastError());
 }
 
+// One Newmark IMEX step: u_n in d_u[parity], writes u_{n+1} into d_u[parity^1].
+// Without c DOFs: the explicit update of every d node, then the step counter.
+// With c DOFs the step is pipelined across steps: the far-d update of step
+// n (type 1: no c node in any incident element) was already done by the previous graph;
+// this graph does the near-d (type 4) and irregular updates of step n, then forks
+//   stream s_hi (high priority): c part of step n  (reads u^c_n, u^d_{n+1}; writes u^c_{n+1})
+//   stream st:                   far-d update of step n+1 (reads u_{n+1} at d nodes only,
+//                                u_n at its own nodes; writes u_{n+2} at far-d nodes)
+// which touch disjoint data, and joins them.
+void enqueue_step(sc_ctx* c, int parity, cudaStream_t st) {
+  double* A = c->d_u[parity];
+  double* B = c->d_u[parity ^ 1];
+  const double dt = c->dt;
+  if (c->n_c == 0) {
+    launch_explicit(c, A, B, B, 2.0, -1.0, dt * dt, 1, st);
+    launch_irregular(c, A, B, B, 2.0, -1.0, dt * dt, st);
+    enqueue_c_part(c, A, B, st);
+    return;
+  }
+  launch_explicit(c, A, B, B, 2.0, -1.0, dt * dt, 4, st);
+  launch_irregular(c, A, B, B, 2.0, -1.0, dt * dt, st);
+  SC_CUDA(cudaEventRecord(c->ev_fork, st));
+  SC_CUDA(cudaStreamWaitEvent(c->s_hi, c->ev_fork, 0));
+  enqueue_c_part(c, A, B, c->s_hi);
+  SC_CUDA(cudaEventRecord(c->ev_join, c->s_hi));
+  launch_explicit(c, B, A, A, 2.0, -1.0, dt * dt, 1, st);   // far-d nodes of step n+1
+  SC_CUDA(cudaStreamWaitEvent(st, c->ev_join, 0));
+}
+
+// far-d update of the current step (type 1 nodes) when no previous graph did it
+void enqueue_far_prologue(sc_ctx* c) {
+  if (c->n_c == 0 || c->far_ready) return;
+  const double* A = c->d_u[c->cur];
+  double* B = c->d_u[c->cur ^ 1];
+  launch_explicit(c, A, B, B, 2.0, -1.0, c->dt * c->dt, 1, c->stream);
+  c->far_ready = true;
+}
+
 void build_graphs(sc_ctx* c) {
+  if (!c->s_hi) {
+    int lo = 0, hi = 0;
+    SC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    SC_CUDA(cudaStreamCreateWithPriority(&c->s_hi, cudaStreamNonBlocking, hi));
+    SC_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    SC_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  }
   for (int par = 0; par < 2; ++par) {
     cudaGraph_t gr;
     SC_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    enqueue_step(c, par);
+    enqueue_step(c, par, c->stream);
     SC_CUDA(cudaStreamEndCapture(c->stream, &gr));
     SC_CUDA(cudaGraphInstantiate(&c->graph[par], gr, 0));
     cudaGraphDestroy(gr);
   }
-  c->kernels_per_step = 1 + (c->n_irr > 0) + 1;
+  // kernels per step: explicit (far) + near + irregular + advance + c part
+  c->kernels_per_step = 1 + (c->n_near > 0 ? 1 : 0) + (c->n_irr > 0) + 1;
   if (c->n_c > 0) c->kernels_per_step += 3 + (c->n_items > 0 ? 1 : 0);
+}
+
+// near-d tile list: tiles of the explicit kernel that own at least one type-4 node (a tile
+// owns nodes [ext*P*t, ext*P*(t+1)) per axis, the last tile also the final boundary node)
+void setup_step_structures(sc_ctx* c) {
+  const GridP& g = c->g;
+  c->n_near_tiles = 0;
+  if (c->n_near == 0 || g.dim == 1) return;
+  int ext[3], tg[3];
+  explicit_tiling(g, ext, tg);
+  std::vector<uint8_t> mark((size_t)tg[0] * tg[1] * tg[2], 0);
+  for (int64_t L = 0; L < c->n_lat; ++L) {
+    if (c->ntype[L] != 4) continue;
+    int64_t r = L;
+    int64_t t[3] = {0, 0, 0};
+    for (int k = 0; k < g.dim; ++k) {
+      const int64_t i = r % g.nl[k];
+      r /= g.nl[k];
+      t[k] = std::min<int64_t>(i / ((int64_t)ext[k] * g.p), tg[k] - 1);
+    }
+    mark[t[0] + (size_t)tg[0] * (t[1] + (size_t)tg[1] * t[2])] = 1;
+  }
+  std::vector<int> tiles;
+  for (size_t i = 0; i < mark.size(); ++i)
+    if (mark[i]) tiles.push_back((int)i);
+  c->n_near_tiles = (int)tiles.size();
+  SC_CUDA(cudaMalloc(&c->d_near_tiles, sizeof(int) * std::max<size_t>(1, tiles.size())));
+  SC_CUDA(cudaMemcpy(c->d_near_tiles, tiles.data(), sizeof(int) * tiles.size(), cudaMemcpyHostToDevice));
 }
 
 void device_upload_reference(sc_ctx* c) {
@@ -582,14 +546,15 @@ void run_startup(sc_ctx* c, const double* u0, const double* v0) {
   // d part: B = u0 - dt v0 + dt^2/2 a0  (P = v0 lattice, or A with a2 = 0 when v0 == 0)
   const double* Pv = vlat ? vlat : A;
   const double a2 = vlat ? -dt : 0.0;
-  launch_explicit(c, A, Pv, B, 1.0, a2, 0.5 * dt * dt);
-  launch_irregular(c, A, Pv, B, 1.0, a2, 0.5 * dt * dt);
+  launch_explicit(c, A, Pv, B, 1.0, a2, 0.5 * dt * dt, 1, c->stream);
+  launch_explicit(c, A, Pv, B, 1.0, a2, 0.5 * dt * dt, 4, c->stream);
+  launch_irregular(c, A, Pv, B, 1.0, a2, 0.5 * dt * dt, c->stream);
   if (c->n_c > 0) {
-    launch_celem(c, 1, A, A);
+    launch_celem(c, 1, A, A, c->stream);
     k_crhs<<<(unsigned)((c->n_c + 255) / 256), 256, 0, c->stream>>>(c->d_b, c->d_fxc, c->d_rhs_ptr, c->d_rhs_idx,
                                                                      c->d_Y, (int)c->n_c, c->d_ft, c->n_t,
                                                                      c->d_step, 0, c->fM.d);
-    launch_solve(c, c->fM);
+    launch_solve(c, c->fM, c->stream);
     k_start_c<<<(unsigned)((c->n_c + 255) / 256), 256, 0, c->stream>>>(c->d_ac, c->d_vc, c->d_x, vlat, c->d_c_lat,
                                                                         (int)c->n_c, c->fM.d);
   }
@@ -597,13 +562,16 @@ void run_startup(sc_ctx* c, const double* u0, const double* v0) {
   SC_CUDA(cudaStreamSynchronize(c->stream));
   if (vlat) cudaFree(vlat);
   c->host_step = 0;
+  c->far_ready = false;
 }
 
 // instrumentation (sc_profile): one launch of a single sub-kernel on the context stream
 void profile_launch(sc_ctx* c, int which) {
   const double* A = c->d_u[c->cur];
   double* B = c->d_u[c->cur ^ 1];
-  if (which == 0) launch_explicit(c, A, B, B, 2.0, -1.0, c->dt * c->dt);
-  else if (which == 1) launch_celem(c, 0, A, B);
-  else launch_solve(c, c->fS);
+  c->far_ready = false;
+  if (which == 0) launch_explicit(c, A, B, B, 2.0, -1.0, c->dt * c->dt, 1, c->stream);
+  else if (which == 1) launch_celem(c, 0, A, B, c->stream);
+  else if (which == 2) launch_solve(c, c->fS, c->stream);
+  else launch_explicit(c, A, B, B, 2.0, -1.0, c->dt * c->dt, 4, c->stream);
 }
