@@ -92,9 +92,14 @@ typedef struct {
 } sc_source;
 
 /* Distribution: NULL => one GPU (current device, current stream semantics below).
- * rank/world: slab decomposition over world ranks (NCCL over NVLink); device: CUDA
- * device ordinal; nccl_unique_id: 128-byte ncclUniqueId shared by all ranks (world>1);
- * cuda_stream: cudaStream_t to enqueue on (NULL => the context creates its own). */
+ * rank/world: slab decomposition over world ranks (z-slabs of whole element
+ * layers, cost-weighted; each c component owned by one rank; one point-to-point exchange per
+ * step); device: CUDA device ordinal; nccl_unique_id: 128-byte ncclUniqueId shared by all
+ * ranks (sc_nccl_unique_id on one rank, broadcast by the caller) -> one process per GPU, the
+ * exchange runs inside sc_step over NCCL (NVLink/NVSwitch); NULL with world > 1 => ranks
+ * living in ONE process (validation on one GPU): the caller alternates sc_step(ctx_r, 1) on
+ * every rank with sc_exchange_local; cuda_stream: cudaStream_t to enqueue on (NULL => the
+ * context creates its own). */
 typedef struct {
   int32_t rank;
   int32_t world;
@@ -126,6 +131,10 @@ typedef struct {
                                        DOFs overlap it) */
   double bytes_solve_per_step;      /* algorithmic HBM bytes of the implicit solve (a5) */
   double bytes_celem_per_step;      /* ... of the c-element products (a3)+(a4) */
+  int32_t rank, world;              /* this context's rank in the slab decomposition */
+  int64_t n_c_local;                /* c DOFs of this rank's components (its implicit solve) */
+  int64_t halo_send, halo_recv;     /* values sent / received per step by the exchange */
+  int64_t n_owned;                  /* DOFs owned by this rank (sc_read_owned writes these) */
 } sc_info;
 
 /* Build the discretisation, classify cells and DOFs, integrate the cut cells, factor
@@ -151,8 +160,22 @@ sc_status sc_step(sc_ctx* ctx, int64_t n);
 /* Wait for all enqueued work; SC_ERR_NUMERIC if a non-finite value was produced. */
 sc_status sc_sync(sc_ctx* ctx);
 
-/* Copy u_n (canonical order) to the host array u of length len >= n_dof.  Synchronises. */
+/* Copy u_n (canonical order) to the host array u of length len >= n_dof.  Synchronises.
+ * world > 1 over NCCL: collective, every rank receives the whole field. */
 sc_status sc_read(sc_ctx* ctx, double* u, int64_t len);
+
+/* Write the DOFs THIS rank owns (canonical order positions) into the host array u (len >=
+ * n_dof); other entries are left untouched.  With world == 1 this is sc_read.  The owned sets
+ * of all ranks partition the DOFs, so the ranks' outputs combined give u_n. */
+sc_status sc_read_owned(sc_ctx* ctx, double* u, int64_t len);
+
+/* In-process ranks (world > 1, no NCCL id): after every rank's sc_step(ctx_r, 1), copy each
+ * rank's packed values to its peers and unpack them (device copies; synchronises all ranks'
+ * streams).  ctxs[r] must be rank r. */
+sc_status sc_exchange_local(sc_ctx* const* ctxs, int32_t world);
+
+/* A new 128-byte ncclUniqueId (world > 1 over NCCL; call on one rank and broadcast). */
+sc_status sc_nccl_unique_id(void* out128);
 
 /* Copy v^c_n and a^c_n of the c DOFs (canonical order of I_c) to host arrays (nullable). */
 sc_status sc_read_c_state(sc_ctx* ctx, double* v_c, double* a_c, int64_t len);

@@ -53,11 +53,14 @@ class sc_info(ctypes.Structure):
                 ("bytes_per_step", ctypes.c_double), ("bytes_explicit_per_step", ctypes.c_double),
                 ("kernels_per_step", ctypes.c_int32), ("lattice_nodes", ctypes.c_int64),
                 ("setup_seconds", ctypes.c_double), ("n_near", ctypes.c_int64),
-                ("bytes_solve_per_step", ctypes.c_double), ("bytes_celem_per_step", ctypes.c_double)]
+                ("bytes_solve_per_step", ctypes.c_double), ("bytes_celem_per_step", ctypes.c_double),
+                ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("n_c_local", ctypes.c_int64),
+                ("halo_send", ctypes.c_int64), ("halo_recv", ctypes.c_int64), ("n_owned", ctypes.c_int64)]
 
 
-EXPORTS = ("sc_setup", "sc_set_state", "sc_step", "sc_sync", "sc_read", "sc_read_c_state", "sc_query",
-           "sc_read_classification", "sc_dof_coords", "sc_profile", "sc_last_error", "sc_destroy")
+EXPORTS = ("sc_setup", "sc_set_state", "sc_step", "sc_sync", "sc_read", "sc_read_owned", "sc_read_c_state",
+           "sc_query", "sc_read_classification", "sc_dof_coords", "sc_profile", "sc_exchange_local",
+           "sc_nccl_unique_id", "sc_last_error", "sc_destroy")
 
 _lib = None
 
@@ -78,6 +81,9 @@ def load_library(path=LIB_PATH):
     lib.sc_step.argtypes = [ctypes.c_void_p, ctypes.c_int64]
     lib.sc_sync.argtypes = [ctypes.c_void_p]
     lib.sc_read.argtypes = [ctypes.c_void_p, P(ctypes.c_double), ctypes.c_int64]
+    lib.sc_read_owned.argtypes = [ctypes.c_void_p, P(ctypes.c_double), ctypes.c_int64]
+    lib.sc_exchange_local.argtypes = [P(ctypes.c_void_p), ctypes.c_int32]
+    lib.sc_nccl_unique_id.argtypes = [ctypes.c_void_p]
     lib.sc_read_c_state.argtypes = [ctypes.c_void_p, P(ctypes.c_double), P(ctypes.c_double), ctypes.c_int64]
     lib.sc_query.argtypes = [ctypes.c_void_p, P(sc_info)]
     lib.sc_read_classification.argtypes = [ctypes.c_void_p, P(ctypes.c_int8), P(ctypes.c_uint8),
@@ -108,7 +114,8 @@ def _dptr(a):
 class Solver:
     """One context of the library (sc_setup ... sc_destroy)."""
 
-    def __init__(self, grid, p, alpha, geometry, dt, source=None, u0=None, v0=None, stream=None, device=None):
+    def __init__(self, grid, p, alpha, geometry, dt, source=None, u0=None, v0=None, stream=None, device=None,
+                 rank=0, world=1, nccl_id=None):
         lib = load_library()
         self._lib = lib
         dim = grid["dim"]
@@ -146,8 +153,12 @@ class Solver:
             src.n_t = len(ft)
             src.f_t = _dptr(ft)
         dist = None
-        if stream is not None or device is not None:
-            dist = sc_dist(0, 1, -1 if device is None else int(device), None,
+        self._nccl_id = None
+        if stream is not None or device is not None or world > 1:
+            if nccl_id is not None:
+                self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            dist = sc_dist(int(rank), int(world), -1 if device is None else int(device),
+                           ctypes.cast(self._nccl_id, ctypes.c_void_p) if self._nccl_id is not None else None,
                            ctypes.c_void_p(stream) if stream is not None else None)
         ctx = ctypes.c_void_p()
         u0a = None if u0 is None else np.ascontiguousarray(u0, dtype=np.float64)
@@ -186,6 +197,11 @@ class Solver:
         if out is None:
             out = np.empty(n, dtype=np.float64)
         self._check(self._lib.sc_read(self.ctx, _dptr(out), len(out)))
+        return out
+
+    def read_owned(self, out):
+        """Write the DOFs this rank owns into ``out`` (length n_dof; other entries untouched)."""
+        self._check(self._lib.sc_read_owned(self.ctx, _dptr(out), len(out)))
         return out
 
     def read_c_state(self):
@@ -230,7 +246,34 @@ class Solver:
             pass
 
 
-def from_config(cfg, f_t=None, stream=None, device=None, set_initial=True):
+def nccl_unique_id():
+    """A new ncclUniqueId (128 bytes) for a world > 1 group; broadcast it to every rank."""
+    lib = load_library()
+    buf = ctypes.create_string_buffer(128)
+    st = lib.sc_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p))
+    if st != SC_OK:
+        raise ScError(st, lib.sc_last_error(None).decode())
+    return buf.raw
+
+
+def exchange_local(solvers):
+    """In-process ranks: sc_exchange_local over the contexts (solvers[r] is rank r)."""
+    lib = load_library()
+    arr = (ctypes.c_void_p * len(solvers))(*[s.ctx.value for s in solvers])
+    st = lib.sc_exchange_local(arr, len(solvers))
+    if st != SC_OK:
+        raise ScError(st, lib.sc_last_error(solvers[0].ctx).decode())
+
+
+def read_group(solvers):
+    """In-process ranks: u_n assembled from every rank's owned DOFs."""
+    u = np.zeros(solvers[0].info["n_dof"])
+    for s in solvers:
+        s.read_owned(u)
+    return u
+
+
+def from_config(cfg, f_t=None, stream=None, device=None, set_initial=True, rank=0, world=1, nccl_id=None):
     """Build a Solver from an ``sc_inputs`` config dict (marshalling only)."""
     src = None
     if cfg.get("source") is not None:
@@ -239,7 +282,8 @@ def from_config(cfg, f_t=None, stream=None, device=None, set_initial=True):
             f_t = source_signal(cfg)
         src = {"x": cfg["source"]["x"], "f_t": f_t}
     geo = {k: cfg[k] for k in ("voids", "tree_depth", "lattice_s", "fill_eps", "rho", "c")}
-    s = Solver(cfg, cfg["p"], cfg["alpha"], geo, cfg["dt"], source=src, stream=stream, device=device)
+    s = Solver(cfg, cfg["p"], cfg["alpha"], geo, cfg["dt"], source=src, stream=stream, device=device,
+               rank=rank, world=world, nccl_id=nccl_id)
     s._n_cells = int(np.prod(cfg["cells"]))
     if set_initial and cfg.get("u0") == "gaussian_pulse":
         from sc_inputs import gaussian_pulse

@@ -11,7 +11,7 @@ BUILD = os.path.join(HERE, "_build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU = ["setup.cu", "step.cu", "solve.cu"]
-CPP = ["rules.cpp", "factor.cpp", "api.cpp"]
+CPP = ["rules.cpp", "factor.cpp", "partition.cpp", "nccl.cpp", "api.cpp"]
 
 
 def _run(cmd):
@@ -52,7 +52,7 @@ def build(force=False, verbose=False):
                           "-c", os.path.join(CSRC, f), "-o", o]))
         objs.append(o)
     tmp = OUT + ".tmp"
-    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-Xcompiler", "-fopenmp", "-lgomp"])
+    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-Xcompiler", "-fopenmp", "-lgomp", "-ldl"])
     os.replace(tmp, OUT)
     if verbose:
         print("\n".join(logs))

@@ -42,6 +42,10 @@ static void free_ctx(sc_ctx* c) {
   cudaGetDevice(&cur);
   cudaSetDevice(c->device);
   dump_trace(c);
+  try {
+    nccl_destroy(c);
+  } catch (const ScError&) {
+  }
   for (int i = 0; i < 2; ++i)
     if (c->graph[i]) cudaGraphExecDestroy(c->graph[i]);
   void* ptrs[] = {c->d_voids, c->d_u[0], c->d_u[1], c->d_ntype, c->d_cell_class, c->d_dof_lat, c->d_out,
@@ -51,7 +55,8 @@ static void free_ctx(sc_ctx* c) {
                   c->d_rhs_idx, c->d_sn_c0, c->d_sn_w, c->d_sn_r, c->d_sn_aoff, c->d_sn_roff,
                   c->d_sn_uoff, c->d_sn_goff, c->d_R, c->d_gptr, c->d_gidx, c->d_items, c->fS.A,
                   c->fM.A, c->fS.d, c->fM.d, c->d_tmp, c->d_nitem, c->d_chptr, c->d_chidx, c->d_parent, c->d_solve_cnt,
-                  c->d_part, c->d_trace, c->d_near_tiles, c->d_qmeta};
+                  c->d_part, c->d_trace, c->d_near_tiles, c->d_qmeta, c->d_far_tiles, c->d_xs_idx, c->d_xr_idx,
+                  c->d_xs_buf, c->d_xr_buf, c->d_own_lat, c->d_own_dof, c->d_full};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -100,7 +105,12 @@ extern "C" sc_status sc_setup(const sc_grid* grid, int32_t p, double alpha, cons
     c->device = dist ? dist->device : -1;
     if (c->device < 0) SC_CUDA(cudaGetDevice(&c->device));
     SC_CUDA(cudaSetDevice(c->device));
-    if (dist && dist->world > 1) throw ScError(SC_ERR_CONFIG, "world > 1 is not supported by this build");
+    if (dist) {
+      if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)
+        throw ScError(SC_ERR_CONFIG, "dist: need 0 <= rank < world");
+      c->rank = dist->rank;
+      c->world = dist->world;
+    }
     if (dist && dist->cuda_stream) {
       c->stream = (cudaStream_t)dist->cuda_stream;
     } else {
@@ -182,12 +192,12 @@ extern "C" sc_status sc_setup(const sc_grid* grid, int32_t p, double alpha, cons
       const double ce = 8.0 * (double)c->n_cut * nbd * nbd + 16.0 * (double)c->n_celem * nbd;
       // solve: forward streams every panel [D_s; G_s], backward G_s again; b, q, x vectors
       // and the update vectors U (written once, read once)
-      const double so = 8.0 * (double)(c->nnz_factor + c->nnz_G) + 32.0 * (double)c->n_c + 16.0 * (double)c->sum_r;
+      const double so = 8.0 * (double)(c->nnz_factor + c->nnz_G) + 32.0 * (double)c->n_cl + 16.0 * (double)c->sum_r;
       c->bytes_explicit = ex;
       c->bytes_celem = ce;
       c->bytes_solve = so;
       c->bytes_per_step = ex + 24.0 * (double)(c->n_near + c->n_irr) + ce + so +
-                          56.0 * (double)c->n_c;   // r^c gather + corrector state (u, v, a, x)
+                          56.0 * (double)c->n_cl;   // r^c gather + corrector state (u, v, a, x)
     }
     if (u0 || v0) {
       double *du = nullptr, *dv = nullptr;
@@ -207,6 +217,7 @@ extern "C" sc_status sc_setup(const sc_grid* grid, int32_t p, double alpha, cons
       run_startup(c, nullptr, nullptr);
     }
     build_graphs(c);
+    if (c->world > 1 && dist->nccl_unique_id) nccl_init(c, dist->nccl_unique_id);
     SC_CUDA(cudaStreamSynchronize(c->stream));
     c->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *out = c;
@@ -255,9 +266,13 @@ extern "C" sc_status sc_step(sc_ctx* c, int64_t n) {
     SC_CUDA(cudaSetDevice(c->device));
     if (n > 0) enqueue_far_prologue(c);
     for (int64_t i = 0; i < n; ++i) {
-      SC_CUDA(cudaGraphLaunch(c->graph[c->cur], c->stream));
+      SC_CUDA(cudaGraphLaunch(c->graph[c->cur], c->stream));   // world > 1: ends with the pack
       c->cur ^= 1;
       ++c->host_step;
+      if (c->world > 1 && c->nccl_comm) {
+        nccl_exchange(c);
+        enqueue_unpack(c, c->d_u[c->cur], c->stream);
+      }
     }
     return SC_OK;
   } catch (const ScError& e) {
@@ -290,11 +305,94 @@ extern "C" sc_status sc_read(sc_ctx* c, double* u, int64_t len) {
   }
   try {
     SC_CUDA(cudaSetDevice(c->device));
-    gather_dofs(c, c->d_u[c->cur], c->d_out);
+    if (c->world > 1) {
+      // every DOF is owned by exactly one rank: sum of the owned parts = the field
+      if (!c->nccl_comm) {
+        c->err = "world > 1 without NCCL (in-process ranks): use sc_read_owned on every rank";
+        return SC_ERR_STATE;
+      }
+      SC_CUDA(cudaMemsetAsync(c->d_out, 0, sizeof(double) * c->n_dof, c->stream));
+      gather_owned(c, c->d_u[c->cur], c->d_out);
+      nccl_allreduce_sum(c, c->d_out, c->n_dof);
+    } else {
+      gather_dofs(c, c->d_u[c->cur], c->d_out);
+    }
     SC_CUDA(cudaMemcpyAsync(u, c->d_out, sizeof(double) * c->n_dof, cudaMemcpyDeviceToHost, c->stream));
     return sc_sync(c);
   } catch (const ScError& e) {
     return fail(c, e);
+  }
+}
+
+extern "C" sc_status sc_read_owned(sc_ctx* c, double* u, int64_t len) {
+  if (!c) return SC_ERR_STATE;
+  if (!u || len < c->n_dof) {
+    c->err = "output buffer too small";
+    return SC_ERR_CONFIG;
+  }
+  try {
+    SC_CUDA(cudaSetDevice(c->device));
+    if (c->world == 1) {
+      gather_dofs(c, c->d_u[c->cur], c->d_out);
+    } else {
+      SC_CUDA(cudaMemsetAsync(c->d_out, 0, sizeof(double) * c->n_dof, c->stream));
+      gather_owned(c, c->d_u[c->cur], c->d_out);
+    }
+    std::vector<double> tmp(c->n_dof);
+    SC_CUDA(cudaMemcpyAsync(tmp.data(), c->d_out, sizeof(double) * c->n_dof, cudaMemcpyDeviceToHost, c->stream));
+    const sc_status st = sc_sync(c);
+    if (c->world == 1) {
+      std::memcpy(u, tmp.data(), sizeof(double) * c->n_dof);
+    } else {
+      for (int32_t i : c->own_dofs) u[i] = tmp[i];
+    }
+    return st;
+  } catch (const ScError& e) {
+    return fail(c, e);
+  }
+}
+
+extern "C" sc_status sc_exchange_local(sc_ctx* const* ctxs, int32_t world) {
+  if (!ctxs || world < 1) return SC_ERR_STATE;
+  sc_ctx* c0 = ctxs[0];
+  try {
+    for (int r = 0; r < world; ++r) {
+      if (!ctxs[r] || ctxs[r]->world != world || ctxs[r]->rank != r || ctxs[r]->nccl_comm)
+        throw ScError(SC_ERR_CONFIG, "sc_exchange_local: ctxs[r] must be rank r of an in-process group");
+      if (ctxs[r]->host_step != c0->host_step) throw ScError(SC_ERR_STATE, "ranks at different steps");
+    }
+    for (int r = 0; r < world; ++r) {
+      SC_CUDA(cudaSetDevice(ctxs[r]->device));
+      SC_CUDA(cudaStreamSynchronize(ctxs[r]->stream));
+    }
+    for (int q = 0; q < world; ++q) {
+      sc_ctx* d = ctxs[q];
+      SC_CUDA(cudaSetDevice(d->device));
+      for (int r = 0; r < world; ++r) {
+        if (r == q) continue;
+        const sc_ctx* src = ctxs[r];
+        const int64_t n = d->xr_off[r + 1] - d->xr_off[r];
+        if (n != src->xs_off[q + 1] - src->xs_off[q]) throw ScError(SC_ERR_STATE, "exchange lists disagree");
+        if (n)
+          SC_CUDA(cudaMemcpyAsync(d->d_xr_buf + d->xr_off[r], src->d_xs_buf + src->xs_off[q], sizeof(double) * n,
+                                  cudaMemcpyDefault, d->stream));
+      }
+      enqueue_unpack(d, d->d_u[d->cur], d->stream);
+      SC_CUDA(cudaStreamSynchronize(d->stream));
+    }
+    return SC_OK;
+  } catch (const ScError& e) {
+    return fail(c0, e);
+  }
+}
+
+extern "C" sc_status sc_nccl_unique_id(void* out128) {
+  try {
+    nccl_unique_id(out128);
+    return SC_OK;
+  } catch (const ScError& e) {
+    g_setup_err = e.msg;
+    return e.st;
   }
 }
 
@@ -306,14 +404,14 @@ extern "C" sc_status sc_read_c_state(sc_ctx* c, double* v_c, double* a_c, int64_
   }
   try {
     SC_CUDA(cudaSetDevice(c->device));
-    std::vector<double> tmp(c->n_c);
+    std::vector<double> tmp(c->n_cl);
     for (int which = 0; which < 2; ++which) {
       double* dst = which == 0 ? v_c : a_c;
-      if (!dst || c->n_c == 0) continue;
-      SC_CUDA(cudaMemcpyAsync(tmp.data(), which == 0 ? c->d_vc : c->d_ac, sizeof(double) * c->n_c,
+      if (!dst || c->n_cl == 0) continue;
+      SC_CUDA(cudaMemcpyAsync(tmp.data(), which == 0 ? c->d_vc : c->d_ac, sizeof(double) * c->n_cl,
                               cudaMemcpyDeviceToHost, c->stream));
       SC_CUDA(cudaStreamSynchronize(c->stream));
-      for (int64_t i = 0; i < c->n_c; ++i) dst[c->c_canon[i]] = tmp[i];
+      for (int64_t i = 0; i < c->n_cl; ++i) dst[c->c_canon[i]] = tmp[i];
     }
     return SC_OK;
   } catch (const ScError& e) {
@@ -345,6 +443,12 @@ extern "C" sc_status sc_query(sc_ctx* c, sc_info* o) {
   o->setup_seconds = c->setup_seconds;
   o->n_near = c->n_near;
   o->bytes_solve_per_step = c->bytes_solve;
+  o->rank = c->rank;
+  o->world = c->world;
+  o->n_c_local = c->n_cl;
+  o->halo_send = c->xs_off.empty() ? 0 : c->xs_off.back();
+  o->halo_recv = c->xr_off.empty() ? 0 : c->xr_off.back();
+  o->n_owned = c->world > 1 ? (int64_t)c->own_dofs.size() : c->n_dof;
   o->bytes_celem_per_step = c->bytes_celem;
   return SC_OK;
 }

@@ -6,8 +6,9 @@
 #pragma once
 
 template <int P, int EX, int EY, int NT>
-__global__ void __launch_bounds__(NT) k_explicit_2d(const double* __restrict__ U, const double* Pv, double* out,
-                                                    const uint8_t* __restrict__ nt, ExpP e, int* flag) {
+__device__ __forceinline__ void explicit2d_tile(const double* __restrict__ U, const double* Pv, double* out,
+                                                const uint8_t* __restrict__ nt, const ExpP& e, int* flag,
+                                                const int3 tb) {
   constexpr int P1 = P + 1;
   constexpr int EXH = EX + 1, EYH = EY + 1;
   constexpr int RX = EXH * P + 1, RY = EYH * P + 1, TY = EY * P + 1;
@@ -19,7 +20,6 @@ __global__ void __launch_bounds__(NT) k_explicit_2d(const double* __restrict__ U
   const int tid = threadIdx.x;
   const int Nx = e.N[0], Ny = e.N[1];
   const int nx = e.nl[0];
-  const int3 tb = tile_of(e);
   const int ex0 = tb.x * EX, ey0 = tb.y * EY;
   const int ex1 = min(ex0 + EX, Nx), ey1 = min(ey0 + EY, Ny);
   const int nEX = ex1 - ex0, nEY = ey1 - ey0;
@@ -129,6 +129,15 @@ __global__ void __launch_bounds__(NT) k_explicit_2d(const double* __restrict__ U
         }
       }
     }
+  }
+}
+
+template <int P, int EX, int EY, int NT>
+__global__ void __launch_bounds__(NT) k_explicit_2d(const double* __restrict__ U, const double* Pv, double* out,
+                                                    const uint8_t* __restrict__ nt, ExpP e, int* flag) {
+  for (int tt = blockIdx.x; tt < e.ntiles; tt += gridDim.x) {
+    explicit2d_tile<P, EX, EY, NT>(U, Pv, out, nt, e, flag, tile_of(e, tt));
+    __syncthreads();   // shared tile buffers reused by the next tile
   }
 }
 

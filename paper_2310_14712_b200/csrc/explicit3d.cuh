@@ -39,10 +39,10 @@ __device__ __forceinline__ double inv_wt(int i, int e_cnt, int P) {
   return (e > 0 && e < e_cnt) ? c_iw2 : c_iw[0];
 }
 
-template <int P, int EX, int EY, int EZ, int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB) k_explicit_3d(const double* __restrict__ U, const double* Pv,
-                                                          double* out, const uint8_t* __restrict__ nt, ExpP e,
-                                                          int* flag) {
+template <int P, int EX, int EY, int EZ, int NT>
+__device__ __forceinline__ void explicit3d_tile(const double* __restrict__ U, const double* Pv, double* out,
+                                                const uint8_t* __restrict__ nt, const ExpP& e, int* flag,
+                                                const int3 tb) {
   constexpr int P1 = P + 1;
   constexpr int EXH = EX + 1, EYH = EY + 1;
   constexpr int RX = EXH * P + 1, RY = EYH * P + 1, TY = EY * P + 1;
@@ -62,7 +62,6 @@ __global__ void __launch_bounds__(NT, MINB) k_explicit_3d(const double* __restri
   const int Nx = e.N[0], Ny = e.N[1], Nz = e.N[2];
   const int nx = e.nl[0], ny = e.nl[1];
   const size_t pl = (size_t)nx * ny;
-  const int3 tb = tile_of(e);
   const int ex0 = tb.x * EX, ey0 = tb.y * EY, ez0 = tb.z * EZ;
   const int ex1 = min(ex0 + EX, Nx), ey1 = min(ey0 + EY, Ny), ez1 = min(ez0 + EZ, Nz);
   const int nEX = ex1 - ex0, nEY = ey1 - ey0;
@@ -270,12 +269,23 @@ __global__ void __launch_bounds__(NT, MINB) k_explicit_3d(const double* __restri
   }
 }
 
+// grid-stride loop over the tiles (a capped grid leaves SM resources to a concurrent kernel)
+template <int P, int EX, int EY, int EZ, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_explicit_3d(const double* __restrict__ U, const double* Pv,
+                                                          double* out, const uint8_t* __restrict__ nt, ExpP e,
+                                                          int* flag) {
+  for (int tt = blockIdx.x; tt < e.ntiles; tt += gridDim.x)
+    explicit3d_tile<P, EX, EY, EZ, NT>(U, Pv, out, nt, e, flag, tile_of(e, tt));
+}
+
+// tile shapes: the z+y phase has RX*(E+1) column items and the x phase (E*P+1) rows of
+// (E+1) lanes; NT is chosen so that both keep >= 84% of the threads busy (one item each)
 template <int P>
 struct Tile3 {
   static constexpr int E = P <= 2 ? 8 : (P == 3 ? 7 : (P == 4 ? 5 : 3));
   static constexpr int EZ = 8;
-  static constexpr int NT = 256;
-  static constexpr int MINB = P <= 4 ? 2 : 1;
+  static constexpr int NT = P == 3 ? 224 : (P == 4 ? 160 : 256);
+  static constexpr int MINB = P == 3 ? 2 : (P == 4 ? 3 : (P <= 2 ? 2 : 1));
   static constexpr int RX = (E + 1) * P + 1;
   static constexpr int TY = E * P + 1;
   static constexpr size_t smem =

@@ -356,9 +356,10 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   }
   c->n_dof = (int64_t)c->dof_lat.size();
   // irregular d nodes: lattice index, 1/M_i (lumped, non-empty incident cells), f_x
+  // (uploaded after the partition plan: each rank keeps the ones it updates)
+  std::vector<int32_t> ilat;
+  std::vector<double> iinv, ifx;
   {
-    std::vector<int32_t> ilat;
-    std::vector<double> iinv, ifx;
     std::vector<std::pair<int64_t, double>> srcs = src;
     std::sort(srcs.begin(), srcs.end());
     for (int64_t i = 0; i < c->n_lat; ++i) {
@@ -396,136 +397,207 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
                                  [](const std::pair<int64_t, double>& a, int64_t v) { return a.first < v; });
       ifx.push_back((it != srcs.end() && it->first == i) ? it->second : 0.0);
     }
-    c->n_irr = (int64_t)ilat.size();
-    if (c->n_irr) {
-      SC_CUDA(cudaMalloc(&c->d_irr_lat, sizeof(int32_t) * c->n_irr));
-      SC_CUDA(cudaMalloc(&c->d_irr_invm, sizeof(double) * c->n_irr));
-      SC_CUDA(cudaMalloc(&c->d_irr_fx, sizeof(double) * c->n_irr));
-      SC_CUDA(cudaMemcpy(c->d_irr_lat, ilat.data(), sizeof(int32_t) * c->n_irr, cudaMemcpyHostToDevice));
-      SC_CUDA(cudaMemcpy(c->d_irr_invm, iinv.data(), sizeof(double) * c->n_irr, cudaMemcpyHostToDevice));
-      SC_CUDA(cudaMemcpy(c->d_irr_fx, ifx.data(), sizeof(double) * c->n_irr, cudaMemcpyHostToDevice));
-    }
   }
-  SC_CUDA(cudaMemcpy(c->d_ntype, c->ntype.data(), c->n_lat, cudaMemcpyHostToDevice));
-  const int nc = (int)c->n_c;
+  int nc = (int)c->n_c;
+  int ne = 0;
+  std::vector<int> comp_id;
+  std::vector<std::vector<int>> comps;
   // canonical c index of a lattice node (binary search in clat)
   auto cidx_of = [&](int64_t lat) -> int {
     auto it = std::lower_bound(b.clat.begin(), b.clat.end(), lat);
     return (it != b.clat.end() && *it == lat) ? (int)(it - b.clat.begin()) : -1;
   };
-  // ---------------- c elements: cut cells + uncut cells with >= 1 c node
-  std::vector<uint8_t> mark;
-  {
-    std::vector<int64_t> cells;
-    for (int64_t lat : b.clat) {
-      int64_t ijk[3];
-      lat_ijk(g, lat, ijk);
-      int64_t e0[3], e1[3];
+  // c elements, node -> element lists and components of the current c set b.clat
+  auto build_c = [&](bool first) {
+    // ---------------- c elements: cut cells + uncut cells with >= 1 c node
+    std::vector<uint8_t> mark;
+    {
+      std::vector<int64_t> cells;
+      for (int64_t lat : b.clat) {
+        int64_t ijk[3];
+        lat_ijk(g, lat, ijk);
+        int64_t e0[3], e1[3];
+        for (int k = 0; k < 3; ++k) {
+          if (k < g.dim) {
+            if (ijk[k] % g.p == 0) {
+              e0[k] = ijk[k] / g.p - 1;
+              e1[k] = ijk[k] / g.p;
+            } else {
+              e0[k] = e1[k] = ijk[k] / g.p;
+            }
+            if (e0[k] < 0) e0[k] = e1[k];
+            if (e1[k] >= g.N[k]) e1[k] = e0[k];
+          } else {
+            e0[k] = e1[k] = 0;
+          }
+        }
+        for (int64_t a2 = e0[2]; a2 <= e1[2]; ++a2)
+          for (int64_t a1 = e0[1]; a1 <= e1[1]; ++a1)
+            for (int64_t a0 = e0[0]; a0 <= e1[0]; ++a0) {
+              int64_t ci[3] = {a0, a1, a2};
+              int64_t cl = cell_lin(g, ci);
+              if (c->cell_class[cl] != 2) cells.push_back(cl);
+            }
+      }
+      std::sort(cells.begin(), cells.end());
+      cells.erase(std::unique(cells.begin(), cells.end()), cells.end());
+      b.celem_cell = cells;
+    }
+    ne = (int)b.celem_cell.size();
+    c->n_celem = ne;
+    b.celem_kidx.assign(ne, -1);
+    b.celem_cidx.assign((size_t)ne * nb, -1);
+    for (int e = 0; e < ne; ++e) {
+      const int64_t cl = b.celem_cell[e];
+      if (c->cell_class[cl] == 1) {
+        auto it = std::lower_bound(c->cut_cells.begin(), c->cut_cells.end(), (long long)cl);
+        b.celem_kidx[e] = (int)(it - c->cut_cells.begin());
+      }
+      int64_t ci[3];
+      int64_t t = cl;
       for (int k = 0; k < 3; ++k) {
         if (k < g.dim) {
-          if (ijk[k] % g.p == 0) {
-            e0[k] = ijk[k] / g.p - 1;
-            e1[k] = ijk[k] / g.p;
-          } else {
-            e0[k] = e1[k] = ijk[k] / g.p;
-          }
-          if (e0[k] < 0) e0[k] = e1[k];
-          if (e1[k] >= g.N[k]) e1[k] = e0[k];
+          ci[k] = t % g.N[k];
+          t /= g.N[k];
         } else {
-          e0[k] = e1[k] = 0;
+          ci[k] = 0;
         }
       }
-      for (int64_t a2 = e0[2]; a2 <= e1[2]; ++a2)
-        for (int64_t a1 = e0[1]; a1 <= e1[1]; ++a1)
-          for (int64_t a0 = e0[0]; a0 <= e1[0]; ++a0) {
-            int64_t ci[3] = {a0, a1, a2};
-            int64_t cl = cell_lin(g, ci);
-            if (c->cell_class[cl] != 2) cells.push_back(cl);
-          }
+      for (int loc = 0; loc < nb; ++loc) b.celem_cidx[(size_t)e * nb + loc] = cidx_of(elem_node(g, ci, loc, n1));
     }
-    std::sort(cells.begin(), cells.end());
-    cells.erase(std::unique(cells.begin(), cells.end()), cells.end());
-    b.celem_cell = cells;
-  }
-  const int ne = (int)b.celem_cell.size();
-  c->n_celem = ne;
-  b.celem_kidx.assign(ne, -1);
-  b.celem_cidx.assign((size_t)ne * nb, -1);
-  for (int e = 0; e < ne; ++e) {
-    const int64_t cl = b.celem_cell[e];
-    if (c->cell_class[cl] == 1) {
-      auto it = std::lower_bound(c->cut_cells.begin(), c->cut_cells.end(), (long long)cl);
-      b.celem_kidx[e] = (int)(it - c->cut_cells.begin());
-    }
-    int64_t ci[3];
-    int64_t t = cl;
-    for (int k = 0; k < 3; ++k) {
-      if (k < g.dim) {
-        ci[k] = t % g.N[k];
-        t /= g.N[k];
-      } else {
-        ci[k] = 0;
+    // near-d nodes (type 4): tensor-d nodes of uncut c elements, i.e. d nodes whose residual
+    // reads a c value; the step pipeline updates them after the c part (step.cu)
+    if (first) c->n_near = 0;
+    for (int e = 0; e < ne && first; ++e) {
+      if (b.celem_kidx[e] >= 0) continue;   // cut cell: all its nodes are c
+      int64_t ci[3];
+      int64_t t = b.celem_cell[e];
+      for (int k = 0; k < 3; ++k) {
+        if (k < g.dim) {
+          ci[k] = t % g.N[k];
+          t /= g.N[k];
+        } else {
+          ci[k] = 0;
+        }
+      }
+      for (int loc = 0; loc < nb; ++loc) {
+        const int64_t L = elem_node(g, ci, loc, n1);
+        if (c->ntype[L] == 1) {
+          c->ntype[L] = 4;
+          ++c->n_near;
+        }
       }
     }
-    for (int loc = 0; loc < nb; ++loc) b.celem_cidx[(size_t)e * nb + loc] = cidx_of(elem_node(g, ci, loc, n1));
-  }
-  // near-d nodes (type 4): tensor-d nodes of uncut c elements, i.e. d nodes whose residual
-  // reads a c value; the step pipeline updates them after the c part (step.cu)
-  c->n_near = 0;
-  for (int e = 0; e < ne; ++e) {
-    if (b.celem_kidx[e] >= 0) continue;   // cut cell: all its nodes are c
-    int64_t ci[3];
-    int64_t t = b.celem_cell[e];
-    for (int k = 0; k < 3; ++k) {
-      if (k < g.dim) {
-        ci[k] = t % g.N[k];
-        t /= g.N[k];
-      } else {
-        ci[k] = 0;
-      }
-    }
-    for (int loc = 0; loc < nb; ++loc) {
-      const int64_t L = elem_node(g, ci, loc, n1);
-      if (c->ntype[L] == 1) {
-        c->ntype[L] = 4;
-        ++c->n_near;
-      }
-    }
-  }
-  if (c->n_near) SC_CUDA(cudaMemcpy(c->d_ntype, c->ntype.data(), c->n_lat, cudaMemcpyHostToDevice));
-  // node -> (e, loc) lists, canonical order
-  b.node_eptr.assign(nc + 1, 0);
-  for (size_t q = 0; q < b.celem_cidx.size(); ++q)
-    if (b.celem_cidx[q] >= 0) ++b.node_eptr[b.celem_cidx[q] + 1];
-  for (int i = 0; i < nc; ++i) b.node_eptr[i + 1] += b.node_eptr[i];
-  b.node_eidx.resize(b.node_eptr[nc]);
-  {
-    std::vector<int> fill(b.node_eptr.begin(), b.node_eptr.end() - 1);
+    // node -> (e, loc) lists, canonical order
+    b.node_eptr.assign(nc + 1, 0);
     for (size_t q = 0; q < b.celem_cidx.size(); ++q)
-      if (b.celem_cidx[q] >= 0) b.node_eidx[fill[b.celem_cidx[q]]++] = (int)q;
-  }
-  // ---------------- components (union-find over c elements)
-  UF uf(std::max(nc, 1));
-  for (int e = 0; e < ne; ++e) {
-    int first = -1;
-    for (int loc = 0; loc < nb; ++loc) {
-      int ci = b.celem_cidx[(size_t)e * nb + loc];
-      if (ci < 0) continue;
-      if (first < 0) first = ci;
-      else uf.u(first, ci);
+      if (b.celem_cidx[q] >= 0) ++b.node_eptr[b.celem_cidx[q] + 1];
+    for (int i = 0; i < nc; ++i) b.node_eptr[i + 1] += b.node_eptr[i];
+    b.node_eidx.resize(b.node_eptr[nc]);
+    {
+      std::vector<int> fill(b.node_eptr.begin(), b.node_eptr.end() - 1);
+      for (size_t q = 0; q < b.celem_cidx.size(); ++q)
+        if (b.celem_cidx[q] >= 0) b.node_eidx[fill[b.celem_cidx[q]]++] = (int)q;
+    }
+    // ---------------- components (union-find over c elements)
+    UF uf(std::max(nc, 1));
+    for (int e = 0; e < ne; ++e) {
+      int first = -1;
+      for (int loc = 0; loc < nb; ++loc) {
+        int ci = b.celem_cidx[(size_t)e * nb + loc];
+        if (ci < 0) continue;
+        if (first < 0) first = ci;
+        else uf.u(first, ci);
+      }
+    }
+    comp_id.assign(nc, -1);
+    comps.clear();
+    for (int i = 0; i < nc; ++i) {
+      int r = uf.f(i);
+      if (comp_id[r] < 0) {
+        comp_id[r] = (int)comps.size();
+        comps.emplace_back();
+      }
+      comps[comp_id[r]].push_back(i);
+    }
+  };
+  build_c(true);
+  // ---------------- partition plan (world > 1; partition.cpp): component owners, regions
+  const std::vector<int64_t> clat_global = b.clat;
+  std::vector<int> c_owner(nc, 0);
+  {
+    const int ax = g.dim - 1;
+    int64_t plane = 1, per_layer = 1;
+    for (int k = 0; k < ax; ++k) {
+      plane *= g.nl[k];
+      per_layer *= g.N[k];
+    }
+    std::vector<CompSpan> spans(comps.size());
+    for (size_t k = 0; k < comps.size(); ++k) {
+      CompSpan sp{INT32_MAX, -1, 0, 0.0};
+      double zsum = 0.0;
+      for (int v : comps[k]) {
+        zsum += (double)(b.clat[v] / plane);
+        for (int q = b.node_eptr[v]; q < b.node_eptr[v + 1]; ++q) {
+          const int L = (int)(b.celem_cell[b.node_eidx[q] / nb] / per_layer);
+          sp.lmin = std::min(sp.lmin, L);
+          sp.lmax = std::max(sp.lmax, L);
+        }
+      }
+      sp.centroid = (int)(zsum / (double)comps[k].size() / g.p);
+      sp.cost = 4500.0 * (double)comps[k].size();   // ~2 sweeps x ~280 panel entries per c DOF
+      spans[k] = sp;
+    }
+    std::vector<int> owner;
+    plan_partition(c, spans, owner);
+    for (size_t k = 0; k < comps.size(); ++k)
+      for (int v : comps[k]) c_owner[v] = owner[k];
+    c->n_components = (int64_t)comps.size();
+    // node types this rank updates: d nodes of planes whose incident elements lie in its region
+    c->ntype_rank = c->ntype;
+    if (c->world > 1)
+      for (int64_t L = 0; L < c->n_lat; ++L) {
+        const uint8_t t = c->ntype[L];
+        if ((t == 1 || t == 2 || t == 4) && !region_computes_plane(c, c->rank, L / plane)) c->ntype_rank[L] = 0;
+      }
+    SC_CUDA(cudaMemcpy(c->d_ntype, c->ntype_rank.data(), c->n_lat, cudaMemcpyHostToDevice));
+    // irregular d nodes this rank updates
+    std::vector<int32_t> il;
+    std::vector<double> im, ifv;
+    for (size_t i = 0; i < ilat.size(); ++i)
+      if (c->ntype_rank[ilat[i]] == 2) {
+        il.push_back(ilat[i]);
+        im.push_back(iinv[i]);
+        ifv.push_back(ifx[i]);
+      }
+    c->n_irr = (int64_t)il.size();
+    if (c->n_irr) {
+      SC_CUDA(cudaMalloc(&c->d_irr_lat, sizeof(int32_t) * c->n_irr));
+      SC_CUDA(cudaMalloc(&c->d_irr_invm, sizeof(double) * c->n_irr));
+      SC_CUDA(cudaMalloc(&c->d_irr_fx, sizeof(double) * c->n_irr));
+      SC_CUDA(cudaMemcpy(c->d_irr_lat, il.data(), sizeof(int32_t) * c->n_irr, cudaMemcpyHostToDevice));
+      SC_CUDA(cudaMemcpy(c->d_irr_invm, im.data(), sizeof(double) * c->n_irr, cudaMemcpyHostToDevice));
+      SC_CUDA(cudaMemcpy(c->d_irr_fx, ifv.data(), sizeof(double) * c->n_irr, cudaMemcpyHostToDevice));
     }
   }
-  std::vector<int> comp_id(nc, -1);
-  std::vector<std::vector<int>> comps;
-  for (int i = 0; i < nc; ++i) {
-    int r = uf.f(i);
-    if (comp_id[r] < 0) {
-      comp_id[r] = (int)comps.size();
-      comps.emplace_back();
-    }
-    comps[comp_id[r]].push_back(i);
+  // this rank's c set: the c nodes of its own components (all of them when world == 1)
+  std::vector<int> glob_of_own;   // own canonical index -> global canonical c index
+  if (c->world > 1) {
+    std::vector<int64_t> own;
+    for (int i = 0; i < nc; ++i)
+      if (c_owner[i] == c->rank) {
+        own.push_back(clat_global[i]);
+        glob_of_own.push_back(i);
+      }
+    b.clat = own;
+    nc = (int)own.size();
+    build_c(false);
+  } else {
+    glob_of_own.resize(nc);
+    std::iota(glob_of_own.begin(), glob_of_own.end(), 0);
   }
-  c->n_components = (int64_t)comps.size();
+  c->n_cl = nc;
+
   // ---------------- nested dissection -> ND order and supernodes
   std::vector<int> order;  // ND index -> canonical
   order.reserve(nc);
@@ -541,7 +613,7 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   c->c_canon.resize(nc);
   for (int i = 0; i < nc; ++i) {
     c->c_lat[i] = b.clat[order[i]];
-    c->c_canon[i] = order[i];
+    c->c_canon[i] = glob_of_own[order[i]];
   }
   // convert element maps to ND indices
   for (auto& v : b.celem_cidx)
@@ -952,6 +1024,7 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
     SC_CUDA(cudaMalloc(&c->d_trace, sizeof(unsigned long long) * 3 * std::max(1, c->n_items)));
     sd.trace = c->d_trace;
   }
+  if (c->world > 1) build_exchange(c, c_owner, clat_global);
   c->Kcut_host.clear();
   c->Kcut_host.shrink_to_fit();
   c->Mcut_host.clear();

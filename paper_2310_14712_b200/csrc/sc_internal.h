@@ -157,6 +157,8 @@ struct sc_ctx {
   cudaStream_t s_hi = nullptr;             // high-priority stream of the c part
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool far_ready = false;                  // far-d update of the current step already enqueued
+  int far_cap = 0;                         // resident CTAs per SM of the forked far-d update (0 = no cap)
+  int solve_cap = 0;                       // resident solve CTAs per SM (0 = occupancy limit)
   int kernels_per_step = 0;
   double bytes_per_step = 0, bytes_explicit = 0, bytes_solve = 0, bytes_celem = 0;
   double setup_seconds = 0;
@@ -167,8 +169,29 @@ struct sc_ctx {
   std::vector<long long> cut_cells;           // ascending cell index of each cut cell
   int max_w = 0;                              // widest supernode
   double* d_tmp = nullptr;
-  // multi-GPU (reserved)
+  // ---- multi-rank slab decomposition (partition.cpp; world > 1)
   int rank = 0, world = 1;
+  std::vector<int> layer_lo;          // [world + 1] slab boundaries (element layers, split axis)
+  std::vector<int> reg_lo, reg_hi;    // [world] compute regions (element layers)
+  int64_t n_cl = 0;                   // c DOFs of this rank's components (device c part)
+  std::vector<uint8_t> ntype_rank;    // node types this rank updates (0 elsewhere)
+  int* d_far_tiles = nullptr;         // world > 1: explicit tiles holding this rank's far-d nodes
+  int n_far_tiles = 0;
+  // exchange after each step: per peer q, send (owned, needed by q) / receive lattice indices
+  std::vector<int64_t> xs_off, xr_off;   // [world + 1]
+  int32_t *d_xs_idx = nullptr, *d_xr_idx = nullptr;
+  double *d_xs_buf = nullptr, *d_xr_buf = nullptr;
+  std::vector<int32_t> own_dofs;      // canonical DOF indices owned by this rank
+  int32_t* d_own_lat = nullptr;       // their lattice indices
+  int32_t* d_own_dof = nullptr;
+  void* nccl_comm = nullptr;          // ncclComm_t (world > 1 with an NCCL unique id)
+  double* d_full = nullptr;           // n_dof reduction buffer of sc_read (NCCL)
+};
+
+// component summary for the partition plan (element layers of the split axis)
+struct CompSpan {
+  int lmin, lmax, centroid;
+  double cost;
 };
 
 // ---------------------------------------------------------------- helpers
@@ -196,6 +219,22 @@ double host_lattice(double lo, double hi, int64_t m, int64_t den);
 
 // setup (setup.cu)
 void setup_device_geometry(sc_ctx* c);
+// partition (partition.cpp)
+void plan_partition(sc_ctx* c, const std::vector<CompSpan>& comps, std::vector<int>& owner);
+bool region_computes_plane(const sc_ctx* c, int q, int64_t z);
+int plane_owner(const sc_ctx* c, int64_t z);
+void build_exchange(sc_ctx* c, const std::vector<int>& c_owner_of_lat_sorted_idx,
+                    const std::vector<int64_t>& clat_global);
+// NCCL transport (nccl.cpp; dlopen'ed, world > 1 with a unique id)
+void nccl_init(sc_ctx* c, const void* unique_id);
+void nccl_exchange(sc_ctx* c);
+void nccl_allreduce_sum(sc_ctx* c, double* buf, int64_t n);
+void nccl_destroy(sc_ctx* c);
+int nccl_unique_id(void* out128);
+// exchange kernels (step.cu)
+void enqueue_pack(sc_ctx* c, const double* u, cudaStream_t st);
+void enqueue_unpack(sc_ctx* c, double* u, cudaStream_t st);
+void gather_owned(sc_ctx* c, const double* d_lat, double* d_dst);
 // factor (factor.cpp)
 void setup_factor(sc_ctx* c, const std::vector<double>& Mcut_host);
 // step (step.cu)

@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
 }  // namespace
 
 void launch_solve(sc_ctx* c, const Factor& f, cudaStream_t st) {
-  if (c->n_c == 0 || c->n_items == 0) return;
+  if (c->n_cl == 0 || c->n_items == 0) return;
   SolveDev a = c->solve_dev;
   a.A = f.A;
   const int smem = (int)(sizeof(double) * STAGE);
@@ -367,8 +367,10 @@ void launch_solve(sc_ctx* c, const Factor& f, cudaStream_t st) {
     SC_CUDA(cudaGetDevice(&dev));
     SC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve, NT, smem));
-    // SC_SOLVE_CTAS_PER_SM caps the resident solve CTAs (room for the concurrent far-d update)
-    if (const char* v = getenv("SC_SOLVE_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, atoi(v)));
+    // cap the resident solve CTAs (room for the concurrent far-d update, step.cu)
+    int cap = c->solve_cap;
+    if (const char* v = getenv("SC_SOLVE_CTAS_PER_SM")) cap = atoi(v);
+    if (cap > 0) per_sm = std::max(1, std::min(per_sm, cap));
     c->solve_grid = std::max(1, std::min(c->n_items, per_sm * sms));
   }
   SC_CUDA(cudaMemsetAsync(c->d_solve_cnt, 0, sizeof(int) * c->n_counters, st));

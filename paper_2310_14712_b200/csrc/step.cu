@@ -12,6 +12,7 @@
 // writes u_{n+1} into d_u[cur^1] (d nodes by (a2), c nodes by (a6)) and flips cur.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "sc_internal.h"
@@ -28,14 +29,14 @@ struct ExpP {
   double s[3];      // (2/h_k)^2
   double a1, a2, coefR;  // out = a1 u + a2 P - coefR * r' / prod(wt)
   int want;         // node type updated by this launch (1 tensor-d far from c, 4 tensor-d near c)
-  int tg[2];        // tile-grid extents in x, y (tile-list launches)
-  const int* tiles; // nullable: tile ids (x fastest) of a tile-list launch, one per block
+  int tg[2];        // tile-grid extents in x, y
+  int ntiles;       // tiles of this launch (blocks loop over them with a grid stride)
+  const int* tiles; // nullable: tile ids (x fastest) of a tile-list launch
 };
 
-// tile coordinates of this block: from the tile list if any, else from blockIdx
-__device__ __forceinline__ int3 tile_of(const ExpP& e) {
-  if (!e.tiles) return make_int3(blockIdx.x, blockIdx.y, blockIdx.z);
-  const int id = e.tiles[blockIdx.x];
+// tile coordinates of the tt-th tile of the launch: from the tile list if any, else linear
+__device__ __forceinline__ int3 tile_of(const ExpP& e, int tt) {
+  const int id = e.tiles ? e.tiles[tt] : tt;
   return make_int3(id % e.tg[0], (id / e.tg[0]) % e.tg[1], id / (e.tg[0] * e.tg[1]));
 }
 
@@ -289,17 +290,22 @@ void tiling_p(const GridP& g, int ext[3], int tg[3]) {
 
 template <int P>
 void launch_explicit_p(sc_ctx* c, const double* U, const double* Pv, double* out, ExpP e, int n_tiles,
-                       cudaStream_t st) {
+                       int cap, cudaStream_t st) {
   const GridP& g = c->g;
   int ext[3], tg[3];
   tiling_p<P>(g, ext, tg);
   e.tg[0] = tg[0];
   e.tg[1] = tg[1];
+  e.ntiles = e.tiles ? n_tiles : tg[0] * tg[1] * tg[2];
+  if (e.ntiles == 0) return;
+  static int sms = 0;
+  if (!sms) SC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+  // cap > 0: at most cap resident CTAs per SM (grid-stride over the tiles)
+  const unsigned grid = (unsigned)(cap > 0 ? std::min(e.ntiles, cap * sms) : e.ntiles);
   if (g.dim == 1) {
     k_explicit_1d<P><<<(unsigned)((g.nl[0] + 255) / 256), 256, 0, st>>>(U, Pv, out, c->d_ntype, e, c->d_flag);
   } else if (g.dim == 2) {
     constexpr int E2 = Tile2v<P>::E;
-    dim3 grid = e.tiles ? dim3(n_tiles) : dim3(tg[0], tg[1]);
     k_explicit_2d<P, E2, E2, Tile2v<P>::NT><<<grid, Tile2v<P>::NT, 0, st>>>(U, Pv, out, c->d_ntype, e, c->d_flag);
   } else {
     if constexpr (P <= 6) {
@@ -310,7 +316,6 @@ void launch_explicit_p(sc_ctx* c, const double* U, const double* Pv, double* out
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::smem);
         attr = true;
       }
-      dim3 grid = e.tiles ? dim3(n_tiles) : dim3(tg[0], tg[1], tg[2]);
       kern<<<grid, T::NT, T::smem, st>>>(U, Pv, out, c->d_ntype, e, c->d_flag);
     }
   }
@@ -335,7 +340,7 @@ void explicit_tiling(const GridP& g, int ext[3], int tg[3]) {
 // (a1)+(a2) on the lattice nodes of type `want` (1: tensor-d far from c nodes, 4: tensor-d
 // sharing an element with a c node).  want 4 runs over the near-tile list only.
 void launch_explicit(sc_ctx* c, const double* U, const double* Pv, double* out, double a1, double a2, double a3,
-                     int want, cudaStream_t st) {
+                     int want, cudaStream_t st, int cap = 0) {
   const GridP& g = c->g;
   ExpP e;
   for (int k = 0; k < 3; ++k) {
@@ -355,16 +360,19 @@ void launch_explicit(sc_ctx* c, const double* U, const double* Pv, double* out, 
       e.tiles = c->d_near_tiles;
       n_tiles = c->n_near_tiles;
     }
+  } else if (c->world > 1 && g.dim > 1) {
+    e.tiles = c->d_far_tiles;   // the tiles of this rank's region
+    n_tiles = c->n_far_tiles;
   }
   switch (g.p) {
-    case 1: launch_explicit_p<1>(c, U, Pv, out, e, n_tiles, st); break;
-    case 2: launch_explicit_p<2>(c, U, Pv, out, e, n_tiles, st); break;
-    case 3: launch_explicit_p<3>(c, U, Pv, out, e, n_tiles, st); break;
-    case 4: launch_explicit_p<4>(c, U, Pv, out, e, n_tiles, st); break;
-    case 5: launch_explicit_p<5>(c, U, Pv, out, e, n_tiles, st); break;
-    case 6: launch_explicit_p<6>(c, U, Pv, out, e, n_tiles, st); break;
-    case 7: launch_explicit_p<7>(c, U, Pv, out, e, n_tiles, st); break;
-    case 8: launch_explicit_p<8>(c, U, Pv, out, e, n_tiles, st); break;
+    case 1: launch_explicit_p<1>(c, U, Pv, out, e, n_tiles, cap, st); break;
+    case 2: launch_explicit_p<2>(c, U, Pv, out, e, n_tiles, cap, st); break;
+    case 3: launch_explicit_p<3>(c, U, Pv, out, e, n_tiles, cap, st); break;
+    case 4: launch_explicit_p<4>(c, U, Pv, out, e, n_tiles, cap, st); break;
+    case 5: launch_explicit_p<5>(c, U, Pv, out, e, n_tiles, cap, st); break;
+    case 6: launch_explicit_p<6>(c, U, Pv, out, e, n_tiles, cap, st); break;
+    case 7: launch_explicit_p<7>(c, U, Pv, out, e, n_tiles, cap, st); break;
+    case 8: launch_explicit_p<8>(c, U, Pv, out, e, n_tiles, cap, st); break;
     default: throw ScError(SC_ERR_CONFIG, "p out of range");
   }
   SC_CUDA(cudaGetLastError());
@@ -395,13 +403,13 @@ static void launch_irregular(sc_ctx* c, const double* U, const double* Pv, doubl
 // the implicit solve S a^c_{n+1} = r^c, the corrector; then the device step counter.
 static void enqueue_c_part(sc_ctx* c, const double* A, double* B, cudaStream_t st) {
   const double dt = c->dt;
-  if (c->n_c > 0) {
+  if (c->n_cl > 0) {
     launch_celem(c, 0, A, B, st);
-    k_crhs<<<(unsigned)((c->n_c + 255) / 256), 256, 0, st>>>(c->d_b, c->d_fxc, c->d_rhs_ptr, c->d_rhs_idx, c->d_Y,
-                                                             (int)c->n_c, c->d_ft, c->n_t, c->d_step, 1, c->fS.d);
-    launch_solve(c, c->fS, st);
-    k_corrector<<<(unsigned)((c->n_c + 255) / 256), 256, 0, st>>>(A, B, c->d_vc, c->d_ac, c->d_x, c->d_c_lat,
-                                                                 (int)c->n_c, dt, c->d_flag, c->fS.d);
+    k_crhs<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, st>>>(c->d_b, c->d_fxc, c->d_rhs_ptr, c->d_rhs_idx, c->d_Y,
+                                                              (int)c->n_cl, c->d_ft, c->n_t, c->d_step, 1, c->fS.d);
+    if (!getenv("SC_DEBUG_NO_SOLVE")) launch_solve(c, c->fS, st);   // timing experiments only
+    k_corrector<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, st>>>(A, B, c->d_vc, c->d_ac, c->d_x, c->d_c_lat,
+                                                                  (int)c->n_cl, dt, c->d_flag, c->fS.d);
   }
   k_advance<<<1, 1, 0, st>>>(c->d_step);
   SC_CUDA(cudaGetLastError());
@@ -420,10 +428,13 @@ void enqueue_step(sc_ctx* c, int parity, cudaStream_t st) {
   double* A = c->d_u[parity];
   double* B = c->d_u[parity ^ 1];
   const double dt = c->dt;
-  if (c->n_c == 0) {
+  if (c->n_c == 0 || c->world > 1) {
+    // no pipelining: with world > 1 the next step's far-d update needs this step's exchange
     launch_explicit(c, A, B, B, 2.0, -1.0, dt * dt, 1, st);
+    launch_explicit(c, A, B, B, 2.0, -1.0, dt * dt, 4, st);
     launch_irregular(c, A, B, B, 2.0, -1.0, dt * dt, st);
     enqueue_c_part(c, A, B, st);
+    if (c->world > 1) enqueue_pack(c, B, st);
     return;
   }
   launch_explicit(c, A, B, B, 2.0, -1.0, dt * dt, 4, st);
@@ -432,13 +443,15 @@ void enqueue_step(sc_ctx* c, int parity, cudaStream_t st) {
   SC_CUDA(cudaStreamWaitEvent(c->s_hi, c->ev_fork, 0));
   enqueue_c_part(c, A, B, c->s_hi);
   SC_CUDA(cudaEventRecord(c->ev_join, c->s_hi));
-  launch_explicit(c, B, A, A, 2.0, -1.0, dt * dt, 1, st);   // far-d nodes of step n+1
+  // far-d nodes of step n+1 on a capped grid: the c part keeps SM resources
+  if (!getenv("SC_DEBUG_NO_FAR"))   // timing experiments only (wrong results when set)
+    launch_explicit(c, B, A, A, 2.0, -1.0, dt * dt, 1, st, c->far_cap);
   SC_CUDA(cudaStreamWaitEvent(st, c->ev_join, 0));
 }
 
 // far-d update of the current step (type 1 nodes) when no previous graph did it
 void enqueue_far_prologue(sc_ctx* c) {
-  if (c->n_c == 0 || c->far_ready) return;
+  if (c->n_c == 0 || c->world > 1 || c->far_ready) return;
   const double* A = c->d_u[c->cur];
   double* B = c->d_u[c->cur ^ 1];
   launch_explicit(c, A, B, B, 2.0, -1.0, c->dt * c->dt, 1, c->stream);
@@ -446,6 +459,11 @@ void enqueue_far_prologue(sc_ctx* c) {
 }
 
 void build_graphs(sc_ctx* c) {
+  // the far-d update of step n+1 is forked against the c part of step n; SC_FAR_CAP caps its
+  // resident CTAs per SM and SC_SOLVE_CTAS_PER_SM those of the persistent solve (solve.cu) so
+  // both can co-reside.  Measured on config 4 (profiles/): caps trade solve latency for
+  // overlap one-for-one, so both default to the occupancy limit.
+  if (const char* v = getenv("SC_FAR_CAP")) c->far_cap = std::max(0, atoi(v));
   if (!c->s_hi) {
     int lo = 0, hi = 0;
     SC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -458,7 +476,9 @@ void build_graphs(sc_ctx* c) {
     SC_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     enqueue_step(c, par, c->stream);
     SC_CUDA(cudaStreamEndCapture(c->stream, &gr));
-    SC_CUDA(cudaGraphInstantiate(&c->graph[par], gr, 0));
+    // per-node priorities: the c part (captured on the high-priority stream) is dispatched ahead
+    // of the concurrent far-d update
+    SC_CUDA(cudaGraphInstantiate(&c->graph[par], gr, cudaGraphInstantiateFlagUseNodePriority));
     cudaGraphDestroy(gr);
   }
   // kernels per step: explicit (far) + near + irregular + advance + c part
@@ -470,28 +490,72 @@ void build_graphs(sc_ctx* c) {
 // owns nodes [ext*P*t, ext*P*(t+1)) per axis, the last tile also the final boundary node)
 void setup_step_structures(sc_ctx* c) {
   const GridP& g = c->g;
-  c->n_near_tiles = 0;
-  if (c->n_near == 0 || g.dim == 1) return;
+  c->n_near_tiles = c->n_far_tiles = 0;
+  if (g.dim == 1) return;
   int ext[3], tg[3];
   explicit_tiling(g, ext, tg);
-  std::vector<uint8_t> mark((size_t)tg[0] * tg[1] * tg[2], 0);
-  for (int64_t L = 0; L < c->n_lat; ++L) {
-    if (c->ntype[L] != 4) continue;
-    int64_t r = L;
-    int64_t t[3] = {0, 0, 0};
-    for (int k = 0; k < g.dim; ++k) {
-      const int64_t i = r % g.nl[k];
-      r /= g.nl[k];
-      t[k] = std::min<int64_t>(i / ((int64_t)ext[k] * g.p), tg[k] - 1);
+  // tile lists of the node types this rank updates: near-d (type 4) always, far-d (type 1)
+  // when world > 1 (the rank's region only)
+  auto tiles_of = [&](uint8_t want, int** d, int* n) {
+    std::vector<uint8_t> mark((size_t)tg[0] * tg[1] * tg[2], 0);
+    for (int64_t L = 0; L < c->n_lat; ++L) {
+      if (c->ntype_rank[L] != want) continue;
+      int64_t r = L;
+      int64_t t[3] = {0, 0, 0};
+      for (int k = 0; k < g.dim; ++k) {
+        const int64_t i = r % g.nl[k];
+        r /= g.nl[k];
+        t[k] = std::min<int64_t>(i / ((int64_t)ext[k] * g.p), tg[k] - 1);
+      }
+      mark[t[0] + (size_t)tg[0] * (t[1] + (size_t)tg[1] * t[2])] = 1;
     }
-    mark[t[0] + (size_t)tg[0] * (t[1] + (size_t)tg[1] * t[2])] = 1;
-  }
-  std::vector<int> tiles;
-  for (size_t i = 0; i < mark.size(); ++i)
-    if (mark[i]) tiles.push_back((int)i);
-  c->n_near_tiles = (int)tiles.size();
-  SC_CUDA(cudaMalloc(&c->d_near_tiles, sizeof(int) * std::max<size_t>(1, tiles.size())));
-  SC_CUDA(cudaMemcpy(c->d_near_tiles, tiles.data(), sizeof(int) * tiles.size(), cudaMemcpyHostToDevice));
+    std::vector<int> tiles;
+    for (size_t i = 0; i < mark.size(); ++i)
+      if (mark[i]) tiles.push_back((int)i);
+    *n = (int)tiles.size();
+    SC_CUDA(cudaMalloc(d, sizeof(int) * std::max<size_t>(1, tiles.size())));
+    if (!tiles.empty()) SC_CUDA(cudaMemcpy(*d, tiles.data(), sizeof(int) * tiles.size(), cudaMemcpyHostToDevice));
+  };
+  if (c->n_near) tiles_of(4, &c->d_near_tiles, &c->n_near_tiles);
+  if (c->world > 1) tiles_of(1, &c->d_far_tiles, &c->n_far_tiles);
+}
+
+// ---- multi-rank exchange (partition.cpp): pack this rank's values for all peers, unpack the
+// received values (one buffer each, peers contiguous)
+__global__ void k_pack(const double* __restrict__ u, const int32_t* __restrict__ idx, double* __restrict__ buf,
+                       long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) buf[i] = u[idx[i]];
+}
+__global__ void k_unpack(double* __restrict__ u, const int32_t* __restrict__ idx, const double* __restrict__ buf,
+                         long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) u[idx[i]] = buf[i];
+}
+
+void enqueue_pack(sc_ctx* c, const double* u, cudaStream_t st) {
+  const long long n = c->xs_off.empty() ? 0 : c->xs_off.back();
+  if (n) k_pack<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(u, c->d_xs_idx, c->d_xs_buf, n);
+}
+
+void enqueue_unpack(sc_ctx* c, double* u, cudaStream_t st) {
+  const long long n = c->xr_off.empty() ? 0 : c->xr_off.back();
+  if (n) k_unpack<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(u, c->d_xr_idx, c->d_xr_buf, n);
+  SC_CUDA(cudaGetLastError());
+}
+
+// owned DOF values -> dst[canonical index] (other entries untouched); DEVICE dst
+__global__ void k_scatter_owned(const double* __restrict__ u, const int32_t* __restrict__ lat,
+                                const int32_t* __restrict__ dof, double* __restrict__ dst, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) dst[dof[i]] = u[lat[i]];
+}
+
+void gather_owned(sc_ctx* c, const double* d_lat, double* d_dst) {
+  const long long n = (long long)c->own_dofs.size();
+  if (n) k_scatter_owned<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(d_lat, c->d_own_lat, c->d_own_dof,
+                                                                             d_dst, n);
+  SC_CUDA(cudaGetLastError());
 }
 
 void device_upload_reference(sc_ctx* c) {
@@ -549,14 +613,14 @@ void run_startup(sc_ctx* c, const double* u0, const double* v0) {
   launch_explicit(c, A, Pv, B, 1.0, a2, 0.5 * dt * dt, 1, c->stream);
   launch_explicit(c, A, Pv, B, 1.0, a2, 0.5 * dt * dt, 4, c->stream);
   launch_irregular(c, A, Pv, B, 1.0, a2, 0.5 * dt * dt, c->stream);
-  if (c->n_c > 0) {
+  if (c->n_cl > 0) {
     launch_celem(c, 1, A, A, c->stream);
-    k_crhs<<<(unsigned)((c->n_c + 255) / 256), 256, 0, c->stream>>>(c->d_b, c->d_fxc, c->d_rhs_ptr, c->d_rhs_idx,
-                                                                     c->d_Y, (int)c->n_c, c->d_ft, c->n_t,
+    k_crhs<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, c->stream>>>(c->d_b, c->d_fxc, c->d_rhs_ptr, c->d_rhs_idx,
+                                                                     c->d_Y, (int)c->n_cl, c->d_ft, c->n_t,
                                                                      c->d_step, 0, c->fM.d);
     launch_solve(c, c->fM, c->stream);
-    k_start_c<<<(unsigned)((c->n_c + 255) / 256), 256, 0, c->stream>>>(c->d_ac, c->d_vc, c->d_x, vlat, c->d_c_lat,
-                                                                        (int)c->n_c, c->fM.d);
+    k_start_c<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, c->stream>>>(c->d_ac, c->d_vc, c->d_x, vlat, c->d_c_lat,
+                                                                         (int)c->n_cl, c->fM.d);
   }
   SC_CUDA(cudaGetLastError());
   SC_CUDA(cudaStreamSynchronize(c->stream));
