@@ -4,8 +4,8 @@ python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|re
 
 * ours: the CUDA path through the C ABI (libsc.so).  W warm-up steps, then K steps timed
   with CUDA events on the library stream, barrier + synchronize on both sides, max over
-  ranks.  value = n_dof * K * world / t (weak scaling: each rank advances its own copy of
-  the workload; the slab-partitioned halo-exchange path is not built yet).
+  ranks.  With N > 1 ranks (torchrun) the ONE workload is slab-decomposed over the GPUs
+  (NCCL exchange inside sc_step): value = n_dof * K / t, strong scaling.
 * roofline: every sub-kernel of the step timed alone with CUDA events on the library
   stream (sc_profile); the dominant one (largest time) is reported against the measured
   HBM copy bandwidth with its algorithmic bytes (sc_query).
@@ -160,7 +160,7 @@ def run_reference(args, rank):
               f"{nsteps} steps ({t:.1f} s; setup {t_setup:.1f} s untimed)")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / nsteps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": _config_dict(cfg, n_dof),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": _cores(), "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -182,7 +182,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-steps", type=int, default=1, help="oracle steps per timed step (reference arm)")
     ap.add_argument("--cpu-steps", type=int, default=3, help="oracle steps for cpu_baseline")
@@ -198,14 +198,21 @@ def main():
     import torch.distributed as dist
     import paper_2310_14712_b200 as pkg
     torch.cuda.set_device(local)
+    nccl_id = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(pkg.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nccl_id = bytes(idt.cpu().numpy().tobytes())
     W, K = max(3, args.warmup), args.steps
     cfg = sc_inputs.get_config(args.config)
     f_t = sc_inputs.source_signal(cfg, W + K + 2) if cfg["source"] else None
     stream = torch.cuda.Stream()
     t0 = time.perf_counter()
-    s = pkg.from_config(cfg, f_t=f_t, stream=stream.cuda_stream)
+    s = pkg.from_config(cfg, f_t=f_t, stream=stream.cuda_stream, device=local, rank=rank, world=world,
+                        nccl_id=nccl_id)
     setup_s = time.perf_counter() - t0
     info = s.info
     n_dof = info["n_dof"]
@@ -232,7 +239,7 @@ def main():
         tt = torch.tensor([t_ms], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = float(tt.item())
-    value = n_dof * K * world / (t_ms / 1e3)
+    value = n_dof * K / (t_ms / 1e3)   # the whole (decomposed) workload
     # ---- per-kernel timings (each sub-kernel timed alone with CUDA events on the library
     # stream, sc_profile) and the roofline of the dominant one (largest time per step)
     peak, peak_kind = _peaks()
@@ -277,7 +284,7 @@ def main():
         e1.record(stream)
     torch.cuda.synchronize()
     t_e2e = e0.elapsed_time(e1)
-    e2e = {"value": n_dof * K * world / (t_e2e / 1e3), "unit": UNIT,
+    e2e = {"value": n_dof * K / (t_e2e / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": 16.0 * n_dof / K, "d2h_bytes_per_step": 8.0 * n_dof / K,
            "job": f"sc_set_state(u0,v0 pinned host) + sc_step({K}) + sc_read(u pinned host)"}
     # ---- CPU baseline (rank 0, N=1 only)
@@ -295,7 +302,7 @@ def main():
         l2 = ("per-step working set larger than L2 (no flush)" if info["bytes_per_step"] > 126e6
               else "L2-resident working set (no flush)")
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-                "ms_per_step": t_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "ms_per_step": t_ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic",
                 "config": _config_dict(cfg, n_dof, {"n_c": info["n_c"], "n_d": info["n_d"],
                                                      "cells_cut": info["cells_cut"], "l2": l2,
@@ -304,7 +311,10 @@ def main():
                                                      "nnz_factor": info["nnz_factor"],
                                                      "factor_height": info["factor_height"],
                                                      "kernels_per_step": info["kernels_per_step"],
-                                                     "parallelism": f"{world} independent replicas"}),
+                                                     "parallelism": (f"z-slabs over {world} GPUs, NCCL exchange"
+                                                                     if world > 1 else "1 GPU"),
+                                                     "halo_values_per_step": info["halo_send"],
+                                                     "n_c_rank0": info["n_c_local"]}),
                 "roofline": roof, "kernels": breakdown, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
                 "gpu_launches": int(info["kernels_per_step"]) * K,
                 "step_bytes_algorithmic": info["bytes_per_step"],
