@@ -243,15 +243,12 @@ def main():
     # ---- per-kernel timings (each sub-kernel timed alone with CUDA events on the library
     # stream, sc_profile) and the roofline of the dominant one (largest time per step)
     peak, peak_kind = _peaks()
-    kern = {"explicit_far": (0, info["bytes_explicit_per_step"], "k_explicit (a1)+(a2), far tensor-d DOFs"),
+    kern = {"explicit": (0, info["bytes_explicit_per_step"], "k_explicit (a1)+(a2), tensor-d DOFs"),
             "celem": (1, info["bytes_celem_per_step"], "k_celem (a3)+(a4) c-element products"),
-            "solve": (2, info["bytes_solve_per_step"], "k_solve (a5) persistent supernodal solve"),
-            "explicit_near": (3, 24.0 * info["n_near"], "k_explicit (a1)+(a2), near tensor-d DOFs")}
+            "solve": (2, info["bytes_solve_per_step"], "k_solve (a5) persistent supernodal solve")}
     breakdown = {}
     for name, (which, nbytes, _) in kern.items():
         if which in (1, 2) and info["n_c"] == 0:
-            continue
-        if which == 3 and info["n_near"] == 0:
             continue
         nprof = 30
         torch.cuda.synchronize()

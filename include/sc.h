@@ -121,8 +121,8 @@ typedef struct {
   double dt_crit_uncut;             /* 2/sqrt(lambda_max(K_e, M_e)) of an uncut cell */
   int64_t step;                     /* steps taken since the last (re)start */
   double bytes_per_step;            /* algorithmic HBM bytes per step */
-  double bytes_explicit_per_step;   /* ... of the fused explicit (a1)+(a2) kernel on the far
-                                       tensor-d DOFs alone (sc_profile which = 0) */
+  double bytes_explicit_per_step;   /* ... of the fused explicit (a1)+(a2) kernel on the
+                                       tensor-d DOFs (sc_profile which = 0) */
   int32_t kernels_per_step;         /* kernel launches per step */
   int64_t lattice_nodes;            /* prod(cells*p+1) */
   double setup_seconds;
@@ -193,8 +193,8 @@ sc_status sc_dof_coords(sc_ctx* ctx, double* xyz, int64_t len);
 
 /* Instrumentation: enqueue n launches of ONE sub-kernel of the step on the context stream
  * so that a caller can time it with events: which = 0 fused explicit (a1)+(a2) tensor
- * kernel on the far tensor-d DOFs, 1 c-element products (a4), 2 supernodal solve of S (a5),
- * 3 the explicit kernel on the near tensor-d DOFs.  Clobbers the state: call sc_set_state
+ * kernel on all tensor-d DOFs, 1 c-element products (a4), 2 supernodal solve of S (a5),
+ * 3 the explicit kernel on the near tensor-d DOFs alone (the pipelined mode's second launch).  Clobbers the state: call sc_set_state
  * before stepping again. */
 sc_status sc_profile(sc_ctx* ctx, int32_t which, int64_t n);
 

@@ -186,8 +186,8 @@ extern "C" sc_status sc_setup(const sc_grid* grid, int32_t p, double alpha, cons
     // algorithmic bytes per step
     {
       const double nbd = (double)c->nb;
-      // far tensor-d nodes (the dominant explicit launch): read u_n, u_{n-1}; write u_{n+1}
-      const double ex = 24.0 * (double)(c->n_d - c->n_irr - c->n_near);
+      // tensor-d nodes (the explicit launch, sc_profile 0): read u_n, u_{n-1}; write u_{n+1}
+      const double ex = 24.0 * (double)(c->n_d - c->n_irr);
       // c-element products: dense cut K_e once, w gathered and Y written per element node
       const double ce = 8.0 * (double)c->n_cut * nbd * nbd + 16.0 * (double)c->n_celem * nbd;
       // solve: forward streams every panel [D_s; G_s], backward G_s again; b, q, x vectors
@@ -196,7 +196,7 @@ extern "C" sc_status sc_setup(const sc_grid* grid, int32_t p, double alpha, cons
       c->bytes_explicit = ex;
       c->bytes_celem = ce;
       c->bytes_solve = so;
-      c->bytes_per_step = ex + 24.0 * (double)(c->n_near + c->n_irr) + ce + so +
+      c->bytes_per_step = ex + 24.0 * (double)c->n_irr + ce + so +
                           56.0 * (double)c->n_cl;   // r^c gather + corrector state (u, v, a, x)
     }
     if (u0 || v0) {

@@ -120,7 +120,7 @@ __device__ __forceinline__ void explicit2d_tile(const double* __restrict__ U, co
           double rr = r[l];
           if (l == 0 && (exl > 1 || ex0 > 0)) rr += left;
           const size_t g = gx + (size_t)nx * gy;
-          if (nt[g] == e.want) {
+          if ((e.want >> nt[g]) & 1) {
             const double uu = SU[(oy + P) * RX + exl * P + l];
             const double res = e.a1 * uu + e.a2 * Pv[g] - cy * inv_wt(gx, Nx, P) * rr;
             out[g] = res;

@@ -39,7 +39,7 @@ __device__ __forceinline__ double inv_wt(int i, int e_cnt, int P) {
   return (e > 0 && e < e_cnt) ? c_iw2 : c_iw[0];
 }
 
-template <int P, int EX, int EY, int EZ, int NT>
+template <int P, int EX, int EY, int EZ, int NT, bool SPV>
 __device__ __forceinline__ void explicit3d_tile(const double* __restrict__ U, const double* Pv, double* out,
                                                 const uint8_t* __restrict__ nt, const ExpP& e, int* flag,
                                                 const int3 tb) {
@@ -57,6 +57,8 @@ __device__ __forceinline__ void explicit3d_tile(const double* __restrict__ U, co
   double* BTb = BMb + 2 * TY * RX;     // [2][TY][RX]  s1 Ky Mz u + s2 My Kz u
   double* BMPb = BTb + 2 * TY * RX;    // [2][EYH][RX] l = P contributions (boundary rows)
   double* BTPb = BMPb + 2 * EYH * RX;
+  constexpr int OXP = EX * P + 1;      // output columns of the tile
+  double* SPb = BTPb + 2 * EYH * RX;   // SPV: [2][P1][TY][OXP] staged u_{n-1} of the layer's outputs
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int Nx = e.N[0], Ny = e.N[1], Nz = e.N[2];
@@ -82,6 +84,19 @@ __device__ __forceinline__ void explicit3d_tile(const double* __restrict__ U, co
 #pragma unroll
       for (int k = 0; k < P1; ++k) cp_async8(dst + k * RC + col, src + (ok ? pl * k : 0), ok);
     }
+    if constexpr (SPV) {
+      // u_{n-1} at the layer's output nodes (the x pass reads it from shared memory)
+      if (ez >= ez0) {
+        double* sp = SPb + buf * P1 * TY * OXP;
+        const int OXW = nEX * P + (lastx ? 1 : 0);
+        const int npl = (ez == Nz - 1) ? P1 : P;
+        for (int t = tid; t < npl * OY * OXW; t += NT) {
+          const int ox = t % OXW, r = t / OXW, oy = r % OY, k = r / OY;
+          const size_t g = (size_t)(ex0 * P + ox) + (size_t)nx * (y0 + oy) + pl * (size_t)(ez * P + k);
+          cp_async8(sp + (k * TY + oy) * OXP + ox, Pv + g, true);
+        }
+      }
+    }
     cp_async_commit();
   };
 
@@ -100,7 +115,7 @@ __device__ __forceinline__ void explicit3d_tile(const double* __restrict__ U, co
         const bool ok = act && (l < P || (exl == nEX && lastx)) && gz < e.nl[2];
         const size_t g = gx + (size_t)nx * gy + pl * gz;
         ntv[q][l] = ok ? __ldg(nt + g) : (uint8_t)0;
-        pv[q][l] = ok ? Pv[g] : 0.0;
+        if constexpr (!SPV) pv[q][l] = ok ? Pv[g] : 0.0;
       }
     }
   };
@@ -196,7 +211,7 @@ __device__ __forceinline__ void explicit3d_tile(const double* __restrict__ U, co
       for (int q = 0; q < NXI; ++q)
 #pragma unroll
         for (int l = 0; l < P1; ++l) {
-          pvc[q][l] = pv[q][l];
+          if constexpr (!SPV) pvc[q][l] = pv[q][l];
           ntc[q][l] = ntv[q][l];
         }
       prefetch(k + 1 < np ? gz + 1 : (ez + 1) * P);   // next plane (next layer's plane 0)
@@ -236,13 +251,16 @@ __device__ __forceinline__ void explicit3d_tile(const double* __restrict__ U, co
           const double cyz = e.coefR * inv_wt(gy, Ny, P) * iwz;
 #pragma unroll
           for (int l = 0; l < P1; ++l) {
-            if (ntc[q][l] == e.want) {
+            if ((e.want >> ntc[q][l]) & 1) {
               const int gx = (ex0 - 1 + exl) * P + l;
               double rr = r[l];
               if (l == 0 && (exl > 1 || ex0 > 0)) rr += left;
               const size_t g = gx + (size_t)nx * gy + pl * gz;
               const double uu = Lk[(oy + P) * RX + exl * P + l];
-              const double res = e.a1 * uu + e.a2 * pvc[q][l] - cyz * inv_wt(gx, Nx, P) * rr;
+              double pvv;
+              if constexpr (SPV) pvv = SPb[((buf * P1 + k) * TY + oy) * OXP + (exl - 1) * P + l];
+              else pvv = pvc[q][l];
+              const double res = e.a1 * uu + e.a2 * pvv - cyz * inv_wt(gx, Nx, P) * rr;
               out[g] = res;
               if (!isfinite(res)) atomicExch(flag, 1);
             }
@@ -270,12 +288,12 @@ __device__ __forceinline__ void explicit3d_tile(const double* __restrict__ U, co
 }
 
 // grid-stride loop over the tiles (a capped grid leaves SM resources to a concurrent kernel)
-template <int P, int EX, int EY, int EZ, int NT, int MINB>
+template <int P, int EX, int EY, int EZ, int NT, int MINB, bool SPV>
 __global__ void __launch_bounds__(NT, MINB) k_explicit_3d(const double* __restrict__ U, const double* Pv,
                                                           double* out, const uint8_t* __restrict__ nt, ExpP e,
                                                           int* flag) {
   for (int tt = blockIdx.x; tt < e.ntiles; tt += gridDim.x)
-    explicit3d_tile<P, EX, EY, EZ, NT>(U, Pv, out, nt, e, flag, tile_of(e, tt));
+    explicit3d_tile<P, EX, EY, EZ, NT, SPV>(U, Pv, out, nt, e, flag, tile_of(e, tt));
 }
 
 // tile shapes: the z+y phase has RX*(E+1) column items and the x phase (E*P+1) rows of
@@ -285,9 +303,10 @@ struct Tile3 {
   static constexpr int E = P <= 2 ? 8 : (P == 3 ? 7 : (P == 4 ? 5 : 3));
   static constexpr int EZ = 8;
   static constexpr int NT = P == 3 ? 224 : (P == 4 ? 160 : 256);
-  static constexpr int MINB = P == 3 ? 2 : (P == 4 ? 3 : (P <= 2 ? 2 : 1));
+  static constexpr int MINB = P == 3 ? 2 : (P == 4 ? 2 : (P <= 2 ? 2 : 1));
+  static constexpr bool SPV = (P == 3 || P == 4);   // u_{n-1} staged through shared memory
   static constexpr int RX = (E + 1) * P + 1;
   static constexpr int TY = E * P + 1;
-  static constexpr size_t smem =
-      sizeof(double) * (2 * (P + 1) * RX * RX + 4 * TY * RX + 4 * (E + 1) * RX);
+  static constexpr size_t smem = sizeof(double) * (2 * (P + 1) * RX * RX + 4 * TY * RX + 4 * (E + 1) * RX +
+                                                   (SPV ? 2 * (P + 1) * TY * (E * P + 1) : 0));
 };

@@ -805,7 +805,9 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
     gidx.insert(gidx.end(), gl[t].begin(), gl[t].end());
   }
   // persistent-solve work list (solve.cu).  Items of a phase cover the supernode's panel in
-  // tiles that fill one staging buffer of SOLVE_STAGE doubles:
+  // tiles that fill one staging buffer of `stage` doubles (SOLVE_STAGE; 2 x SOLVE_STAGE for
+  // large factors, where the solve is throughput-bound and bigger items move more bytes per
+  // item latency; SC_SOLVE_STAGE overrides):
   //  forward  F: panel rows [r0, r0 + nr) x columns [c0, c0 + nc); C = min(w, SOLVE_TILE)
   //              columns per tile, R = 32 * 2^k rows (as many as fit, >= 32)
   //  backward B: G_s columns [c0, c0 + nc) (nc <= 32) x G_s rows [r0, r0 + nr), rows as
@@ -815,6 +817,14 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   // needs, one load): (type, s, t, ntb) (pslot, bctr, r0, nr) (col0, nc, dof0, w)
   // (r, goff, uoff, roff) (aoff lo, aoff hi, ld, wp).
   const int TILE = SOLVE_TILE;
+  int stage = SOLVE_STAGE;
+  {
+    int64_t ent = 0;
+    for (int s = 0; s < nsn; ++s) ent += (int64_t)wv[s] * panel_ld(wv[s], rv[s]);
+    if (ent > 200000000) stage = 2 * SOLVE_STAGE;
+    if (const char* v = getenv("SC_SOLVE_STAGE")) stage = std::max(SOLVE_STAGE, std::min(4 * SOLVE_STAGE, atoi(v)));
+  }
+  c->solve_stage = stage;
   std::vector<int32_t> items;
   std::vector<int32_t> nblk(2 * (size_t)nsn, 0);
   std::vector<std::vector<int>> by_h(c->height);
@@ -841,7 +851,7 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
     const int w = wv[s], ld = panel_ld(w, rv[s]);
     const int C = std::min(w, TILE);
     int R = 32;
-    while (2 * R * C <= SOLVE_STAGE && R < ((ld + 31) / 32) * 32) R *= 2;
+    while (2 * R * C <= stage && R < ((ld + 31) / 32) * 32) R *= 2;
     const int ntb = (w + C - 1) / C;
     for (int r0 = 0; r0 < ld; r0 += R)
       group(0, s, ntb, R, [&](int t, int& rr, int& nr, int& cc, int& nc) {
@@ -854,7 +864,7 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   auto bwd_items = [&](int s) {
     const int w = wv[s], rp = (rv[s] + 1) & ~1;
     const int NC = std::min(32, w);
-    int RR = std::min(SOLVE_BROWS, (SOLVE_STAGE / NC) & ~1);
+    int RR = std::min(SOLVE_BROWS, (stage / NC) & ~1);
     RR = std::max(2, std::min(RR, std::max(rp, 2)));
     const int ntb = std::max(1, (rp + RR - 1) / RR);
     for (int o0 = 0; o0 < w; o0 += 32)

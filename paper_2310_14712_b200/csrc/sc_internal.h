@@ -139,7 +139,7 @@ struct sc_ctx {
   int n_init = 0;
   int* d_solve_cnt = nullptr;         // [2*n_sn] phase counters, [n_bctr] tickets, head
   double* d_part = nullptr;           // tile partials
-  int n_items = 0, solve_grid = 0;
+  int n_items = 0, solve_grid = 0, solve_stage = SOLVE_STAGE;
   unsigned long long* d_trace = nullptr;   // SC_TRACE: solve item timeline (debug)
   std::vector<int32_t> h_items;            // host copy of the work list (debug)
   size_t n_counters = 0;
@@ -157,6 +157,7 @@ struct sc_ctx {
   cudaStream_t s_hi = nullptr;             // high-priority stream of the c part
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool far_ready = false;                  // far-d update of the current step already enqueued
+  bool pipelined = false;                  // SC_PIPELINE: far-d update forked against the c part
   int far_cap = 0;                         // resident CTAs per SM of the forked far-d update (0 = no cap)
   int solve_cap = 0;                       // resident solve CTAs per SM (0 = occupancy limit)
   int kernels_per_step = 0;

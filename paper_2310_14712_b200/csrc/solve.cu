@@ -37,7 +37,6 @@ namespace {
 enum { IT_F = 0, IT_B = 1 };
 constexpr int NT = 256;               // threads per CTA
 constexpr int NW = NT / 32;
-constexpr int STAGE = SOLVE_STAGE;    // staging buffer (doubles)
 constexpr int VS = SOLVE_BROWS > SOLVE_TILE ? SOLVE_BROWS : SOLVE_TILE;   // gathered vector
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -205,7 +204,7 @@ __device__ __forceinline__ void stage_item(const SolveDev& a, const Item& m, dou
 }
 
 __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
-  extern __shared__ __align__(128) double stg[];   // STAGE doubles
+  extern __shared__ __align__(128) double stg[];   // c->solve_stage doubles (factor.cpp)
   __shared__ double vs[VS];
   __shared__ double red[NT];
   __shared__ __align__(8) uint64_t bar;
@@ -360,7 +359,7 @@ void launch_solve(sc_ctx* c, const Factor& f, cudaStream_t st) {
   if (c->n_cl == 0 || c->n_items == 0) return;
   SolveDev a = c->solve_dev;
   a.A = f.A;
-  const int smem = (int)(sizeof(double) * STAGE);
+  const int smem = (int)(sizeof(double) * c->solve_stage);
   if (c->solve_grid == 0) {
     SC_CUDA(cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int per_sm = 0, sms = 0, dev = 0;

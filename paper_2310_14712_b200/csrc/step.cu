@@ -23,12 +23,15 @@ __constant__ double c_w[SC_MAXP1];
 __constant__ double c_iw[SC_MAXP1];   // 1 / w_l
 __constant__ double c_iw2;            // 1 / (2 w_0): interior element-boundary node
 
+enum { WANT_FAR = 1 << 1, WANT_NEAR = 1 << 4 };
+
 struct ExpP {
   int nl[3];
   int N[3];
   double s[3];      // (2/h_k)^2
   double a1, a2, coefR;  // out = a1 u + a2 P - coefR * r' / prod(wt)
-  int want;         // node type updated by this launch (1 tensor-d far from c, 4 tensor-d near c)
+  int want;         // bit mask of the node types updated by this launch: bit 1 tensor-d far
+                    // from c nodes, bit 4 tensor-d near c nodes (WANT_FAR / WANT_NEAR)
   int tg[2];        // tile-grid extents in x, y
   int ntiles;       // tiles of this launch (blocks loop over them with a grid stride)
   const int* tiles; // nullable: tile ids (x fastest) of a tile-list launch
@@ -76,7 +79,7 @@ template <int P>
 __global__ void k_explicit_1d(const double* __restrict__ U, const double* Pv, double* out,
                               const uint8_t* __restrict__ nt, ExpP e, int* flag) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= e.nl[0] || nt[i] != e.want) return;
+  if (i >= e.nl[0] || !((e.want >> nt[i]) & 1)) return;
   const double r = e.s[0] * op1d<P>(c_Kh, i, e.N[0], [&](int k) { return U[k]; });
   const double u = U[i];
   const double res = e.a1 * u + e.a2 * Pv[i] - e.coefR * r / wt(i, e.N[0], P);
@@ -310,7 +313,7 @@ void launch_explicit_p(sc_ctx* c, const double* U, const double* Pv, double* out
   } else {
     if constexpr (P <= 6) {
       using T = Tile3<P>;
-      auto kern = k_explicit_3d<P, T::E, T::E, T::EZ, T::NT, T::MINB>;
+      auto kern = k_explicit_3d<P, T::E, T::E, T::EZ, T::NT, T::MINB, T::SPV>;
       static bool attr = false;
       if (!attr) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::smem);
@@ -351,9 +354,10 @@ void launch_explicit(sc_ctx* c, const double* U, const double* Pv, double* out, 
   e.a1 = a1;
   e.a2 = a2;
   e.coefR = a3 * c->c * c->c;
-  e.want = want;
+  e.want = want == 1 ? WANT_FAR : (want == 4 ? WANT_NEAR : WANT_FAR | WANT_NEAR);
   e.tiles = nullptr;
   int n_tiles = 0;
+  if (want == 5 && c->n_near == 0) e.want = WANT_FAR;
   if (want == 4) {
     if (c->n_near == 0) return;
     if (g.dim > 1) {
@@ -361,7 +365,7 @@ void launch_explicit(sc_ctx* c, const double* U, const double* Pv, double* out, 
       n_tiles = c->n_near_tiles;
     }
   } else if (c->world > 1 && g.dim > 1) {
-    e.tiles = c->d_far_tiles;   // the tiles of this rank's region
+    e.tiles = c->d_far_tiles;   // the tiles of this rank's region (they hold its near nodes too)
     n_tiles = c->n_far_tiles;
   }
   switch (g.p) {
@@ -428,10 +432,10 @@ void enqueue_step(sc_ctx* c, int parity, cudaStream_t st) {
   double* A = c->d_u[parity];
   double* B = c->d_u[parity ^ 1];
   const double dt = c->dt;
-  if (c->n_c == 0 || c->world > 1) {
-    // no pipelining: with world > 1 the next step's far-d update needs this step's exchange
-    launch_explicit(c, A, B, B, 2.0, -1.0, dt * dt, 1, st);
-    launch_explicit(c, A, B, B, 2.0, -1.0, dt * dt, 4, st);
+  if (!c->pipelined) {
+    // one explicit launch for far and near d nodes (want 5), irregular nodes, c part; with
+    // world > 1 the pack of the exchange (the next step's explicit update needs it)
+    launch_explicit(c, A, B, B, 2.0, -1.0, dt * dt, 5, st);
     launch_irregular(c, A, B, B, 2.0, -1.0, dt * dt, st);
     enqueue_c_part(c, A, B, st);
     if (c->world > 1) enqueue_pack(c, B, st);
@@ -451,7 +455,7 @@ void enqueue_step(sc_ctx* c, int parity, cudaStream_t st) {
 
 // far-d update of the current step (type 1 nodes) when no previous graph did it
 void enqueue_far_prologue(sc_ctx* c) {
-  if (c->n_c == 0 || c->world > 1 || c->far_ready) return;
+  if (!c->pipelined || c->far_ready) return;
   const double* A = c->d_u[c->cur];
   double* B = c->d_u[c->cur ^ 1];
   launch_explicit(c, A, B, B, 2.0, -1.0, c->dt * c->dt, 1, c->stream);
@@ -464,6 +468,10 @@ void build_graphs(sc_ctx* c) {
   // both can co-reside.  Measured on config 4 (profiles/): caps trade solve latency for
   // overlap one-for-one, so both default to the occupancy limit.
   if (const char* v = getenv("SC_FAR_CAP")) c->far_cap = std::max(0, atoi(v));
+  // SC_PIPELINE=1: fork the far-d update of step n+1 against the c part of step n (one rank
+  // with c DOFs); default off: measured no gain and it costs a second
+  // (near-node) explicit launch
+  c->pipelined = c->n_c > 0 && c->world == 1 && getenv("SC_PIPELINE") && atoi(getenv("SC_PIPELINE"));
   if (!c->s_hi) {
     int lo = 0, hi = 0;
     SC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -481,8 +489,8 @@ void build_graphs(sc_ctx* c) {
     SC_CUDA(cudaGraphInstantiate(&c->graph[par], gr, cudaGraphInstantiateFlagUseNodePriority));
     cudaGraphDestroy(gr);
   }
-  // kernels per step: explicit (far) + near + irregular + advance + c part
-  c->kernels_per_step = 1 + (c->n_near > 0 ? 1 : 0) + (c->n_irr > 0) + 1;
+  // kernels per step: explicit (+ near when pipelined) + irregular + advance + c part (+ pack)
+  c->kernels_per_step = 1 + (c->pipelined && c->n_near > 0 ? 1 : 0) + (c->n_irr > 0) + 1 + (c->world > 1);
   if (c->n_c > 0) c->kernels_per_step += 3 + (c->n_items > 0 ? 1 : 0);
 }
 
@@ -610,8 +618,7 @@ void run_startup(sc_ctx* c, const double* u0, const double* v0) {
   // d part: B = u0 - dt v0 + dt^2/2 a0  (P = v0 lattice, or A with a2 = 0 when v0 == 0)
   const double* Pv = vlat ? vlat : A;
   const double a2 = vlat ? -dt : 0.0;
-  launch_explicit(c, A, Pv, B, 1.0, a2, 0.5 * dt * dt, 1, c->stream);
-  launch_explicit(c, A, Pv, B, 1.0, a2, 0.5 * dt * dt, 4, c->stream);
+  launch_explicit(c, A, Pv, B, 1.0, a2, 0.5 * dt * dt, 5, c->stream);
   launch_irregular(c, A, Pv, B, 1.0, a2, 0.5 * dt * dt, c->stream);
   if (c->n_cl > 0) {
     launch_celem(c, 1, A, A, c->stream);
@@ -634,7 +641,7 @@ void profile_launch(sc_ctx* c, int which) {
   const double* A = c->d_u[c->cur];
   double* B = c->d_u[c->cur ^ 1];
   c->far_ready = false;
-  if (which == 0) launch_explicit(c, A, B, B, 2.0, -1.0, c->dt * c->dt, 1, c->stream);
+  if (which == 0) launch_explicit(c, A, B, B, 2.0, -1.0, c->dt * c->dt, 5, c->stream);
   else if (which == 1) launch_celem(c, 0, A, B, c->stream);
   else if (which == 2) launch_solve(c, c->fS, c->stream);
   else launch_explicit(c, A, B, B, 2.0, -1.0, c->dt * c->dt, 4, c->stream);
