@@ -805,9 +805,8 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
     gidx.insert(gidx.end(), gl[t].begin(), gl[t].end());
   }
   // persistent-solve work list (solve.cu).  Items of a phase cover the supernode's panel in
-  // tiles that fill one staging buffer of `stage` doubles (SOLVE_STAGE; 2 x SOLVE_STAGE for
-  // large factors, where the solve is throughput-bound and bigger items move more bytes per
-  // item latency; SC_SOLVE_STAGE overrides):
+  // tiles that fill one staging buffer of `stage` doubles (SOLVE_STAGE = 32 KB: 5 CTAs per
+  // SM; measured 8 K / 16 K doubles slower on configs 4 and 5 — fewer resident CTAs):
   //  forward  F: panel rows [r0, r0 + nr) x columns [c0, c0 + nc); C = min(w, SOLVE_TILE)
   //              columns per tile, R = 32 * 2^k rows (as many as fit, >= 32)
   //  backward B: G_s columns [c0, c0 + nc) (nc <= 32) x G_s rows [r0, r0 + nr), rows as
@@ -818,12 +817,7 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   // (r, goff, uoff, roff) (aoff lo, aoff hi, ld, wp).
   const int TILE = SOLVE_TILE;
   int stage = SOLVE_STAGE;
-  {
-    int64_t ent = 0;
-    for (int s = 0; s < nsn; ++s) ent += (int64_t)wv[s] * panel_ld(wv[s], rv[s]);
-    if (ent > 200000000) stage = 2 * SOLVE_STAGE;
-    if (const char* v = getenv("SC_SOLVE_STAGE")) stage = std::max(SOLVE_STAGE, std::min(4 * SOLVE_STAGE, atoi(v)));
-  }
+  if (const char* v = getenv("SC_SOLVE_STAGE")) stage = std::max(SOLVE_STAGE, std::min(4 * SOLVE_STAGE, atoi(v)));
   c->solve_stage = stage;
   std::vector<int32_t> items;
   std::vector<int32_t> nblk(2 * (size_t)nsn, 0);
