@@ -42,7 +42,7 @@ __device__ __forceinline__ double inv_wt(int i, int e_cnt, int P) {
 template <int P, int EX, int EY, int EZ, int NT, bool SPV>
 __device__ __forceinline__ void explicit3d_tile(const double* __restrict__ U, const double* Pv, double* out,
                                                 const uint8_t* __restrict__ nt, const ExpP& e, int* flag,
-                                                const int3 tb) {
+                                                const int3 tb, const bool clean) {
   constexpr int P1 = P + 1;
   constexpr int EXH = EX + 1, EYH = EY + 1;
   constexpr int RX = EXH * P + 1, RY = EYH * P + 1, TY = EY * P + 1;
@@ -114,12 +114,14 @@ __device__ __forceinline__ void explicit3d_tile(const double* __restrict__ U, co
         const int gx = (ex0 - 1 + exl) * P + l;
         const bool ok = act && (l < P || (exl == nEX && lastx)) && gz < e.nl[2];
         const size_t g = gx + (size_t)nx * gy + pl * gz;
-        ntv[q][l] = ok ? __ldg(nt + g) : (uint8_t)0;
+        // clean tile: every node it owns is tensor-d of a wanted type (setup_step_structures)
+        ntv[q][l] = ok ? (clean ? (uint8_t)1 : __ldg(nt + g)) : (uint8_t)0;
         if constexpr (!SPV) pv[q][l] = ok ? Pv[g] : 0.0;
       }
     }
   };
 
+  bool bad = false;                  // a non-finite update (reported once per tile)
   double ca[NYI][P1], cb[NYI][P1];   // z carries of the column items' P+1 rows
 #pragma unroll
   for (int q = 0; q < NYI; ++q)
@@ -262,7 +264,7 @@ __device__ __forceinline__ void explicit3d_tile(const double* __restrict__ U, co
               else pvv = pvc[q][l];
               const double res = e.a1 * uu + e.a2 * pvv - cyz * inv_wt(gx, Nx, P) * rr;
               out[g] = res;
-              if (!isfinite(res)) atomicExch(flag, 1);
+              bad |= !isfinite(res);
             }
           }
         }
@@ -285,6 +287,7 @@ __device__ __forceinline__ void explicit3d_tile(const double* __restrict__ U, co
       }
     __syncthreads();  // all reads of this layer's buffer done before it is refilled
   }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(flag, 1);
 }
 
 // grid-stride loop over the tiles (a capped grid leaves SM resources to a concurrent kernel)
@@ -292,8 +295,10 @@ template <int P, int EX, int EY, int EZ, int NT, int MINB, bool SPV>
 __global__ void __launch_bounds__(NT, MINB) k_explicit_3d(const double* __restrict__ U, const double* Pv,
                                                           double* out, const uint8_t* __restrict__ nt, ExpP e,
                                                           int* flag) {
-  for (int tt = blockIdx.x; tt < e.ntiles; tt += gridDim.x)
-    explicit3d_tile<P, EX, EY, EZ, NT, SPV>(U, Pv, out, nt, e, flag, tile_of(e, tt));
+  for (int tt = blockIdx.x; tt < e.ntiles; tt += gridDim.x) {
+    const int id = e.tiles ? e.tiles[tt] : tt;
+    explicit3d_tile<P, EX, EY, EZ, NT, SPV>(U, Pv, out, nt, e, flag, tile_of(e, tt), e.clean && e.clean[id]);
+  }
 }
 
 // tile shapes: the z+y phase has RX*(E+1) column items and the x phase (E*P+1) rows of

@@ -57,6 +57,7 @@ struct SolveDev {
   const int32_t* init;         // forward items of the leaves (ready at launch)
   int n_init;
   int tile;                    // reduction-tile length (SOLVE_TILE)
+  int stage;                   // staging buffer (doubles; two per CTA)
   int prefetch;                // SC_SOLVE_PREFETCH=1: L2 bulk prefetch of a phase's panel at push
   unsigned long long* trace;   // optional (SC_TRACE): per item [dequeued, deps met, done] ns
 };
@@ -150,6 +151,7 @@ struct sc_ctx {
   int64_t sum_r = 0;        // sum_s r_s (update-vector entries)
   int64_t n_components = 0;
   // near-d tiles of the explicit kernel (tile ids, x fastest)
+  uint8_t* d_clean = nullptr;         // 3D: per explicit tile, 1 = owns only tensor-d nodes
   int* d_near_tiles = nullptr;
   int n_near_tiles = 0;
   // graphs and the step pipeline (step.cu)

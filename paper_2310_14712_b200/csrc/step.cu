@@ -35,6 +35,7 @@ struct ExpP {
   int tg[2];        // tile-grid extents in x, y
   int ntiles;       // tiles of this launch (blocks loop over them with a grid stride)
   const int* tiles; // nullable: tile ids (x fastest) of a tile-list launch
+  const uint8_t* clean;  // nullable: per tile id, 1 = every node it owns is wanted tensor-d
 };
 
 // tile coordinates of the tt-th tile of the launch: from the tile list if any, else linear
@@ -355,6 +356,7 @@ void launch_explicit(sc_ctx* c, const double* U, const double* Pv, double* out, 
   e.a2 = a2;
   e.coefR = a3 * c->c * c->c;
   e.want = want == 1 ? WANT_FAR : (want == 4 ? WANT_NEAR : WANT_FAR | WANT_NEAR);
+  e.clean = want == 5 ? c->d_clean : nullptr;
   e.tiles = nullptr;
   int n_tiles = 0;
   if (want == 5 && c->n_near == 0) e.want = WANT_FAR;
@@ -526,6 +528,26 @@ void setup_step_structures(sc_ctx* c) {
   };
   if (c->n_near) tiles_of(4, &c->d_near_tiles, &c->n_near_tiles);
   if (c->world > 1) tiles_of(1, &c->d_far_tiles, &c->n_far_tiles);
+  // clean tiles (3D): every node a tile owns is tensor-d (type 1 or 4) -> the combined
+  // far+near launch needs no per-node type loads there
+  if (g.dim == 3) {
+    const size_t nt_ = (size_t)tg[0] * tg[1] * tg[2];
+    std::vector<uint8_t> clean(nt_, 1);
+    for (int64_t L = 0; L < c->n_lat; ++L) {
+      const uint8_t t = c->ntype_rank[L];
+      if (t == 1 || t == 4) continue;
+      int64_t r = L;
+      int64_t ti[3] = {0, 0, 0};
+      for (int k = 0; k < 3; ++k) {
+        const int64_t i = r % g.nl[k];
+        r /= g.nl[k];
+        ti[k] = std::min<int64_t>(i / ((int64_t)ext[k] * g.p), tg[k] - 1);
+      }
+      clean[ti[0] + (size_t)tg[0] * (ti[1] + (size_t)tg[1] * ti[2])] = 0;
+    }
+    SC_CUDA(cudaMalloc(&c->d_clean, nt_));
+    SC_CUDA(cudaMemcpy(c->d_clean, clean.data(), nt_, cudaMemcpyHostToDevice));
+  }
 }
 
 // ---- multi-rank exchange (partition.cpp): pack this rank's values for all peers, unpack the
