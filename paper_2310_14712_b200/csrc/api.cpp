@@ -122,6 +122,7 @@ extern "C" sc_status sc_setup(const sc_grid* grid, int32_t p, double alpha, cons
     g.p = p;
     g.s = geom->lattice_s;
     g.depth = geom->tree_depth;
+    g.ezl = 0;
     c->nb = 1;
     c->n_cells = 1;
     c->n_lat = 1;

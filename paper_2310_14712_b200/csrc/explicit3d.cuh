@@ -39,7 +39,7 @@ __device__ __forceinline__ double inv_wt(int i, int e_cnt, int P) {
   return (e > 0 && e < e_cnt) ? c_iw2 : c_iw[0];
 }
 
-template <int P, int EX, int EY, int EZ, int NT, bool SPV>
+template <int P, int EX, int EY, int NT, bool SPV>
 __device__ __forceinline__ void explicit3d_tile(const double* __restrict__ U, const double* Pv, double* out,
                                                 const uint8_t* __restrict__ nt, const ExpP& e, int* flag,
                                                 const int3 tb, const bool clean) {
@@ -64,6 +64,7 @@ __device__ __forceinline__ void explicit3d_tile(const double* __restrict__ U, co
   const int Nx = e.N[0], Ny = e.N[1], Nz = e.N[2];
   const int nx = e.nl[0], ny = e.nl[1];
   const size_t pl = (size_t)nx * ny;
+  const int EZ = e.ezl;   // element layers per tile along z (runtime, step.cu)
   const int ex0 = tb.x * EX, ey0 = tb.y * EY, ez0 = tb.z * EZ;
   const int ex1 = min(ex0 + EX, Nx), ey1 = min(ey0 + EY, Ny), ez1 = min(ez0 + EZ, Nz);
   const int nEX = ex1 - ex0, nEY = ey1 - ey0;
@@ -90,11 +91,12 @@ __device__ __forceinline__ void explicit3d_tile(const double* __restrict__ U, co
         double* sp = SPb + buf * P1 * TY * OXP;
         const int OXW = nEX * P + (lastx ? 1 : 0);
         const int npl = (ez == Nz - 1) ? P1 : P;
-        for (int t = tid; t < npl * OY * OXW; t += NT) {
-          const int ox = t % OXW, r = t / OXW, oy = r % OY, k = r / OY;
-          const size_t g = (size_t)(ex0 * P + ox) + (size_t)nx * (y0 + oy) + pl * (size_t)(ez * P + k);
-          cp_async8(sp + (k * TY + oy) * OXP + ox, Pv + g, true);
-        }
+        // warp per output row (no integer division), lanes along x
+        const double* pv0 = Pv + (size_t)(ex0 * P) + (size_t)nx * y0 + pl * (size_t)(ez * P);
+        for (int k = 0; k < npl; ++k)
+          for (int oy = warp; oy < OY; oy += NW)
+            if (lane < OXW)
+              cp_async8(sp + (k * TY + oy) * OXP + lane, pv0 + (size_t)nx * oy + pl * (size_t)k + lane, true);
       }
     }
     cp_async_commit();
@@ -249,21 +251,26 @@ __device__ __forceinline__ void explicit3d_tile(const double* __restrict__ U, co
         }
         const double left = __shfl_up_sync(0xffffffffu, r[P], 1);
         if (act && exl > 0) {
+          // per row item: pointers and the lumped-mass reciprocals hoisted out of the node loop
           const int gy = y0 + oy;
+          const int xe = ex0 - 1 + exl;                 // x element of this row item
           const double cyz = e.coefR * inv_wt(gy, Ny, P) * iwz;
+          double* orow = out + (size_t)nx * gy + pl * gz + (size_t)xe * P;
+          const double* urow = Lk + (oy + P) * RX + exl * P;
+          const double* prow = SPV ? SPb + ((buf * P1 + k) * TY + oy) * OXP + (exl - 1) * P : nullptr;
+          const double iw0 = (xe > 0) ? c_iw2 : c_iw[0];           // node xe*P (left boundary)
+          const double iwP = (xe + 1 < Nx) ? c_iw2 : c_iw[0];      // node (xe+1)*P
 #pragma unroll
           for (int l = 0; l < P1; ++l) {
             if ((e.want >> ntc[q][l]) & 1) {
-              const int gx = (ex0 - 1 + exl) * P + l;
               double rr = r[l];
               if (l == 0 && (exl > 1 || ex0 > 0)) rr += left;
-              const size_t g = gx + (size_t)nx * gy + pl * gz;
-              const double uu = Lk[(oy + P) * RX + exl * P + l];
               double pvv;
-              if constexpr (SPV) pvv = SPb[((buf * P1 + k) * TY + oy) * OXP + (exl - 1) * P + l];
+              if constexpr (SPV) pvv = prow[l];
               else pvv = pvc[q][l];
-              const double res = e.a1 * uu + e.a2 * pvv - cyz * inv_wt(gx, Nx, P) * rr;
-              out[g] = res;
+              const double iwx = l == 0 ? iw0 : (l == P ? iwP : c_iw[l]);
+              const double res = e.a1 * urow[l] + e.a2 * pvv - cyz * iwx * rr;
+              orow[l] = res;
               bad |= !isfinite(res);
             }
           }
@@ -291,13 +298,13 @@ __device__ __forceinline__ void explicit3d_tile(const double* __restrict__ U, co
 }
 
 // grid-stride loop over the tiles (a capped grid leaves SM resources to a concurrent kernel)
-template <int P, int EX, int EY, int EZ, int NT, int MINB, bool SPV>
+template <int P, int EX, int EY, int NT, int MINB, bool SPV>
 __global__ void __launch_bounds__(NT, MINB) k_explicit_3d(const double* __restrict__ U, const double* Pv,
                                                           double* out, const uint8_t* __restrict__ nt, ExpP e,
                                                           int* flag) {
   for (int tt = blockIdx.x; tt < e.ntiles; tt += gridDim.x) {
     const int id = e.tiles ? e.tiles[tt] : tt;
-    explicit3d_tile<P, EX, EY, EZ, NT, SPV>(U, Pv, out, nt, e, flag, tile_of(e, tt), e.clean && e.clean[id]);
+    explicit3d_tile<P, EX, EY, NT, SPV>(U, Pv, out, nt, e, flag, tile_of(e, tt), e.clean && e.clean[id]);
   }
 }
 
@@ -306,7 +313,7 @@ __global__ void __launch_bounds__(NT, MINB) k_explicit_3d(const double* __restri
 template <int P>
 struct Tile3 {
   static constexpr int E = P <= 2 ? 8 : (P == 3 ? 7 : (P == 4 ? 5 : 3));
-  static constexpr int EZ = 8;
+  static constexpr int EZ = 8;    // default element layers per tile (+1 warm-up layer)
   static constexpr int NT = P == 3 ? 224 : (P == 4 ? 160 : 256);
   static constexpr int MINB = P == 3 ? 2 : (P == 4 ? 2 : (P <= 2 ? 2 : 1));
   static constexpr bool SPV = (P == 3 || P == 4);   // u_{n-1} staged through shared memory

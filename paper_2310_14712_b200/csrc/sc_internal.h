@@ -33,6 +33,7 @@ struct GridP {
   int64_t nl[3];       // lattice nodes per axis (N*p+1; 1 for unused axes)
   double lo[3], hi[3];
   double h[3];
+  int ezl;             // 3D explicit tiles: element layers per tile along z (step.cu)
 };
 
 // device view of the supernodal factor structure + persistent-solve work list (solve.cu)

@@ -256,18 +256,37 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
       for (int i = tid; i < rr; i += NT) vs[i] = __ldcg(a.x + a.R[m.roff + m.r0 + i]);
       if (tid == 0 && rr < m.nr && rr >= 0) vs[rr] = 0.0;   // padding row
     }
+    // forward: the children's contributions to the update rows this thread will emit (rows
+    // r0 + tid + k NT), gathered now so they overlap the panel copy instead of following it
+    constexpr int NCR = 4;
+    double crv[NCR];
+#pragma unroll
+    for (int k = 0; k < NCR; ++k) {
+      crv[k] = 0.0;
+      const int i = m.r0 + tid + k * NT;
+      if (fwd && tid + k * NT < m.nr && i >= m.wp && i < m.wp + m.r) {
+        const int kk = m.w + (i - m.wp);
+        for (int q = a.gptr[go + kk]; q < a.gptr[go + kk + 1]; ++q) crv[k] += __ldcg(a.U + a.gidx[q]);
+      }
+    }
     if (a.trace && tid == 0) a.trace[3 * (size_t)it + 1] = gtimer();
     while (!mbar_try(&bar, phase)) {
     }
     phase ^= 1;
     __syncthreads();
-    // panel row i of the forward phase -> q_s or U_s (children's contributions added)
-    auto emit_f = [&](int i, double v) {
+    // panel row i (= r0 + tid + kq NT) of the forward phase -> q_s or U_s
+    auto emit_f = [&](int i, double v, int kq) {
       if (i < m.w) {
         a.q[m.dof0 + i] = v;
       } else if (i >= m.wp && i < m.wp + m.r) {
         const int k = i - m.wp;
-        for (int q = a.gptr[go + m.w + k]; q < a.gptr[go + m.w + k + 1]; ++q) v += __ldcg(a.U + a.gidx[q]);
+        if (kq < NCR) {
+#pragma unroll
+          for (int t = 0; t < NCR; ++t)
+            if (t == kq) v += crv[t];
+        } else {
+          for (int q = a.gptr[go + m.w + k]; q < a.gptr[go + m.w + k + 1]; ++q) v += __ldcg(a.U + a.gidx[q]);
+        }
         a.U[m.uoff + k] = v;
       }
     };
@@ -288,7 +307,7 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
             a1 += stg[(j + 1) * nr + i] * vs[j + 1];
           }
           if (j < nc) a0 += stg[j * nr + i] * vs[j];
-          if (m.ntb == 1) emit_f(m.r0 + i, a0 + a1);
+          if (m.ntb == 1) emit_f(m.r0 + i, a0 + a1, (i - tid) / NT);
           else P[m.t * nr + i] = a0 + a1;
         }
       } else {
@@ -302,7 +321,7 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
         if (tid < nr) {
           double v = 0.0;
           for (int k = 0; k < G; ++k) v += red[k * nr + tid];
-          if (m.ntb == 1) emit_f(m.r0 + tid, v);
+          if (m.ntb == 1) emit_f(m.r0 + tid, v, 0);
           else P[m.t * nr + tid] = v;
         }
       }
@@ -340,7 +359,7 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
         for (int o = tid; o < outs; o += NT) {
           double v = 0.0;
           for (int k = 0; k < m.ntb; ++k) v += __ldcg(P + k * stride + o);
-          if (fwd) emit_f(m.r0 + o, v);
+          if (fwd) emit_f(m.r0 + o, v, (o - tid) / NT);
           else emit_b(m.c0 + o, v);
         }
       }

@@ -36,6 +36,7 @@ struct ExpP {
   int ntiles;       // tiles of this launch (blocks loop over them with a grid stride)
   const int* tiles; // nullable: tile ids (x fastest) of a tile-list launch
   const uint8_t* clean;  // nullable: per tile id, 1 = every node it owns is wanted tensor-d
+  int ezl;          // 3D: element layers per tile along z
 };
 
 // tile coordinates of the tt-th tile of the launch: from the tile list if any, else linear
@@ -286,7 +287,7 @@ void tiling_p(const GridP& g, int ext[3], int tg[3]) {
   } else if (g.dim == 3) {
     if constexpr (P <= 6) {
       ext[0] = ext[1] = Tile3<P>::E;
-      ext[2] = Tile3<P>::EZ;
+      ext[2] = g.ezl > 0 ? g.ezl : Tile3<P>::EZ;
     }
   }
   for (int k = 0; k < 3; ++k) tg[k] = (g.N[k] + ext[k] - 1) / ext[k];
@@ -300,6 +301,7 @@ void launch_explicit_p(sc_ctx* c, const double* U, const double* Pv, double* out
   tiling_p<P>(g, ext, tg);
   e.tg[0] = tg[0];
   e.tg[1] = tg[1];
+  e.ezl = ext[2];
   e.ntiles = e.tiles ? n_tiles : tg[0] * tg[1] * tg[2];
   if (e.ntiles == 0) return;
   static int sms = 0;
@@ -314,7 +316,7 @@ void launch_explicit_p(sc_ctx* c, const double* U, const double* Pv, double* out
   } else {
     if constexpr (P <= 6) {
       using T = Tile3<P>;
-      auto kern = k_explicit_3d<P, T::E, T::E, T::EZ, T::NT, T::MINB, T::SPV>;
+      auto kern = k_explicit_3d<P, T::E, T::E, T::NT, T::MINB, T::SPV>;
       static bool attr = false;
       if (!attr) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::smem);
@@ -499,17 +501,23 @@ void build_graphs(sc_ctx* c) {
 // near-d tile list: tiles of the explicit kernel that own at least one type-4 node (a tile
 // owns nodes [ext*P*t, ext*P*(t+1)) per axis, the last tile also the final boundary node)
 void setup_step_structures(sc_ctx* c) {
-  const GridP& g = c->g;
+  GridP& g = c->g;
   c->n_near_tiles = c->n_far_tiles = 0;
   if (g.dim == 1) return;
   int ext[3], tg[3];
+  if (g.dim == 3) {
+    // longer z tiles amortise the warm-up layer, but keep >= 4 waves of 2 CTAs per SM
+    g.ezl = 16;
+    explicit_tiling(g, ext, tg);
+    if ((int64_t)tg[0] * tg[1] * tg[2] < 4 * 2 * 148) g.ezl = 8;
+  }
   explicit_tiling(g, ext, tg);
   // tile lists of the node types this rank updates: near-d (type 4) always, far-d (type 1)
   // when world > 1 (the rank's region only)
-  auto tiles_of = [&](uint8_t want, int** d, int* n) {
+  auto tiles_of = [&](unsigned want_mask, int** d, int* n) {
     std::vector<uint8_t> mark((size_t)tg[0] * tg[1] * tg[2], 0);
     for (int64_t L = 0; L < c->n_lat; ++L) {
-      if (c->ntype_rank[L] != want) continue;
+      if (!((want_mask >> c->ntype_rank[L]) & 1)) continue;
       int64_t r = L;
       int64_t t[3] = {0, 0, 0};
       for (int k = 0; k < g.dim; ++k) {
@@ -526,8 +534,10 @@ void setup_step_structures(sc_ctx* c) {
     SC_CUDA(cudaMalloc(d, sizeof(int) * std::max<size_t>(1, tiles.size())));
     if (!tiles.empty()) SC_CUDA(cudaMemcpy(*d, tiles.data(), sizeof(int) * tiles.size(), cudaMemcpyHostToDevice));
   };
-  if (c->n_near) tiles_of(4, &c->d_near_tiles, &c->n_near_tiles);
-  if (c->world > 1) tiles_of(1, &c->d_far_tiles, &c->n_far_tiles);
+  if (c->n_near) tiles_of(WANT_NEAR, &c->d_near_tiles, &c->n_near_tiles);
+  // world > 1: the tiles holding this rank's tensor-d nodes, far OR near (the combined
+  // launch updates both; a tile inside a void's c shell may hold near nodes only)
+  if (c->world > 1) tiles_of(WANT_FAR | WANT_NEAR, &c->d_far_tiles, &c->n_far_tiles);
   // clean tiles (3D): every node a tile owns is tensor-d (type 1 or 4) -> the combined
   // far+near launch needs no per-node type loads there
   if (g.dim == 3) {
