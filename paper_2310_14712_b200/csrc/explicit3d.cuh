@@ -39,7 +39,7 @@ __device__ __forceinline__ double inv_wt(int i, int e_cnt, int P) {
   return (e > 0 && e < e_cnt) ? c_iw2 : c_iw[0];
 }
 
-template <int P, int EX, int EY, int NT, bool SPV>
+template <int P, int EX, int EY, int NT, bool SPV, bool INT>
 __device__ __forceinline__ void explicit3d_tile(const double* __restrict__ U, const double* Pv, double* out,
                                                 const uint8_t* __restrict__ nt, const ExpP& e, int* flag,
                                                 const int3 tb, const bool clean) {
@@ -66,13 +66,17 @@ __device__ __forceinline__ void explicit3d_tile(const double* __restrict__ U, co
   const size_t pl = (size_t)nx * ny;
   const int EZ = e.ezl;   // element layers per tile along z (runtime, step.cu)
   const int ex0 = tb.x * EX, ey0 = tb.y * EY, ez0 = tb.z * EZ;
-  const int ex1 = min(ex0 + EX, Nx), ey1 = min(ey0 + EY, Ny), ez1 = min(ez0 + EZ, Nz);
-  const int nEX = ex1 - ex0, nEY = ey1 - ey0;
+  // INT: an interior tile (full EX x EY elements, neither on a low nor on a high x/y face of
+  // the box): every boundary test below folds at compile time
+  const int ex1 = INT ? ex0 + EX : min(ex0 + EX, Nx), ey1 = INT ? ey0 + EY : min(ey0 + EY, Ny);
+  const int ez1 = min(ez0 + EZ, Nz);
+  const int nEX = INT ? EX : ex1 - ex0, nEY = INT ? EY : ey1 - ey0;
+  const bool xlo = INT || ex0 > 0, ylo = INT || ey0 > 0;   // a halo element exists below
   const int xr0 = (ex0 - 1) * P, yr0 = (ey0 - 1) * P;
   const int gxmax = ex1 * P, gymax = ey1 * P;
   const int y0 = ey0 * P;
-  const int OY = nEY * P + (ey1 == Ny ? 1 : 0);
-  const bool lastx = (ex1 == Nx);
+  const int OY = INT ? EY * P : nEY * P + (ey1 == Ny ? 1 : 0);
+  const bool lastx = INT ? false : (ex1 == Nx);
   const int rin = lane / EXH, exl = lane % EXH;
 
   auto issue = [&](int ez, int buf) {
@@ -80,7 +84,7 @@ __device__ __forceinline__ void explicit3d_tile(const double* __restrict__ U, co
     for (int col = tid; col < RC; col += NT) {
       const int ix = col % RX, iy = col / RX;
       const int gx = xr0 + ix, gy = yr0 + iy;
-      const bool ok = gx >= 0 && gy >= 0 && gx <= gxmax && gy <= gymax;
+      const bool ok = INT || (gx >= 0 && gy >= 0 && gx <= gxmax && gy <= gymax);
       const double* src = U + (ok ? gx + (size_t)nx * gy + pl * (size_t)(ez * P) : 0);
 #pragma unroll
       for (int k = 0; k < P1; ++k) cp_async8(dst + k * RC + col, src + (ok ? pl * k : 0), ok);
@@ -170,7 +174,7 @@ __device__ __forceinline__ void explicit3d_tile(const double* __restrict__ U, co
       for (int q = 0; q < NYI; ++q) {
         const int it = tid + q * NT;
         const int ix = it % RX, eyl = it / RX;
-        if (it < RX * EYH && eyl <= nEY && (eyl > 0 || ey0 > 0)) {
+        if (it < RX * EYH && eyl <= nEY && (eyl > 0 || ylo)) {
           double sa[P1], sb[P1];
 #pragma unroll
           for (int j = 0; j < P1; ++j) {
@@ -223,10 +227,10 @@ __device__ __forceinline__ void explicit3d_tile(const double* __restrict__ U, co
 #pragma unroll
       for (int q = 0; q < NXI; ++q) {
         const int oy = (warp + q * NW) * RPW + rin;
-        const bool act = rin < RPW && oy < OY && exl <= nEX && (exl > 0 || ex0 > 0);
+        const bool act = rin < RPW && oy < OY && exl <= nEX && (exl > 0 || xlo);
         const int qq = oy / P;
         const bool hasA = oy < nEY * P;
-        const bool hasP = (oy - qq * P) == 0 && (qq > 0 || ey0 > 0);
+        const bool hasP = (oy - qq * P) == 0 && (qq > 0 || ylo);
         double r[P1];
 #pragma unroll
         for (int l = 0; l < P1; ++l) r[l] = 0.0;
@@ -264,7 +268,7 @@ __device__ __forceinline__ void explicit3d_tile(const double* __restrict__ U, co
           for (int l = 0; l < P1; ++l) {
             if ((e.want >> ntc[q][l]) & 1) {
               double rr = r[l];
-              if (l == 0 && (exl > 1 || ex0 > 0)) rr += left;
+              if (l == 0 && (exl > 1 || xlo)) rr += left;
               double pvv;
               if constexpr (SPV) pvv = prow[l];
               else pvv = pvc[q][l];
@@ -304,7 +308,12 @@ __global__ void __launch_bounds__(NT, MINB) k_explicit_3d(const double* __restri
                                                           int* flag) {
   for (int tt = blockIdx.x; tt < e.ntiles; tt += gridDim.x) {
     const int id = e.tiles ? e.tiles[tt] : tt;
-    explicit3d_tile<P, EX, EY, NT, SPV>(U, Pv, out, nt, e, flag, tile_of(e, tt), e.clean && e.clean[id]);
+    const int3 tb = tile_of(e, tt);
+    const bool clean = e.clean && e.clean[id];
+    if (tb.x > 0 && tb.y > 0 && (tb.x + 1) * EX < e.N[0] && (tb.y + 1) * EY < e.N[1])
+      explicit3d_tile<P, EX, EY, NT, SPV, true>(U, Pv, out, nt, e, flag, tb, clean);
+    else
+      explicit3d_tile<P, EX, EY, NT, SPV, false>(U, Pv, out, nt, e, flag, tb, clean);
   }
 }
 
