@@ -266,9 +266,20 @@ def main():
                            "frac": nbytes / (ms / 1e3) / 1e9 / peak}
     dom = max(breakdown, key=lambda k: breakdown[k]["ms"])
     bd = breakdown[dom]
+    # measured DRAM traffic per launch of that kernel from the committed ncu --set full capture
+    # of the same workload (scripts/ncu_traffic.py), when there is one
+    traffic, traffic_src = None, None
+    tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_config{cfg['id']}.json")
+    kname = {"explicit": "k_explicit_3d" if cfg["dim"] == 3 else f"k_explicit_{cfg['dim']}d",
+             "celem": "k_celem", "solve": "k_solve"}[dom]
+    if world == 1 and os.path.exists(tpath):
+        tj = json.load(open(tpath))
+        if kname in tj:
+            traffic, traffic_src = tj[kname]["bytes"], tj[kname]["report"]
     roof = {"kernel": kern[dom][2], "bound": "hbm", "achieved": bd["GBps"], "peak": peak, "unit": "GB/s",
-            "frac": bd["frac"], "traffic": None, "peak_kind": peak_kind, "kernel_ms": bd["ms"],
-            "share_of_step": bd["ms"] / (t_ms / K), "algorithmic_bytes": bd["algorithmic_bytes"]}
+            "frac": bd["frac"], "traffic": traffic, "traffic_source": traffic_src, "peak_kind": peak_kind,
+            "kernel_ms": bd["ms"], "share_of_step": bd["ms"] / (t_ms / K),
+            "algorithmic_bytes": bd["algorithmic_bytes"]}
     # ---- e2e through the public API with host buffers (pinned): the initial state goes
     # host -> device, K steps, the final displacement comes back device -> host
     u0t = torch.zeros(n_dof, dtype=torch.float64).pin_memory()

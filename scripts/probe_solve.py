@@ -20,8 +20,9 @@ def analyse(path):
     off = 8
     items = np.frombuffer(raw[off:off + 80 * n_items], np.int32).reshape(n_items, 20)
     off += 80 * n_items
-    tr = np.frombuffer(raw[off:off + 24 * n_items], np.uint64).reshape(n_items, 3).astype(np.int64)
-    off += 24 * n_items
+    tr5 = np.frombuffer(raw[off:off + 40 * n_items], np.uint64).reshape(n_items, 5).astype(np.int64)
+    off += 40 * n_items
+    tr = tr5[:, [1, 2, 4]]   # item known, gathered, done
     wrp = np.frombuffer(raw[off:off + 12 * n_sn], np.int32).reshape(3, n_sn)
     w, r, parent = wrp
     t0 = tr[:, 0].min()
@@ -32,7 +33,12 @@ def analyse(path):
             height[parent[s]] = max(height[parent[s]], height[s] + 1)
     ph = items[:, 0]
     fused = items[:, 3] == 1   # single-tile groups
-    out = {"span_us": float(tr[:, 2].max() / 1e3), "n_items": int(n_items),
+    d = np.diff(tr5 - tr5[:, :1], axis=1) / 1e3
+    out = {"stage_us_median": {k: round(float(np.median(d[:, i])), 2) for i, k in
+                               enumerate(["claim->item", "item->gathered", "gathered->staged", "staged->done"])},
+           "stage_us_p90": {k: round(float(np.percentile(d[:, i], 90)), 2) for i, k in
+                            enumerate(["claim->item", "item->gathered", "gathered->staged", "staged->done"])},
+           "span_us": float(tr[:, 2].max() / 1e3), "n_items": int(n_items),
            "fused_work_us_mean": float((tr[fused, 2] - tr[fused, 1]).mean() / 1e3) if fused.any() else None,
            "tiled_work_us_mean": float((tr[~fused, 2] - tr[~fused, 1]).mean() / 1e3) if (~fused).any() else None,
            "wait_us_mean": float((tr[:, 1] - tr[:, 0]).mean() / 1e3)}
@@ -85,7 +91,7 @@ if __name__ == "__main__":
         variants = sys.argv[2:] or ["256:16384"]
         for k, v in enumerate(variants):
             tile, fuse = map(int, v.split(":"))
-            tp = f"gpurun_out/trace_c{cid}_{tile}_{fuse}.bin"
+            tp = f"/tmp/trace_c{cid}_{tile}_{fuse}.bin"
             run_variant(cid, tile, fuse, tp)
             if os.path.exists(tp):
                 analyse(tp)
