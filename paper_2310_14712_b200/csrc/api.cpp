@@ -19,7 +19,7 @@ static sc_status fail(sc_ctx* c, const ScError& e) {
 static void dump_trace(sc_ctx* c) {
   const char* path = getenv("SC_TRACE");
   if (!path || !c->d_trace || c->n_items == 0) return;
-  std::vector<unsigned long long> t(3 * (size_t)c->n_items);
+  std::vector<unsigned long long> t(5 * (size_t)c->n_items);
   if (cudaMemcpy(t.data(), c->d_trace, sizeof(unsigned long long) * t.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
     return;
   FILE* f = fopen(path, "wb");

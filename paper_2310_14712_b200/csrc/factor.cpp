@@ -1025,7 +1025,7 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   sd.prefetch = getenv("SC_SOLVE_PREFETCH") ? atoi(getenv("SC_SOLVE_PREFETCH")) : 0;
   sd.trace = nullptr;
   if (getenv("SC_TRACE")) {
-    SC_CUDA(cudaMalloc(&c->d_trace, sizeof(unsigned long long) * 3 * std::max(1, c->n_items)));
+    SC_CUDA(cudaMalloc(&c->d_trace, sizeof(unsigned long long) * 5 * std::max(1, c->n_items)));
     sd.trace = c->d_trace;
   }
   if (c->world > 1) build_exchange(c, c_owner, clat_global);

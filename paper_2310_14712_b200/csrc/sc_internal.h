@@ -60,7 +60,7 @@ struct SolveDev {
   int tile;                    // reduction-tile length (SOLVE_TILE)
   int stage;                   // staging buffer (doubles; two per CTA)
   int prefetch;                // SC_SOLVE_PREFETCH=1: L2 bulk prefetch of a phase's panel at push
-  unsigned long long* trace;   // optional (SC_TRACE): per item [dequeued, deps met, done] ns
+  unsigned long long* trace;   // optional (SC_TRACE): per item [claim, item, gathered, staged, done] ns
 };
 
 // Device factor of one SPD matrix (S or M^cc), shared symbolic structure.  For supernode s

@@ -214,7 +214,9 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
   unsigned phase = 0;
   while (true) {
     __syncthreads();   // previous item fully consumed (stage buffer and vs free)
+    unsigned long long tclaim = 0;
     if (tid == 0) {
+      if (a.trace) tclaim = gtimer();
       const int h = atomicAdd(a.head, 1);
       int itm = -1;
       if (h < a.n_items) {
@@ -238,7 +240,10 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
     if (it < 0) return;
     const Item m = load_item(a, it);
     const bool fwd = (m.type == IT_F);
-    if (a.trace && tid == 0) a.trace[3 * (size_t)it] = gtimer();
+    if (a.trace && tid == 0) {
+      a.trace[5 * (size_t)it] = tclaim;
+      a.trace[5 * (size_t)it + 1] = gtimer();
+    }
     // ---- stream the panel tile (TMA) and gather the input vector meanwhile (every producer
     // of it completed before this item was pushed; L1 bypass)
     if (warp == 0) stage_item(a, m, stg, &bar, lane);
@@ -269,10 +274,11 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
         for (int q = a.gptr[go + kk]; q < a.gptr[go + kk + 1]; ++q) crv[k] += __ldcg(a.U + a.gidx[q]);
       }
     }
-    if (a.trace && tid == 0) a.trace[3 * (size_t)it + 1] = gtimer();
+    if (a.trace && tid == 0) a.trace[5 * (size_t)it + 2] = gtimer();
     while (!mbar_try(&bar, phase)) {
     }
     phase ^= 1;
+    if (a.trace && tid == 0) a.trace[5 * (size_t)it + 3] = gtimer();
     __syncthreads();
     // panel row i (= r0 + tid + kq NT) of the forward phase -> q_s or U_s
     auto emit_f = [&](int i, double v, int kq) {
@@ -368,7 +374,7 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
       __syncthreads();   // the CTA's result stores precede lane 0's releasing fence (cumulative)
       if (warp == 0) complete_block(a, fwd ? 0 : 1, m.s, lane);
     }
-    if (a.trace && tid == 0) a.trace[3 * (size_t)it + 2] = gtimer();
+    if (a.trace && tid == 0) a.trace[5 * (size_t)it + 4] = gtimer();
   }
 }
 
