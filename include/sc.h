@@ -174,6 +174,12 @@ sc_status sc_read_owned(sc_ctx* ctx, double* u, int64_t len);
  * streams).  ctxs[r] must be rank r. */
 sc_status sc_exchange_local(sc_ctx* const* ctxs, int32_t world);
 
+/* Critical time step of the explicit subsystem:
+ * `iters` power iterations for lambda_max of M_dd^{-1} K_dd on the device (c DOFs held at
+ * zero), dt_crit = 2 / sqrt(lambda_max).  The estimate approaches lambda_max from below.
+ * Clobbers the state: call sc_set_state before stepping again.  One rank only. */
+sc_status sc_estimate_dt(sc_ctx* ctx, int32_t iters, double* lambda_max, double* dt_crit);
+
 /* A new 128-byte ncclUniqueId (world > 1 over NCCL; call on one rank and broadcast). */
 sc_status sc_nccl_unique_id(void* out128);
 

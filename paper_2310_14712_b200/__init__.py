@@ -60,7 +60,7 @@ class sc_info(ctypes.Structure):
 
 EXPORTS = ("sc_setup", "sc_set_state", "sc_step", "sc_sync", "sc_read", "sc_read_owned", "sc_read_c_state",
            "sc_query", "sc_read_classification", "sc_dof_coords", "sc_profile", "sc_exchange_local",
-           "sc_nccl_unique_id", "sc_last_error", "sc_destroy")
+           "sc_nccl_unique_id", "sc_estimate_dt", "sc_last_error", "sc_destroy")
 
 _lib = None
 
@@ -84,6 +84,7 @@ def load_library(path=LIB_PATH):
     lib.sc_read_owned.argtypes = [ctypes.c_void_p, P(ctypes.c_double), ctypes.c_int64]
     lib.sc_exchange_local.argtypes = [P(ctypes.c_void_p), ctypes.c_int32]
     lib.sc_nccl_unique_id.argtypes = [ctypes.c_void_p]
+    lib.sc_estimate_dt.argtypes = [ctypes.c_void_p, ctypes.c_int32, P(ctypes.c_double), P(ctypes.c_double)]
     lib.sc_read_c_state.argtypes = [ctypes.c_void_p, P(ctypes.c_double), P(ctypes.c_double), ctypes.c_int64]
     lib.sc_query.argtypes = [ctypes.c_void_p, P(sc_info)]
     lib.sc_read_classification.argtypes = [ctypes.c_void_p, P(ctypes.c_int8), P(ctypes.c_uint8),
@@ -203,6 +204,13 @@ class Solver:
         """Write the DOFs this rank owns into ``out`` (length n_dof; other entries untouched)."""
         self._check(self._lib.sc_read_owned(self.ctx, _dptr(out), len(out)))
         return out
+
+    def estimate_dt(self, iters=2000):
+        """(lambda_max, dt_crit) of the explicit subsystem by device power iteration
+        (clobbers the state: call set_state before stepping again)."""
+        lam, dt = ctypes.c_double(), ctypes.c_double()
+        self._check(self._lib.sc_estimate_dt(self.ctx, int(iters), ctypes.byref(lam), ctypes.byref(dt)))
+        return lam.value, dt.value
 
     def read_c_state(self):
         n = self.info["n_c"]

@@ -387,6 +387,23 @@ extern "C" sc_status sc_exchange_local(sc_ctx* const* ctxs, int32_t world) {
   }
 }
 
+extern "C" sc_status sc_estimate_dt(sc_ctx* c, int32_t iters, double* lambda_max, double* dt_crit) {
+  if (!c) return SC_ERR_STATE;
+  if (iters < 1 || c->world > 1) {
+    c->err = "sc_estimate_dt: iters >= 1, one rank";
+    return SC_ERR_CONFIG;
+  }
+  try {
+    SC_CUDA(cudaSetDevice(c->device));
+    const double lam = estimate_lambda(c, iters);
+    if (lambda_max) *lambda_max = lam;
+    if (dt_crit) *dt_crit = lam > 0.0 ? 2.0 / std::sqrt(lam) : 0.0;
+    return SC_OK;
+  } catch (const ScError& e) {
+    return fail(c, e);
+  }
+}
+
 extern "C" sc_status sc_nccl_unique_id(void* out128) {
   try {
     nccl_unique_id(out128);

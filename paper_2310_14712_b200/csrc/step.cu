@@ -102,8 +102,8 @@ __global__ void k_irregular(const double* __restrict__ U, const double* Pv, doub
                             const double* __restrict__ invm, const double* __restrict__ fx, int n,
                             const int8_t* __restrict__ cls, const double* __restrict__ Kref, GridP g,
                             const double* __restrict__ ft, long long n_t, const long long* step, double a1,
-                            double a2, double a3, int* flag) {
-  // one warp per node; lanes split the element-local dot products
+                            double a2, double a3, int* flag, double fsc) {
+  // one warp per node; lanes split the element-local dot products (fsc scales the load term)
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= n) return;
@@ -155,7 +155,7 @@ __global__ void k_irregular(const double* __restrict__ U, const double* Pv, doub
 #pragma unroll
   for (int o = 16; o; o >>= 1) Ku += __shfl_xor_sync(0xffffffffu, Ku, o);
   if (lane) return;
-  const double r = ft_at(ft, n_t, step, 0) * fx[t] - Ku;
+  const double r = fsc * ft_at(ft, n_t, step, 0) * fx[t] - Ku;
   const double res = a1 * U[L] + a2 * Pv[L] + a3 * r * invm[t];
   out[L] = res;
   if (!isfinite(res)) atomicExch(flag, 1);
@@ -399,11 +399,11 @@ static void launch_celem(sc_ctx* c, int mode, const double* A, const double* B, 
 }
 
 static void launch_irregular(sc_ctx* c, const double* U, const double* Pv, double* out, double a1, double a2,
-                             double a3, cudaStream_t st) {
+                             double a3, cudaStream_t st, double fsc = 1.0) {
   if (c->n_irr == 0) return;
   k_irregular<<<(unsigned)((c->n_irr * 32 + 127) / 128), 128, 0, st>>>(
       U, Pv, out, c->d_irr_lat, c->d_irr_invm, c->d_irr_fx, (int)c->n_irr, c->d_cell_class, c->d_Kref, c->g,
-      c->d_ft, c->n_t, c->d_step, a1, a2, a3, c->d_flag);
+      c->d_ft, c->n_t, c->d_step, a1, a2, a3, c->d_flag, fsc);
   SC_CUDA(cudaGetLastError());
 }
 
@@ -677,4 +677,94 @@ void profile_launch(sc_ctx* c, int which) {
   else if (which == 1) launch_celem(c, 0, A, B, c->stream);
   else if (which == 2) launch_solve(c, c->fS, c->stream);
   else launch_explicit(c, A, B, B, 2.0, -1.0, c->dt * c->dt, 4, c->stream);
+}
+
+// ---- NEXT-2: critical time step of the explicit subsystem on the device.
+// Power iteration for lambda_max of M_dd^{-1} K_dd (dt_crit = 2 / omega_max): the
+// operator is the explicit kernels themselves with a1 = a2 = 0, a3 = -1 and no load, applied
+// to vectors that vanish off the d DOFs (so the c DOFs are held at zero: the IMEX limit is
+// that of the d subsystem).  Rayleigh-type estimate (x.y)/(x.x); deterministic
+// two-pass reductions.  Clobbers the state (both lattice buffers).
+namespace {
+__global__ void k_power_init(double* x, const uint8_t* __restrict__ nt, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint8_t t = nt[i];
+  // deterministic pseudo-random start in [0.5, 1.5) on the d DOFs
+  unsigned long long z = (unsigned long long)i * 0x9E3779B97F4A7C15ull;
+  z ^= z >> 29;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 32;
+  x[i] = (t == 1 || t == 2 || t == 4) ? 0.5 + (double)(z >> 11) * (1.0 / 9007199254740992.0) : 0.0;
+}
+// per-block partial sums of x.y, x.x, y.y
+__global__ void k_dots(const double* __restrict__ x, const double* __restrict__ y, long long n, double* part) {
+  __shared__ double sh[3][8];
+  double a = 0.0, b = 0.0, cc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double xi = x[i], yi = y[i];
+    a += xi * yi;
+    b += xi * xi;
+    cc += yi * yi;
+  }
+  for (int o = 16; o; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+    cc += __shfl_xor_sync(0xffffffffu, cc, o);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+    sh[0][w] = a;
+    sh[1][w] = b;
+    sh[2][w] = cc;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double s = 0.0;
+    for (int k = 0; k < 8; ++k) s += sh[threadIdx.x][k];
+    part[3 * blockIdx.x + threadIdx.x] = s;
+  }
+}
+// sums the partials (fixed order), records lambda_k = (x.y)/(x.x), scale = 1/|y|
+__global__ void k_dots_final(const double* part, int nblk, double* out) {
+  double a = 0.0, b = 0.0, cc = 0.0;
+  for (int k = 0; k < nblk; ++k) {
+    a += part[3 * k];
+    b += part[3 * k + 1];
+    cc += part[3 * k + 2];
+  }
+  out[0] = a / b;
+  out[1] = cc > 0.0 ? 1.0 / sqrt(cc) : 0.0;
+}
+__global__ void k_scale_into(double* x, const double* __restrict__ y, const double* sc, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) x[i] = y[i] * sc[1];
+}
+}  // namespace
+
+double estimate_lambda(sc_ctx* c, int iters) {
+  const long long n = c->n_lat;
+  double* X = c->d_u[0];
+  double* Y = c->d_u[1];
+  const int nblk = 148 * 4;
+  double* scratch = nullptr;
+  SC_CUDA(cudaMalloc(&scratch, sizeof(double) * (3 * nblk + 2)));
+  double* part = scratch;
+  double* res = scratch + 3 * nblk;
+  const unsigned gb = (unsigned)((n + 255) / 256);
+  k_power_init<<<gb, 256, 0, c->stream>>>(X, c->d_ntype, n);
+  for (int k = 0; k < iters; ++k) {
+    SC_CUDA(cudaMemsetAsync(Y, 0, sizeof(double) * n, c->stream));
+    launch_explicit(c, X, X, Y, 0.0, 0.0, -1.0, 5, c->stream);
+    launch_irregular(c, X, X, Y, 0.0, 0.0, -1.0, c->stream, 0.0);
+    k_dots<<<nblk, 256, 0, c->stream>>>(X, Y, n, part);
+    k_dots_final<<<1, 1, 0, c->stream>>>(part, nblk, res);
+    k_scale_into<<<gb, 256, 0, c->stream>>>(X, Y, res, n);
+  }
+  double h[2] = {0.0, 0.0};
+  SC_CUDA(cudaMemcpyAsync(h, res, sizeof(double) * 2, cudaMemcpyDeviceToHost, c->stream));
+  SC_CUDA(cudaStreamSynchronize(c->stream));
+  cudaFree(scratch);
+  c->far_ready = false;
+  return h[0];
 }
