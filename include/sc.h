@@ -69,7 +69,7 @@ typedef struct {
 
 /* Geometry and material.  tree_depth = spacetree depth D; lattice_s = s of the
  * cut-test lattice (reading C6, default 4); fill_eps = empty-cell threshold (P:866-868,
- * default 1e-10; reading C7); rho, c constant (reading C10). */
+ * default 1e-10; reading C7); rho, c constant (reading C10); integrator below. */
 typedef struct {
   int32_t n_voids;
   const sc_void* voids;
@@ -78,6 +78,9 @@ typedef struct {
   double fill_eps;
   double rho;
   double c;
+  int32_t integrator; /* 0: Newmark IMEX (the method); 1: CDM on the HRZ-lumped SCM, the
+                         paper's explicit comparison scheme (every DOF explicit, cut
+                         cells HRZ-lumped; needs dt below its much smaller critical step) */
 } sc_geometry;
 
 /* Separable point source f(x,t) = f_t(t) delta(x - x_s) (reading C11):
@@ -176,9 +179,20 @@ sc_status sc_exchange_local(sc_ctx* const* ctxs, int32_t world);
 
 /* Critical time step of the explicit subsystem:
  * `iters` power iterations for lambda_max of M_dd^{-1} K_dd on the device (c DOFs held at
- * zero), dt_crit = 2 / sqrt(lambda_max).  The estimate approaches lambda_max from below.
+ * zero; with integrator 1 of M~^{-1} K over all DOFs), dt_crit = 2 / sqrt(lambda_max).  The estimate approaches lambda_max from below.
  * Clobbers the state: call sc_set_state before stepping again.  One rank only. */
 sc_status sc_estimate_dt(sc_ctx* ctx, int32_t iters, double* lambda_max, double* dt_crit);
+
+/* Receivers (the paper's receiver traces, fig:solutions3D):
+ * record u(x_r, t_{n+1}) = sum_i N_i(x_r) u_i (basis of the lowest-index non-empty cell
+ * containing x_r) after every step; xyz: n points (x, y, z) each (unused dims ignored);
+ * capacity: rows kept (steps after the last sc_set_state / setup; later rows dropped).
+ * Replaces any previous set; n = 0 removes the receivers.  One rank only. */
+sc_status sc_set_receivers(sc_ctx* ctx, const double* xyz, int32_t n, int64_t capacity);
+
+/* Copy the recorded rows (row k = after step k+1, n_rec values each) to out (host,
+ * max_rows x n_rec); *rows receives the number of rows copied.  Synchronises. */
+sc_status sc_read_traces(sc_ctx* ctx, double* out, int64_t max_rows, int64_t* rows);
 
 /* A new 128-byte ncclUniqueId (world > 1 over NCCL; call on one rank and broadcast). */
 sc_status sc_nccl_unique_id(void* out128);

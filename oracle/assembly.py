@@ -159,6 +159,36 @@ def point_load(cfg, cl, x):
     raise ValueError("source point is outside every non-empty cell")
 
 
+def point_values(cfg, cl, x):
+    """Receiver weights: u(x) = sum_i N_i(x) u_i with the basis of the lowest-index
+    non-empty cell containing x (the evaluation point_load uses, without alpha; SURVEY
+    NEXT-3, the paper's receiver traces P:1758-1765)."""
+    d = cfg["dim"]
+    grid = cl.grid
+    cand = []
+    for k in range(d):
+        ks = []
+        for e in range(grid["cells"][k]):
+            lo_e = grid["lo"][k] + (grid["hi"][k] - grid["lo"][k]) * (np.float64(e) / grid["cells"][k])
+            hi_e = grid["lo"][k] + (grid["hi"][k] - grid["lo"][k]) * (np.float64(e + 1) / grid["cells"][k])
+            if lo_e <= x[k] <= hi_e:
+                ks.append(e)
+        cand.append(ks)
+    cells = [()]
+    for k in range(d):
+        cells = [c + (e,) for c in cells for e in cand[k]]
+    N = grid["cells"]
+    cells.sort(key=lambda c: sum(c[k] * int(np.prod(N[:k])) for k in range(d)))
+    for c in cells:
+        ci = sum(c[k] * int(np.prod(N[:k])) for k in range(d))
+        if cl.cell_class[ci] == EMPTY:
+            continue
+        w = np.zeros(cl.n_dof)
+        w[cl.dof_of_lattice[cl.enodes[ci]]] += eval_basis_at(grid, c, np.asarray(x[:d], dtype=np.float64), cfg["p"])
+        return w
+    raise ValueError("point outside every non-empty cell")
+
+
 def build_system(cfg, mode="sparse", cl=None):
     """Assemble the partitioned system of P:449-543 for the input dict."""
     if cl is None:
@@ -253,6 +283,25 @@ def build_system(cfg, mode="sparse", cl=None):
     else:
         sysm.f_x = np.zeros(n)
     return sysm
+
+
+def hrz_element(Me):
+    """HRZ lumping of a consistent element mass (§Lumping of Cut Cells):
+    M~_ii = m_e / (sum_k M_kk) * M_ii with m_e = sum_ij M_ij (the element's total mass),
+    M~_ij = 0 for i != j.  Returns the diagonal."""
+    Me = np.asarray(Me, dtype=np.float64)
+    d = np.diag(Me)
+    return Me.sum() / d.sum() * d
+
+
+def hrz_mass(sysm):
+    """Global diagonal mass of the HRZ-lumped SCM: nodally lumped uncut cells plus
+    HRZ-lumped cut cells."""
+    n = sysm.n_dof
+    m = np.bincount(sysm.uncut_dofs.ravel(), weights=np.tile(sysm.Me_uncut, len(sysm.uncut_dofs)), minlength=n)
+    for e in range(len(sysm.cut_dofs)):
+        m += np.bincount(sysm.cut_dofs[e], weights=hrz_element(sysm.cut_M[e]), minlength=n)
+    return m
 
 
 def K_apply(sysm, u):

@@ -30,7 +30,8 @@ class sc_void(ctypes.Structure):
 class sc_geometry(ctypes.Structure):
     _fields_ = [("n_voids", ctypes.c_int32), ("voids", ctypes.POINTER(sc_void)),
                 ("tree_depth", ctypes.c_int32), ("lattice_s", ctypes.c_int32),
-                ("fill_eps", ctypes.c_double), ("rho", ctypes.c_double), ("c", ctypes.c_double)]
+                ("fill_eps", ctypes.c_double), ("rho", ctypes.c_double), ("c", ctypes.c_double),
+                ("integrator", ctypes.c_int32)]
 
 
 class sc_source(ctypes.Structure):
@@ -60,7 +61,8 @@ class sc_info(ctypes.Structure):
 
 EXPORTS = ("sc_setup", "sc_set_state", "sc_step", "sc_sync", "sc_read", "sc_read_owned", "sc_read_c_state",
            "sc_query", "sc_read_classification", "sc_dof_coords", "sc_profile", "sc_exchange_local",
-           "sc_nccl_unique_id", "sc_estimate_dt", "sc_last_error", "sc_destroy")
+           "sc_nccl_unique_id", "sc_estimate_dt", "sc_set_receivers", "sc_read_traces", "sc_last_error",
+           "sc_destroy")
 
 _lib = None
 
@@ -85,6 +87,8 @@ def load_library(path=LIB_PATH):
     lib.sc_exchange_local.argtypes = [P(ctypes.c_void_p), ctypes.c_int32]
     lib.sc_nccl_unique_id.argtypes = [ctypes.c_void_p]
     lib.sc_estimate_dt.argtypes = [ctypes.c_void_p, ctypes.c_int32, P(ctypes.c_double), P(ctypes.c_double)]
+    lib.sc_set_receivers.argtypes = [ctypes.c_void_p, P(ctypes.c_double), ctypes.c_int32, ctypes.c_int64]
+    lib.sc_read_traces.argtypes = [ctypes.c_void_p, P(ctypes.c_double), ctypes.c_int64, P(ctypes.c_int64)]
     lib.sc_read_c_state.argtypes = [ctypes.c_void_p, P(ctypes.c_double), P(ctypes.c_double), ctypes.c_int64]
     lib.sc_query.argtypes = [ctypes.c_void_p, P(sc_info)]
     lib.sc_read_classification.argtypes = [ctypes.c_void_p, P(ctypes.c_int8), P(ctypes.c_uint8),
@@ -141,7 +145,8 @@ class Solver:
                     arr[i].n[k] = v["n"][k]
                 arr[i].b = v["b"]
         geo = sc_geometry(len(vs), arr, geometry.get("tree_depth", 2), geometry.get("lattice_s", 4),
-                          geometry.get("fill_eps", 1e-10), geometry.get("rho", 1.0), geometry.get("c", 1.0))
+                          geometry.get("fill_eps", 1e-10), geometry.get("rho", 1.0), geometry.get("c", 1.0),
+                          {"imex": 0, "cdm_hrz": 1}[geometry.get("integrator", "imex")])
         src = None
         self._ft = None
         if source is not None:
@@ -204,6 +209,21 @@ class Solver:
         """Write the DOFs this rank owns into ``out`` (length n_dof; other entries untouched)."""
         self._check(self._lib.sc_read_owned(self.ctx, _dptr(out), len(out)))
         return out
+
+    def set_receivers(self, xyz, capacity):
+        """Record u at the points xyz (n x 3) after every step (at most `capacity` rows)."""
+        X = np.ascontiguousarray(np.asarray(xyz, dtype=np.float64).reshape(-1, 3))
+        self._n_rec = len(X)
+        self._check(self._lib.sc_set_receivers(self.ctx, _dptr(X), len(X), int(capacity)))
+
+    def traces(self, max_rows=None):
+        """Recorded receiver rows (rows x n_rec): row k is u after step k+1."""
+        n = getattr(self, "_n_rec", 0)
+        cap = max_rows if max_rows is not None else self.query()["step"]
+        out = np.zeros((max(cap, 1), max(n, 1)))
+        rows = ctypes.c_int64()
+        self._check(self._lib.sc_read_traces(self.ctx, _dptr(out), int(cap), ctypes.byref(rows)))
+        return out[:rows.value, :n]
 
     def estimate_dt(self, iters=2000):
         """(lambda_max, dt_crit) of the explicit subsystem by device power iteration
@@ -290,6 +310,7 @@ def from_config(cfg, f_t=None, stream=None, device=None, set_initial=True, rank=
             f_t = source_signal(cfg)
         src = {"x": cfg["source"]["x"], "f_t": f_t}
     geo = {k: cfg[k] for k in ("voids", "tree_depth", "lattice_s", "fill_eps", "rho", "c")}
+    geo["integrator"] = cfg.get("integrator", "imex")
     s = Solver(cfg, cfg["p"], cfg["alpha"], geo, cfg["dt"], source=src, stream=stream, device=device,
                rank=rank, world=world, nccl_id=nccl_id)
     s._n_cells = int(np.prod(cfg["cells"]))

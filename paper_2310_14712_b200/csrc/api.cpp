@@ -1,4 +1,5 @@
 // C ABI entry points of libsc (include/sc.h).
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -46,8 +47,7 @@ static void free_ctx(sc_ctx* c) {
     nccl_destroy(c);
   } catch (const ScError&) {
   }
-  for (int i = 0; i < 2; ++i)
-    if (c->graph[i]) cudaGraphExecDestroy(c->graph[i]);
+  destroy_graphs(c);
   void* ptrs[] = {c->d_voids, c->d_u[0], c->d_u[1], c->d_ntype, c->d_cell_class, c->d_dof_lat, c->d_out,
                   c->d_ft, c->d_step, c->d_flag, c->d_irr_lat, c->d_irr_invm, c->d_irr_fx, c->d_Kref,
                   c->d_c_lat, c->d_vc, c->d_ac, c->d_fxc, c->d_b, c->d_q, c->d_x, c->d_U,
@@ -56,7 +56,8 @@ static void free_ctx(sc_ctx* c) {
                   c->d_sn_uoff, c->d_sn_goff, c->d_R, c->d_gptr, c->d_gidx, c->d_items, c->fS.A,
                   c->fM.A, c->fS.d, c->fM.d, c->d_tmp, c->d_nitem, c->d_chptr, c->d_chidx, c->d_parent, c->d_solve_cnt,
                   c->d_part, c->d_trace, c->d_near_tiles, c->d_qmeta, c->d_far_tiles, c->d_xs_idx, c->d_xr_idx,
-                  c->d_xs_buf, c->d_xr_buf, c->d_own_lat, c->d_own_dof, c->d_full, c->d_clean};
+                  c->d_xs_buf, c->d_xr_buf, c->d_own_lat, c->d_own_dof, c->d_full, c->d_clean, c->d_rec_lat, c->d_rec_w,
+                  c->d_rec_trace, c->d_mc};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -150,6 +151,8 @@ extern "C" sc_status sc_setup(const sc_grid* grid, int32_t p, double alpha, cons
     c->c = geom->c;
     c->dt = dt;
     c->fill_eps = geom->fill_eps;
+    if (geom->integrator != 0 && geom->integrator != 1) throw ScError(SC_ERR_CONFIG, "integrator must be 0 or 1");
+    c->integrator = geom->integrator;
     for (int i = 0; i < geom->n_voids; ++i) {
       DVoid v;
       std::memset(&v, 0, sizeof(v));
@@ -399,6 +402,63 @@ extern "C" sc_status sc_estimate_dt(sc_ctx* c, int32_t iters, double* lambda_max
     if (lambda_max) *lambda_max = lam;
     if (dt_crit) *dt_crit = lam > 0.0 ? 2.0 / std::sqrt(lam) : 0.0;
     return SC_OK;
+  } catch (const ScError& e) {
+    return fail(c, e);
+  }
+}
+
+extern "C" sc_status sc_set_receivers(sc_ctx* c, const double* xyz, int32_t n, int64_t capacity) {
+  if (!c) return SC_ERR_STATE;
+  if (n < 0 || (n > 0 && (!xyz || capacity < 1)) || c->world > 1) {
+    c->err = "sc_set_receivers: n >= 0 points (xyz[3n]), capacity >= 1 rows, one rank";
+    return SC_ERR_CONFIG;
+  }
+  try {
+    SC_CUDA(cudaSetDevice(c->device));
+    SC_CUDA(cudaStreamSynchronize(c->stream));
+    const int nb = c->nb;
+    std::vector<int32_t> lat((size_t)n * nb, 0);
+    std::vector<double> w((size_t)n * nb, 0.0);
+    std::vector<std::pair<int64_t, double>> pw;
+    for (int r = 0; r < n; ++r) {
+      point_weights(c, xyz + 3 * (size_t)r, false, pw);
+      for (size_t k = 0; k < pw.size(); ++k) {
+        lat[(size_t)r * nb + k] = (int32_t)pw[k].first;
+        w[(size_t)r * nb + k] = pw[k].second;
+      }
+    }
+    for (void* p : {(void*)c->d_rec_lat, (void*)c->d_rec_w, (void*)c->d_rec_trace})
+      if (p) cudaFree(p);
+    c->d_rec_lat = nullptr;
+    c->d_rec_w = nullptr;
+    c->d_rec_trace = nullptr;
+    c->n_rec = n;
+    c->rec_cap = n ? capacity : 0;
+    if (n) {
+      SC_CUDA(cudaMalloc(&c->d_rec_lat, sizeof(int32_t) * lat.size()));
+      SC_CUDA(cudaMalloc(&c->d_rec_w, sizeof(double) * w.size()));
+      SC_CUDA(cudaMalloc(&c->d_rec_trace, sizeof(double) * (size_t)n * capacity));
+      SC_CUDA(cudaMemcpy(c->d_rec_lat, lat.data(), sizeof(int32_t) * lat.size(), cudaMemcpyHostToDevice));
+      SC_CUDA(cudaMemcpy(c->d_rec_w, w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice));
+      SC_CUDA(cudaMemset(c->d_rec_trace, 0, sizeof(double) * (size_t)n * capacity));
+    }
+    destroy_graphs(c);
+    build_graphs(c);
+    return SC_OK;
+  } catch (const ScError& e) {
+    return fail(c, e);
+  }
+}
+
+extern "C" sc_status sc_read_traces(sc_ctx* c, double* out, int64_t max_rows, int64_t* rows) {
+  if (!c) return SC_ERR_STATE;
+  try {
+    SC_CUDA(cudaSetDevice(c->device));
+    const int64_t nr = std::min<int64_t>(std::min<int64_t>(c->host_step, c->rec_cap), std::max<int64_t>(0, max_rows));
+    if (rows) *rows = nr;
+    if (nr > 0 && c->n_rec > 0 && out)
+      SC_CUDA(cudaMemcpyAsync(out, c->d_rec_trace, sizeof(double) * nr * c->n_rec, cudaMemcpyDeviceToHost, c->stream));
+    return sc_sync(c);
   } catch (const ScError& e) {
     return fail(c, e);
   }

@@ -283,6 +283,56 @@ static void nested_dissection(Builder& b, int comp, std::vector<int>& nodes, std
   rec(nodes, roots);
 }
 
+// Basis functions of the lowest-index non-empty cell containing x at x (P:456-459 for the
+// point load, reading C11): out = (lattice index, [alpha(x)] N_i(x)) for the nonzero N_i.
+void point_weights(const sc_ctx* c, const double* x, bool with_alpha,
+                   std::vector<std::pair<int64_t, double>>& out) {
+  const GridP& g = c->g;
+  const int n1 = g.p + 1, nb = c->nb;
+  out.clear();
+  int64_t cand[3][2];
+  int nc[3] = {1, 1, 1};
+  for (int k = 0; k < 3; ++k) {
+    cand[k][0] = 0;
+    if (k >= g.dim) continue;
+    nc[k] = 0;
+    for (int64_t e = 0; e < g.N[k]; ++e) {
+      double lo = host_lattice(g.lo[k], g.hi[k], e, g.N[k]);
+      double hi = host_lattice(g.lo[k], g.hi[k], e + 1, g.N[k]);
+      if (lo <= x[k] && x[k] <= hi && nc[k] < 2) cand[k][nc[k]++] = e;
+    }
+    if (nc[k] == 0) throw ScError(SC_ERR_CONFIG, "point outside the grid");
+  }
+  // lowest linear index first: iterate z, y, x ascending
+  for (int a2 = 0; a2 < nc[2]; ++a2)
+    for (int a1 = 0; a1 < nc[1]; ++a1)
+      for (int a0 = 0; a0 < nc[0]; ++a0) {
+        int64_t ci[3] = {cand[0][a0], cand[1][a1], cand[2][a2]};
+        int64_t cl = cell_lin(g, ci);
+        if (c->cell_class[cl] == 2) continue;
+        double xs[3] = {x[0], g.dim > 1 ? x[1] : 0.0, g.dim > 2 ? x[2] : 0.0};
+        const double al = (!with_alpha || host_phys(c->voids, xs)) ? 1.0 : c->alpha;
+        double v[3][SC_MAXP1];
+        for (int k = 0; k < 3; ++k) {
+          if (k < g.dim) {
+            double lo = host_lattice(g.lo[k], g.hi[k], ci[k], g.N[k]);
+            double hi = host_lattice(g.lo[k], g.hi[k], ci[k] + 1, g.N[k]);
+            double xi = -1.0 + 2.0 * (xs[k] - lo) / (hi - lo);
+            host_lagrange(c->gll_x, xi, v[k], nullptr);
+          } else {
+            for (int i = 0; i < n1; ++i) v[k][i] = (i == 0) ? 1.0 : 0.0;
+          }
+        }
+        for (int loc = 0; loc < nb; ++loc) {
+          int l0 = loc % n1, l1 = (loc / n1) % n1, l2 = loc / (n1 * n1);
+          double val = al * v[0][l0] * v[1][l1] * v[2][l2];
+          if (val != 0.0) out.push_back({elem_node(g, ci, loc, n1), val});
+        }
+        return;
+      }
+  throw ScError(SC_ERR_CONFIG, "point lies only in empty cells");
+}
+
 void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   Builder b;
   b.c = c;
@@ -294,50 +344,7 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   const int nb = c->nb, n1 = b.n1;
   // ---------------- source, DOF lists, irregular nodes
   std::vector<std::pair<int64_t, double>> src;  // (lattice, f_x value)
-  if (c->src_kind == 1) {
-    int64_t cand[3][2];
-    int nc[3] = {1, 1, 1};
-    for (int k = 0; k < 3; ++k) {
-      cand[k][0] = 0;
-      if (k >= g.dim) continue;
-      nc[k] = 0;
-      for (int64_t e = 0; e < g.N[k]; ++e) {
-        double lo = host_lattice(g.lo[k], g.hi[k], e, g.N[k]);
-        double hi = host_lattice(g.lo[k], g.hi[k], e + 1, g.N[k]);
-        if (lo <= c->src_x[k] && c->src_x[k] <= hi && nc[k] < 2) cand[k][nc[k]++] = e;
-      }
-      if (nc[k] == 0) throw ScError(SC_ERR_CONFIG, "source point outside the grid");
-    }
-    // lowest linear index first: iterate z, y, x ascending
-    bool found = false;
-    for (int a2 = 0; a2 < nc[2] && !found; ++a2)
-      for (int a1 = 0; a1 < nc[1] && !found; ++a1)
-        for (int a0 = 0; a0 < nc[0] && !found; ++a0) {
-          int64_t ci[3] = {cand[0][a0], cand[1][a1], cand[2][a2]};
-          int64_t cl = cell_lin(g, ci);
-          if (c->cell_class[cl] == 2) continue;
-          found = true;
-          double xs[3] = {c->src_x[0], g.dim > 1 ? c->src_x[1] : 0.0, g.dim > 2 ? c->src_x[2] : 0.0};
-          const double al = host_phys(c->voids, xs) ? 1.0 : c->alpha;
-          double v[3][SC_MAXP1];
-          for (int k = 0; k < 3; ++k) {
-            if (k < g.dim) {
-              double lo = host_lattice(g.lo[k], g.hi[k], ci[k], g.N[k]);
-              double hi = host_lattice(g.lo[k], g.hi[k], ci[k] + 1, g.N[k]);
-              double xi = -1.0 + 2.0 * (xs[k] - lo) / (hi - lo);
-              host_lagrange(c->gll_x, xi, v[k], nullptr);
-            } else {
-              for (int i = 0; i < n1; ++i) v[k][i] = (i == 0) ? 1.0 : 0.0;
-            }
-          }
-          for (int loc = 0; loc < nb; ++loc) {
-            int l0 = loc % n1, l1 = (loc / n1) % n1, l2 = loc / (n1 * n1);
-            double val = al * v[0][l0] * v[1][l1] * v[2][l2];
-            if (val != 0.0) src.push_back({elem_node(g, ci, loc, n1), val});
-          }
-        }
-    if (!found) throw ScError(SC_ERR_CONFIG, "source point lies only in empty cells");
-  }
+  if (c->src_kind == 1) point_weights(c, c->src_x, true, src);
   for (auto& sv : src)
     if (c->ntype[sv.first] == 1) c->ntype[sv.first] = 2;  // point-load d nodes -> irregular path
   c->dof_lat.clear();
@@ -677,6 +684,31 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
       dM[i] += m;
     }
   }
+  // CDM with HRZ-lumped cut cells (integrator 1): the c DOFs are explicit
+  // with the diagonal mass sum_e M~_ii, M~_ii = m_e / (sum_k M_kk) M_ii on cut cells
+  if (c->integrator == 1) {
+    std::vector<double> mc(nc, 0.0);
+    for (int e = 0; e < ne; ++e) {
+      const int kidx = b.celem_kidx[e];
+      double scale = 1.0;
+      if (kidx >= 0) {
+        const double* Me = &c->Mcut_host[(size_t)kidx * nb * nb];
+        double tot = 0.0, dia = 0.0;
+        for (size_t q = 0; q < (size_t)nb * nb; ++q) tot += Me[q];
+        for (int l = 0; l < nb; ++l) dia += Me[(size_t)l * nb + l];
+        scale = tot / dia;
+      }
+      for (int l = 0; l < nb; ++l) {
+        const int i = b.celem_cidx[(size_t)e * nb + l];
+        if (i < 0) continue;
+        mc[i] += kidx >= 0 ? scale * c->Mcut_host[(size_t)kidx * nb * nb + (size_t)l * nb + l] : c->Mref[l];
+      }
+    }
+    for (int i = 0; i < nc; ++i)
+      if (!(mc[i] > 0.0)) throw ScError(SC_ERR_NUMERIC, "non-positive HRZ mass at c DOF " + std::to_string(i));
+    SC_CUDA(cudaMalloc(&c->d_mc, sizeof(double) * std::max(1, nc)));
+    SC_CUDA(cudaMemcpy(c->d_mc, mc.data(), sizeof(double) * nc, cudaMemcpyHostToDevice));
+  }
   for (int i = 0; i < nc; ++i) {
     if (!(dS[i] > 0.0) || !(dM[i] > 0.0))
       throw ScError(SC_ERR_NUMERIC, "non-positive diagonal of S or M^cc at c DOF " + std::to_string(i));
@@ -698,8 +730,10 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   int fail_comp = -1, fail_row = -1, fail_which = 0;
   const double* Kref = c->Kref.data();
   const double* Mref = c->Mref.data();
+  // (no factor for the explicit HRZ integrator: the panels stay zero and the solve never runs)
+  const int n_fact = c->integrator == 1 ? 0 : (int)comps.size();
 #pragma omp parallel for schedule(dynamic, 1)
-  for (int k = 0; k < (int)comps.size(); ++k) {
+  for (int k = 0; k < n_fact; ++k) {
     for (int which = 0; which < 2; ++which) {  // 0: S, 1: M^cc
       std::vector<std::vector<double>> upd(nsn);  // update matrices (sparse by sn id; only this comp used)
       for (int s : comp_sn[k]) {

@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/sc.h"
@@ -78,6 +79,8 @@ struct sc_ctx {
   GridP g;
   int nb = 0;               // (p+1)^dim
   double alpha = 0, rho = 1, c = 1, dt = 0, fill_eps = 1e-10;
+  int integrator = 0;       // 0 Newmark IMEX; 1 CDM with HRZ-lumped cut cells (NEXT-1(c))
+  double* d_mc = nullptr;   // integrator 1: HRZ-lumped mass of the c DOFs (ND order)
   std::vector<DVoid> voids;
   int64_t n_cells = 0, n_lat = 0;
   // rules (host, own implementation)
@@ -190,6 +193,12 @@ struct sc_ctx {
   int32_t* d_own_dof = nullptr;
   void* nccl_comm = nullptr;          // ncclComm_t (world > 1 with an NCCL unique id)
   double* d_full = nullptr;           // n_dof reduction buffer of sc_read (NCCL)
+  // receivers (NEXT-3): u(x_r, t_{n+1}) = sum_i N_i(x_r) u_i recorded after every step
+  int n_rec = 0;
+  int64_t rec_cap = 0;
+  int32_t* d_rec_lat = nullptr;       // [n_rec][nb] lattice indices (0 for padding)
+  double* d_rec_w = nullptr;          // [n_rec][nb] basis values (0 for padding)
+  double* d_rec_trace = nullptr;      // [rec_cap][n_rec]
 };
 
 // component summary for the partition plan (element layers of the split axis)
@@ -242,10 +251,13 @@ void gather_owned(sc_ctx* c, const double* d_lat, double* d_dst);
 double estimate_lambda(sc_ctx* c, int iters);
 // factor (factor.cpp)
 void setup_factor(sc_ctx* c, const std::vector<double>& Mcut_host);
+void point_weights(const sc_ctx* c, const double* x, bool with_alpha,
+                   std::vector<std::pair<int64_t, double>>& out);
 // step (step.cu)
 void setup_step_structures(sc_ctx* c);
 void explicit_tiling(const GridP& g, int ext[3], int tg[3]);
 void build_graphs(sc_ctx* c);
+void destroy_graphs(sc_ctx* c);
 void run_startup(sc_ctx* c, const double* u0, const double* v0);
 void enqueue_step(sc_ctx* c, int parity, cudaStream_t st);
 void enqueue_far_prologue(sc_ctx* c);

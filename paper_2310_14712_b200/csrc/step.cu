@@ -225,12 +225,43 @@ __global__ void k_celem(int mode, const double* __restrict__ A, const double* __
 __global__ void k_crhs(double* __restrict__ b, const double* __restrict__ fxc, const int32_t* __restrict__ ptr,
                        const int32_t* __restrict__ idx, const double* __restrict__ Y, int nc,
                        const double* __restrict__ ft, long long n_t, const long long* step, int off,
-                       const double* __restrict__ dscale) {
+                       const double* __restrict__ dscale, double fsc = 1.0) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nc) return;
   double s = 0.0;
   for (int q = ptr[i]; q < ptr[i + 1]; ++q) s += Y[idx[q]];
-  b[i] = dscale[i] * (ft_at(ft, n_t, step, off) * fxc[i] - s);   // D r^c (scaled system)
+  const double r = fsc * ft_at(ft, n_t, step, off) * fxc[i] - s;
+  b[i] = dscale ? dscale[i] * r : r;   // D r^c (scaled system) or r^c
+}
+
+// CDM on the c DOFs with the HRZ-lumped mass (integrator 1): u^c_{n+1} = 2u^c_n - u^c_{n-1}
+// + dt^2 r^c / m^c, r^c = f_t(t_n) f_x^c - (K u_n)_c (P:577, P:580-583 with M~ of P:604-611)
+__global__ void k_cdm_c(const double* __restrict__ A, double* __restrict__ B, const double* __restrict__ r,
+                        const double* __restrict__ mc, const int32_t* __restrict__ clat, int nc, double dt2,
+                        int* flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nc) return;
+  const int32_t L = clat[i];
+  const double un = 2.0 * A[L] - B[L] + dt2 * r[i] / mc[i];
+  B[L] = un;
+  if (!isfinite(un)) atomicExch(flag, 1);
+}
+
+// start of integrator 1 at the c DOFs: u_{-1} = u_0 - dt v_0 + dt^2/2 a_0, a_0 = r^c / m^c
+__global__ void k_start_hrz(const double* __restrict__ A, double* __restrict__ B, const double* __restrict__ r,
+                            const double* __restrict__ mc, const double* __restrict__ vlat,
+                            const int32_t* __restrict__ clat, int nc, double dt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nc) return;
+  const int32_t L = clat[i];
+  B[L] = A[L] - (vlat ? dt * vlat[L] : 0.0) + 0.5 * dt * dt * r[i] / mc[i];
+}
+
+// M~^{-1} K x at the c DOFs (power iteration of integrator 1): r = -(K x)_c
+__global__ void k_hrz_apply(double* __restrict__ Y, const double* __restrict__ r, const double* __restrict__ mc,
+                            const int32_t* __restrict__ clat, int nc) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nc) Y[clat[i]] = -r[i] / mc[i];
 }
 
 // ------------------------------------------------------------------ corrector / misc
@@ -261,6 +292,19 @@ __global__ void k_start_c(double* __restrict__ ac, double* __restrict__ vc, cons
 }
 
 __global__ void k_advance(long long* step) { *step += 1; }
+
+// receivers: row *step of the trace = sum_k w[r][k] u[lat[r][k]] (warp per receiver)
+__global__ void k_record(const double* __restrict__ u, const int32_t* __restrict__ lat,
+                         const double* __restrict__ w, int n_rec, int nb, double* trace, long long cap,
+                         const long long* step) {
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const long long row = *step;
+  if (r >= n_rec || row >= cap) return;
+  double s = 0.0;
+  for (int k = lane; k < nb; k += 32) s += w[(size_t)r * nb + k] * u[lat[(size_t)r * nb + k]];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) trace[row * n_rec + r] = s;
+}
 
 __global__ void k_gather(const double* __restrict__ lat, const int64_t* __restrict__ idx, double* __restrict__ out,
                          long long n) {
@@ -411,7 +455,14 @@ static void launch_irregular(sc_ctx* c, const double* U, const double* Pv, doubl
 // the implicit solve S a^c_{n+1} = r^c, the corrector; then the device step counter.
 static void enqueue_c_part(sc_ctx* c, const double* A, double* B, cudaStream_t st) {
   const double dt = c->dt;
-  if (c->n_cl > 0) {
+  if (c->n_cl > 0 && c->integrator == 1) {
+    // CDM with HRZ-lumped cut cells: (K u_n)_c from the c-element products, explicit update
+    launch_celem(c, 1, A, A, st);
+    k_crhs<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, st>>>(c->d_b, c->d_fxc, c->d_rhs_ptr, c->d_rhs_idx, c->d_Y,
+                                                              (int)c->n_cl, c->d_ft, c->n_t, c->d_step, 0, nullptr);
+    k_cdm_c<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, st>>>(A, B, c->d_b, c->d_mc, c->d_c_lat, (int)c->n_cl,
+                                                               dt * dt, c->d_flag);
+  } else if (c->n_cl > 0) {
     launch_celem(c, 0, A, B, st);
     k_crhs<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, st>>>(c->d_b, c->d_fxc, c->d_rhs_ptr, c->d_rhs_idx, c->d_Y,
                                                               (int)c->n_cl, c->d_ft, c->n_t, c->d_step, 1, c->fS.d);
@@ -419,8 +470,19 @@ static void enqueue_c_part(sc_ctx* c, const double* A, double* B, cudaStream_t s
     k_corrector<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, st>>>(A, B, c->d_vc, c->d_ac, c->d_x, c->d_c_lat,
                                                                   (int)c->n_cl, dt, c->d_flag, c->fS.d);
   }
+  if (c->n_rec > 0)   // NEXT-3 observers: u at the receivers after this step
+    k_record<<<(unsigned)((c->n_rec * 32 + 127) / 128), 128, 0, st>>>(B, c->d_rec_lat, c->d_rec_w, c->n_rec, c->nb,
+                                                                        c->d_rec_trace, c->rec_cap, c->d_step);
   k_advance<<<1, 1, 0, st>>>(c->d_step);
   SC_CUDA(cudaGetLastError());
+}
+
+void destroy_graphs(sc_ctx* c) {
+  for (int i = 0; i < 2; ++i)
+    if (c->graph[i]) {
+      cudaGraphExecDestroy(c->graph[i]);
+      c->graph[i] = nullptr;
+    }
 }
 
 // One Newmark IMEX step: u_n in d_u[parity], writes u_{n+1} into d_u[parity^1].
@@ -475,7 +537,8 @@ void build_graphs(sc_ctx* c) {
   // SC_PIPELINE=1: fork the far-d update of step n+1 against the c part of step n (one rank
   // with c DOFs); default off: measured no gain and it costs a second
   // (near-node) explicit launch
-  c->pipelined = c->n_c > 0 && c->world == 1 && getenv("SC_PIPELINE") && atoi(getenv("SC_PIPELINE"));
+  c->pipelined = c->n_c > 0 && c->world == 1 && c->integrator == 0 && getenv("SC_PIPELINE") &&
+                 atoi(getenv("SC_PIPELINE"));
   if (!c->s_hi) {
     int lo = 0, hi = 0;
     SC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -495,7 +558,7 @@ void build_graphs(sc_ctx* c) {
   }
   // kernels per step: explicit (+ near when pipelined) + irregular + advance + c part (+ pack)
   c->kernels_per_step = 1 + (c->pipelined && c->n_near > 0 ? 1 : 0) + (c->n_irr > 0) + 1 + (c->world > 1);
-  if (c->n_c > 0) c->kernels_per_step += 3 + (c->n_items > 0 ? 1 : 0);
+  if (c->n_c > 0) c->kernels_per_step += c->integrator == 1 ? 3 : 3 + (c->n_items > 0 ? 1 : 0);
 }
 
 // near-d tile list: tiles of the explicit kernel that own at least one type-4 node (a tile
@@ -652,7 +715,14 @@ void run_startup(sc_ctx* c, const double* u0, const double* v0) {
   const double a2 = vlat ? -dt : 0.0;
   launch_explicit(c, A, Pv, B, 1.0, a2, 0.5 * dt * dt, 5, c->stream);
   launch_irregular(c, A, Pv, B, 1.0, a2, 0.5 * dt * dt, c->stream);
-  if (c->n_cl > 0) {
+  if (c->n_cl > 0 && c->integrator == 1) {
+    launch_celem(c, 1, A, A, c->stream);
+    k_crhs<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, c->stream>>>(c->d_b, c->d_fxc, c->d_rhs_ptr, c->d_rhs_idx,
+                                                                      c->d_Y, (int)c->n_cl, c->d_ft, c->n_t,
+                                                                      c->d_step, 0, nullptr);
+    k_start_hrz<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, c->stream>>>(A, B, c->d_b, c->d_mc, vlat, c->d_c_lat,
+                                                                           (int)c->n_cl, dt);
+  } else if (c->n_cl > 0) {
     launch_celem(c, 1, A, A, c->stream);
     k_crhs<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, c->stream>>>(c->d_b, c->d_fxc, c->d_rhs_ptr, c->d_rhs_idx,
                                                                      c->d_Y, (int)c->n_cl, c->d_ft, c->n_t,
@@ -686,7 +756,7 @@ void profile_launch(sc_ctx* c, int which) {
 // that of the d subsystem).  Rayleigh-type estimate (x.y)/(x.x); deterministic
 // two-pass reductions.  Clobbers the state (both lattice buffers).
 namespace {
-__global__ void k_power_init(double* x, const uint8_t* __restrict__ nt, long long n) {
+__global__ void k_power_init(double* x, const uint8_t* __restrict__ nt, long long n, bool all) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint8_t t = nt[i];
@@ -695,7 +765,8 @@ __global__ void k_power_init(double* x, const uint8_t* __restrict__ nt, long lon
   z ^= z >> 29;
   z *= 0xBF58476D1CE4E5B9ull;
   z ^= z >> 32;
-  x[i] = (t == 1 || t == 2 || t == 4) ? 0.5 + (double)(z >> 11) * (1.0 / 9007199254740992.0) : 0.0;
+  x[i] = (t == 1 || t == 2 || t == 4 || (t == 3 && all)) ? 0.5 + (double)(z >> 11) * (1.0 / 9007199254740992.0)
+                                                        : 0.0;
 }
 // per-block partial sums of x.y, x.x, y.y
 __global__ void k_dots(const double* __restrict__ x, const double* __restrict__ y, long long n, double* part) {
@@ -752,11 +823,19 @@ double estimate_lambda(sc_ctx* c, int iters) {
   double* part = scratch;
   double* res = scratch + 3 * nblk;
   const unsigned gb = (unsigned)((n + 255) / 256);
-  k_power_init<<<gb, 256, 0, c->stream>>>(X, c->d_ntype, n);
+  k_power_init<<<gb, 256, 0, c->stream>>>(X, c->d_ntype, n, c->integrator == 1);
   for (int k = 0; k < iters; ++k) {
     SC_CUDA(cudaMemsetAsync(Y, 0, sizeof(double) * n, c->stream));
     launch_explicit(c, X, X, Y, 0.0, 0.0, -1.0, 5, c->stream);
     launch_irregular(c, X, X, Y, 0.0, 0.0, -1.0, c->stream, 0.0);
+    if (c->integrator == 1 && c->n_cl > 0) {   // all DOFs explicit: the c rows with M~
+      launch_celem(c, 1, X, X, c->stream);
+      k_crhs<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, c->stream>>>(
+          c->d_b, c->d_fxc, c->d_rhs_ptr, c->d_rhs_idx, c->d_Y, (int)c->n_cl, c->d_ft, c->n_t, c->d_step, 0, nullptr,
+          0.0);
+      k_hrz_apply<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, c->stream>>>(Y, c->d_b, c->d_mc, c->d_c_lat,
+                                                                              (int)c->n_cl);
+    }
     k_dots<<<nblk, 256, 0, c->stream>>>(X, Y, n, part);
     k_dots_final<<<1, 1, 0, c->stream>>>(part, nblk, res);
     k_scale_into<<<gb, 256, 0, c->stream>>>(X, Y, res, n);
