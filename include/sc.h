@@ -78,9 +78,14 @@ typedef struct {
   double fill_eps;
   double rho;
   double c;
-  int32_t integrator; /* 0: Newmark IMEX (the method); 1: CDM on the HRZ-lumped SCM, the
-                         paper's explicit comparison scheme (every DOF explicit, cut
-                         cells HRZ-lumped; needs dt below its much smaller critical step) */
+  int32_t integrator; /* the paper's schemes on the same kernels (Table tab:times3D):
+                         0 Newmark IMEX (the method);
+                         1 CDM on the HRZ-lumped SCM (every DOF explicit, cut cells
+                           HRZ-lumped; dt below its much smaller critical step);
+                         2 trapezoidal Newmark on all DOFs (every DOF implicit, S
+                           factored over the whole mesh: small problems);
+                         3 CDM on the consistent SCM (M^cc solved each step
+                           with its factor; dt below the consistent critical step) */
 } sc_geometry;
 
 /* Separable point source f(x,t) = f_t(t) delta(x - x_s) (reading C11):
@@ -179,7 +184,8 @@ sc_status sc_exchange_local(sc_ctx* const* ctxs, int32_t world);
 
 /* Critical time step of the explicit subsystem:
  * `iters` power iterations for lambda_max of M_dd^{-1} K_dd on the device (c DOFs held at
- * zero; with integrator 1 of M~^{-1} K over all DOFs), dt_crit = 2 / sqrt(lambda_max).  The estimate approaches lambda_max from below.
+ * zero; integrators 1 and 3: of M^{-1} K over all DOFs with their mass), dt_crit =
+ * 2 / sqrt(lambda_max); not for integrator 2 (unconditionally stable).  The estimate approaches lambda_max from below.
  * Clobbers the state: call sc_set_state before stepping again.  One rank only. */
 sc_status sc_estimate_dt(sc_ctx* ctx, int32_t iters, double* lambda_max, double* dt_crit);
 

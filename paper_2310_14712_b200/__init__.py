@@ -146,7 +146,8 @@ class Solver:
                 arr[i].b = v["b"]
         geo = sc_geometry(len(vs), arr, geometry.get("tree_depth", 2), geometry.get("lattice_s", 4),
                           geometry.get("fill_eps", 1e-10), geometry.get("rho", 1.0), geometry.get("c", 1.0),
-                          {"imex": 0, "cdm_hrz": 1}[geometry.get("integrator", "imex")])
+                          {"imex": 0, "cdm_hrz": 1, "trapezoidal": 2, "cdm_consistent": 3}[
+                              geometry.get("integrator", "imex")])
         src = None
         self._ft = None
         if source is not None:

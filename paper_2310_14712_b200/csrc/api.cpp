@@ -151,7 +151,7 @@ extern "C" sc_status sc_setup(const sc_grid* grid, int32_t p, double alpha, cons
     c->c = geom->c;
     c->dt = dt;
     c->fill_eps = geom->fill_eps;
-    if (geom->integrator != 0 && geom->integrator != 1) throw ScError(SC_ERR_CONFIG, "integrator must be 0 or 1");
+    if (geom->integrator < 0 || geom->integrator > 3) throw ScError(SC_ERR_CONFIG, "integrator must be 0..3");
     c->integrator = geom->integrator;
     for (int i = 0; i < geom->n_voids; ++i) {
       DVoid v;
@@ -392,8 +392,8 @@ extern "C" sc_status sc_exchange_local(sc_ctx* const* ctxs, int32_t world) {
 
 extern "C" sc_status sc_estimate_dt(sc_ctx* c, int32_t iters, double* lambda_max, double* dt_crit) {
   if (!c) return SC_ERR_STATE;
-  if (iters < 1 || c->world > 1) {
-    c->err = "sc_estimate_dt: iters >= 1, one rank";
+  if (iters < 1 || c->world > 1 || c->integrator == 2) {
+    c->err = "sc_estimate_dt: iters >= 1, one rank, an explicit or IMEX integrator";
     return SC_ERR_CONFIG;
   }
   try {

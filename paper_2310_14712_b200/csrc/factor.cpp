@@ -347,6 +347,10 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   if (c->src_kind == 1) point_weights(c, c->src_x, true, src);
   for (auto& sv : src)
     if (c->ntype[sv.first] == 1) c->ntype[sv.first] = 2;  // point-load d nodes -> irregular path
+  // integrator 2 (trapezoidal Newmark on all DOFs): every DOF is treated implicitly
+  if (c->integrator == 2)
+    for (int64_t L = 0; L < c->n_lat; ++L)
+      if (c->ntype[L] == 1 || c->ntype[L] == 2 || c->ntype[L] == 4) c->ntype[L] = 3;
   c->dof_lat.clear();
   c->n_d = c->n_c = c->n_irr = 0;
   for (int64_t i = 0; i < c->n_lat; ++i) {

@@ -247,6 +247,29 @@ __global__ void k_cdm_c(const double* __restrict__ A, double* __restrict__ B, co
   if (!isfinite(un)) atomicExch(flag, 1);
 }
 
+// CDM on the consistent SCM at the c DOFs (integrator 3): u^c_{n+1} = 2u^c_n - u^c_{n-1} +
+// dt^2 a^c_n with M^cc a^c_n = r^c (the solve returns x with a = D x, Jacobi scaling)
+__global__ void k_cdm_cons(const double* __restrict__ A, double* __restrict__ B, const double* __restrict__ x,
+                           const double* __restrict__ dscale, const int32_t* __restrict__ clat, int nc, double dt2,
+                           int* flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nc) return;
+  const int32_t L = clat[i];
+  const double un = 2.0 * A[L] - B[L] + dt2 * (dscale[i] * x[i]);
+  B[L] = un;
+  if (!isfinite(un)) atomicExch(flag, 1);
+}
+
+// start of integrator 3 at the c DOFs: u_{-1} = u_0 - dt v_0 + dt^2/2 a_0 (a_0 = D x, M solve)
+__global__ void k_start_cons(const double* __restrict__ A, double* __restrict__ B, const double* __restrict__ x,
+                             const double* __restrict__ dscale, const double* __restrict__ vlat,
+                             const int32_t* __restrict__ clat, int nc, double dt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nc) return;
+  const int32_t L = clat[i];
+  B[L] = A[L] - (vlat ? dt * vlat[L] : 0.0) + 0.5 * dt * dt * (dscale[i] * x[i]);
+}
+
 // start of integrator 1 at the c DOFs: u_{-1} = u_0 - dt v_0 + dt^2/2 a_0, a_0 = r^c / m^c
 __global__ void k_start_hrz(const double* __restrict__ A, double* __restrict__ B, const double* __restrict__ r,
                             const double* __restrict__ mc, const double* __restrict__ vlat,
@@ -255,6 +278,14 @@ __global__ void k_start_hrz(const double* __restrict__ A, double* __restrict__ B
   if (i >= nc) return;
   const int32_t L = clat[i];
   B[L] = A[L] - (vlat ? dt * vlat[L] : 0.0) + 0.5 * dt * dt * r[i] / mc[i];
+}
+
+// M^{-1} K x at the c DOFs with the consistent M^cc (power iteration of integrator 3):
+// the M solve of r = -(K x)_c returned a = D x
+__global__ void k_cons_apply(double* __restrict__ Y, const double* __restrict__ x, const double* __restrict__ dscale,
+                             const int32_t* __restrict__ clat, int nc) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nc) Y[clat[i]] = -dscale[i] * x[i];
 }
 
 // M~^{-1} K x at the c DOFs (power iteration of integrator 1): r = -(K x)_c
@@ -401,6 +432,7 @@ void launch_explicit(sc_ctx* c, const double* U, const double* Pv, double* out, 
   e.a1 = a1;
   e.a2 = a2;
   e.coefR = a3 * c->c * c->c;
+  if (c->n_d == c->n_irr) return;   // no tensor-d DOFs (e.g. integrator 2: all implicit)
   e.want = want == 1 ? WANT_FAR : (want == 4 ? WANT_NEAR : WANT_FAR | WANT_NEAR);
   e.clean = want == 5 ? c->d_clean : nullptr;
   e.tiles = nullptr;
@@ -462,6 +494,14 @@ static void enqueue_c_part(sc_ctx* c, const double* A, double* B, cudaStream_t s
                                                               (int)c->n_cl, c->d_ft, c->n_t, c->d_step, 0, nullptr);
     k_cdm_c<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, st>>>(A, B, c->d_b, c->d_mc, c->d_c_lat, (int)c->n_cl,
                                                                dt * dt, c->d_flag);
+  } else if (c->n_cl > 0 && c->integrator == 3) {
+    // CDM on the consistent SCM: M^cc a^c_n = f_t(t_n) f_x^c - (K u_n)_c with the M factor
+    launch_celem(c, 1, A, A, st);
+    k_crhs<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, st>>>(c->d_b, c->d_fxc, c->d_rhs_ptr, c->d_rhs_idx, c->d_Y,
+                                                              (int)c->n_cl, c->d_ft, c->n_t, c->d_step, 0, c->fM.d);
+    launch_solve(c, c->fM, st);
+    k_cdm_cons<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, st>>>(A, B, c->d_x, c->fM.d, c->d_c_lat, (int)c->n_cl,
+                                                                  dt * dt, c->d_flag);
   } else if (c->n_cl > 0) {
     launch_celem(c, 0, A, B, st);
     k_crhs<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, st>>>(c->d_b, c->d_fxc, c->d_rhs_ptr, c->d_rhs_idx, c->d_Y,
@@ -537,7 +577,7 @@ void build_graphs(sc_ctx* c) {
   // SC_PIPELINE=1: fork the far-d update of step n+1 against the c part of step n (one rank
   // with c DOFs); default off: measured no gain and it costs a second
   // (near-node) explicit launch
-  c->pipelined = c->n_c > 0 && c->world == 1 && c->integrator == 0 && getenv("SC_PIPELINE") &&
+  c->pipelined = c->n_c > 0 && c->n_d > c->n_irr && c->world == 1 && c->integrator == 0 && getenv("SC_PIPELINE") &&
                  atoi(getenv("SC_PIPELINE"));
   if (!c->s_hi) {
     int lo = 0, hi = 0;
@@ -728,6 +768,9 @@ void run_startup(sc_ctx* c, const double* u0, const double* v0) {
                                                                      c->d_Y, (int)c->n_cl, c->d_ft, c->n_t,
                                                                      c->d_step, 0, c->fM.d);
     launch_solve(c, c->fM, c->stream);
+    if (c->integrator == 3)
+      k_start_cons<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, c->stream>>>(A, B, c->d_x, c->fM.d, vlat, c->d_c_lat,
+                                                                             (int)c->n_cl, dt);
     k_start_c<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, c->stream>>>(c->d_ac, c->d_vc, c->d_x, vlat, c->d_c_lat,
                                                                          (int)c->n_cl, c->fM.d);
   }
@@ -823,7 +866,7 @@ double estimate_lambda(sc_ctx* c, int iters) {
   double* part = scratch;
   double* res = scratch + 3 * nblk;
   const unsigned gb = (unsigned)((n + 255) / 256);
-  k_power_init<<<gb, 256, 0, c->stream>>>(X, c->d_ntype, n, c->integrator == 1);
+  k_power_init<<<gb, 256, 0, c->stream>>>(X, c->d_ntype, n, c->integrator == 1 || c->integrator == 3);
   for (int k = 0; k < iters; ++k) {
     SC_CUDA(cudaMemsetAsync(Y, 0, sizeof(double) * n, c->stream));
     launch_explicit(c, X, X, Y, 0.0, 0.0, -1.0, 5, c->stream);
@@ -835,6 +878,14 @@ double estimate_lambda(sc_ctx* c, int iters) {
           0.0);
       k_hrz_apply<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, c->stream>>>(Y, c->d_b, c->d_mc, c->d_c_lat,
                                                                               (int)c->n_cl);
+    } else if (c->integrator == 3 && c->n_cl > 0) {   // c rows with the consistent M^cc (its factor)
+      launch_celem(c, 1, X, X, c->stream);
+      k_crhs<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, c->stream>>>(
+          c->d_b, c->d_fxc, c->d_rhs_ptr, c->d_rhs_idx, c->d_Y, (int)c->n_cl, c->d_ft, c->n_t, c->d_step, 0, c->fM.d,
+          0.0);
+      launch_solve(c, c->fM, c->stream);
+      k_cons_apply<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, c->stream>>>(Y, c->d_x, c->fM.d, c->d_c_lat,
+                                                                               (int)c->n_cl);
     }
     k_dots<<<nblk, 256, 0, c->stream>>>(X, Y, n, part);
     k_dots_final<<<1, 1, 0, c->stream>>>(part, nblk, res);

@@ -7,6 +7,7 @@ timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_ou
 timeout 900 python bench.py > gpurun_out/bench_c5.log 2>&1; echo "rc=$?" >> gpurun_out/bench_c5.log
 timeout 600 python bench.py --config 4 --no-cpu > gpurun_out/bench_c4.log 2>&1; echo "rc=$?" >> gpurun_out/bench_c4.log
 timeout 600 python bench.py --config 2 --no-cpu > gpurun_out/bench_c2.log 2>&1; echo "rc=$?" >> gpurun_out/bench_c2.log
+timeout 600 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/bench_ref.log 2>&1; echo "rc=$?" >> gpurun_out/bench_ref.log
 CMD="python bench.py --steps 3 --warmup 3 --no-cpu"
 timeout 600 $CMD > gpurun_out/plain.log 2>&1 && \
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c5.csv $CMD > gpurun_out/ncu_launch.log 2>&1 ; echo "rc=$?" >> gpurun_out/ncu_launch.log

@@ -63,3 +63,39 @@ def test_hrz_step_is_restricted_by_cut_cells(pkg):
     _, dt_hrz = s.estimate_dt(3000)
     s.close()
     assert dt_hrz < 0.5 * cfg["dt"]
+
+
+@pytest.mark.parametrize("dim,cells,p,void", CASES[:2])
+def test_trapezoidal_and_consistent_cdm_match_oracle(pkg, dim, cells, p, void):
+    """NEXT-1(a, b): CDM on the consistent SCM (integrator 3) and trapezoidal Newmark on all DOFs
+    (integrator 2) on the same kernels, against oracle.integrators.cdm_consistent / trapezoidal
+    (pinned in tests/test_oracle_integrators.py)."""
+    from oracle.integrators import cdm_consistent, from_system, trapezoidal
+    steps = 80
+    cfg = sc_inputs.small_config(dim, cells, p, voids=[void], depth=2, steps=steps,
+                                 source={"x": [0.25, 0.3, 0.3], "f0": 5.0})
+    sysm = build_system(cfg, "sparse")
+    pr = from_system(sysm)
+    # consistent CDM at half its critical step (device estimate vs the dense eigenvalue)
+    lam = lambda_max(sysm.K.toarray(), sysm.M.toarray())
+    c3 = dict(cfg, dt=0.5 * 2.0 / np.sqrt(lam), integrator="cdm_consistent")
+    s = pkg.from_config(c3)
+    s.step(steps)
+    u = s.read()
+    lam_gpu, _ = s.estimate_dt(6000)
+    s.close()
+    ref = cdm_consistent(pr, c3["dt"], steps, sc_inputs.source_signal(c3, steps + 1), np.zeros(sysm.n_dof))
+    assert np.linalg.norm(u - ref) / np.linalg.norm(ref) < 1e-10
+    assert abs(lam_gpu - lam) / lam < 1e-3
+    # trapezoidal Newmark on all DOFs at 3x the IMEX step (unconditionally stable)
+    from oracle.spectra import dt_crit_uncut
+    c2 = dict(cfg, dt=3.0 * 0.9 * dt_crit_uncut(dim, p, 1.0 / max(cells)), integrator="trapezoidal")
+    s = pkg.from_config(c2)
+    assert s.info["n_d"] == 0 and s.info["n_c"] == sysm.n_dof
+    s.step(steps)
+    u = s.read()
+    s.close()
+    M = sysm.M
+    prt = Problem(M, sysm.K, sysm.f_x, np.array([], dtype=int), np.arange(sysm.n_dof))
+    ref = trapezoidal(prt, c2["dt"], steps, sc_inputs.source_signal(c2, steps + 1), np.zeros(sysm.n_dof))
+    assert np.linalg.norm(u - ref) / np.linalg.norm(ref) < 1e-10

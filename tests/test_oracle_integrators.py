@@ -238,3 +238,37 @@ def test_config2_crosscheck_p15():
     src = s.cl.dof_of_lattice[64 + 257 * 64]
     assert abs(np.linalg.norm(u) - 2.973550776199) < 1e-9
     assert abs(u[src] - 5.586249111673e-2) < 1e-11
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_cdm_consistent_pins(seed):
+    """CDM on the consistent SCM (oracle.integrators.cdm_consistent, NEXT-1(a)): with I_c empty
+    it is the diagonal CDM bit for bit; with a non-diagonal M^cc the modified energy
+    1/2 v_{n+1/2}'M v_{n+1/2} + 1/2 u_{n+1}'K u_n is conserved (unforced, dt below critical)."""
+    from oracle.integrators import cdm_consistent
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(4, 12))
+    M, K = _random_system(rng, n, True)
+    f = rng.standard_normal(n)
+    f_t = rng.standard_normal(80)
+    u0, v0 = rng.standard_normal(n), rng.standard_normal(n)
+    dt = 0.5 * dt_crit(K.toarray(), M.toarray())
+    pr = Problem(M, K, f, np.arange(n), np.array([], dtype=int))
+    assert np.array_equal(cdm_consistent(pr, dt, 60, f_t, u0, v0), cdm(pr, dt, 60, f_t, u0, v0))
+    # block mass: diagonal d block, SPD c block
+    nd = n // 2
+    Mc = rng.standard_normal((n - nd, n - nd)) * 0.2
+    Mfull = np.zeros((n, n))
+    Mfull[:nd, :nd] = np.diag(rng.uniform(0.5, 2.0, nd))
+    Mfull[nd:, nd:] = np.eye(n - nd) + Mc @ Mc.T
+    prc = Problem(sp.csr_matrix(Mfull), K, np.zeros(n), np.arange(nd), np.arange(nd, n))
+    dtc = 0.6 * dt_crit(K.toarray(), Mfull)
+    us = [u0.copy()]
+    cdm_consistent(prc, dtc, 5000, None, u0, v0, observer=lambda k, u: us.append(u.copy()))
+    Kd = K.toarray()
+    Em = []
+    for i in range(len(us) - 1):
+        vh = (us[i + 1] - us[i]) / dtc
+        Em.append(0.5 * vh @ Mfull @ vh + 0.5 * us[i + 1] @ Kd @ us[i])
+    Em = np.array(Em)
+    assert np.max(np.abs(Em - Em[0])) / Em[0] < 1e-11
