@@ -163,8 +163,34 @@ struct Item {
   int64_t aoff;
 };
 
-__device__ __forceinline__ Item load_item(const SolveDev& a, int it) {
+// the item in queue slot h (waits until the slot is filled); -1 past the end
+__device__ __forceinline__ int slot_item(const SolveDev& a, int h) {
+  if (h >= a.n_items) return -1;
+  if (h < a.n_init) return a.init[h];
+  const int* slot = a.ready + (h - a.n_init);
+  int v;
+  unsigned ns = 32;
+  while ((v = ld_acquire(slot)) == 0) {
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+  }
+  return v - 1;
+}
+
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// copy item it's 80-byte descriptor to shared memory (one thread)
+__device__ __forceinline__ void fetch_desc(const SolveDev& a, int it, int4* dst) {
   const int4* d = a.items + 5 * (size_t)it;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) dst[k] = d[k];
+}
+
+__device__ __forceinline__ Item load_item(const int4* d) {
   const int4 d0 = d[0], d1 = d[1], d2 = d[2], d3 = d[3], d4 = d[4];
   Item m;
   m.type = d0.x;
@@ -208,45 +234,51 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
   __shared__ double vs[VS];
   __shared__ double red[NT];
   __shared__ __align__(8) uint64_t bar;
-  __shared__ int s_item, s_last;
+  __shared__ int s_item, s_next, s_issued, s_last;
+  __shared__ int4 s_desc[5], s_desc2[5];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) mbar_init(&bar);
+  if (tid == 0) {
+    mbar_init(&bar);
+    s_next = -2;   // -2: nothing claimed ahead
+  }
   unsigned phase = 0;
   while (true) {
     __syncthreads();   // previous item fully consumed (stage buffer and vs free)
+    // the item: either claimed during the previous item (queue backlog) — its descriptor
+    // staged in s_desc and its panel copy already issued — or claimed now
     unsigned long long tclaim = 0;
     if (tid == 0) {
       if (a.trace) tclaim = gtimer();
-      const int h = atomicAdd(a.head, 1);
-      int itm = -1;
-      if (h < a.n_items) {
-        if (h < a.n_init) {
-          itm = a.init[h];
-        } else {
-          const int* slot = a.ready + (h - a.n_init);
-          int v;
-          unsigned ns = 32;
-          while ((v = ld_acquire(slot)) == 0) {
-            __nanosleep(ns);
-            if (ns < 256) ns <<= 1;
-          }
-          itm = v - 1;
-        }
+      if (s_next != -2) {
+        s_item = s_next;
+        s_issued = 1;
+        s_next = -2;
+      } else {
+        s_item = slot_item(a, atomicAdd(a.head, 1));
+        s_issued = 0;
+        if (s_item >= 0) fetch_desc(a, s_item, s_desc);
       }
-      s_item = itm;
     }
     __syncthreads();
     const int it = s_item;
     if (it < 0) return;
-    const Item m = load_item(a, it);
+    const Item m = load_item(s_desc);
     const bool fwd = (m.type == IT_F);
     if (a.trace && tid == 0) {
       a.trace[5 * (size_t)it] = tclaim;
       a.trace[5 * (size_t)it + 1] = gtimer();
     }
-    // ---- stream the panel tile (TMA) and gather the input vector meanwhile (every producer
-    // of it completed before this item was pushed; L1 bypass)
-    if (warp == 0) stage_item(a, m, stg, &bar, lane);
+    // ---- stream the panel tile (TMA) unless already in flight; gather the input vector
+    // meanwhile (every producer of it completed before this item was pushed; L1 bypass)
+    if (warp == 0 && !s_issued) stage_item(a, m, stg, &bar, lane);
+    // ---- early claim of the next item when the queue backlog exceeds one item per CTA (the
+    // throughput-bound regime; a latency-bound solve never parks a ready item behind a busy
+    // CTA): its panel copy is issued as soon as this item's contraction releases the buffer
+    if (tid == NT - 32 && a.n_init + ld_relaxed(a.tail) > ld_relaxed(a.head) + (int)gridDim.x) {
+      const int nx = slot_item(a, atomicAdd(a.head, 1));
+      if (nx >= 0) fetch_desc(a, nx, s_desc2);
+      s_next = nx;
+    }
     const int go = m.goff;
     if (fwd) {
       // v_j = b_j - sum of the children's update entries at column position j
@@ -350,6 +382,13 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
           else P[m.t * 32 + cc] = v;
         }
       }
+    }
+    // the staging buffer is free once every thread has contracted: start the next item's copy
+    __syncthreads();
+    if (s_next >= 0) {
+      if (tid < 20) reinterpret_cast<int*>(s_desc)[tid] = reinterpret_cast<const int*>(s_desc2)[tid];
+      __syncwarp();
+      if (warp == 0) stage_item(a, load_item(s_desc2), stg, &bar, lane);
     }
     if (m.ntb > 1) {
       // partials of this tile written; the last tile of the group sums them in tile order
