@@ -57,7 +57,7 @@ static void free_ctx(sc_ctx* c) {
                   c->fM.A, c->fS.d, c->fM.d, c->d_tmp, c->d_nitem, c->d_chptr, c->d_chidx, c->d_parent, c->d_solve_cnt,
                   c->d_part, c->d_trace, c->d_near_tiles, c->d_qmeta, c->d_far_tiles, c->d_xs_idx, c->d_xr_idx,
                   c->d_xs_buf, c->d_xr_buf, c->d_own_lat, c->d_own_dof, c->d_full, c->d_clean, c->d_rec_lat, c->d_rec_w,
-                  c->d_rec_trace, c->d_mc};
+                  c->d_rec_trace, c->d_mc, c->d_g2};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);

@@ -842,6 +842,17 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
     gptr[t + 1] = gptr[t] + (int32_t)gl[t].size();
     gidx.insert(gidx.end(), gl[t].begin(), gl[t].end());
   }
+  // the same lists with the (usual) <= 2 entries inline: (i0, i1), -1 = none; longer lists
+  // are flagged (-2 - first CSR position) and read through gptr/gidx
+  std::vector<int32_t> g2(2 * (size_t)goff[nsn], -1);
+  for (int32_t t = 0; t < goff[nsn]; ++t) {
+    if (gl[t].size() > 2) {
+      g2[2 * (size_t)t] = -2 - gptr[t];
+    } else {
+      if (gl[t].size() > 0) g2[2 * (size_t)t] = gl[t][0];
+      if (gl[t].size() > 1) g2[2 * (size_t)t + 1] = gl[t][1];
+    }
+  }
   // persistent-solve work list (solve.cu).  Items of a phase cover the supernode's panel in
   // tiles that fill one staging buffer of `stage` doubles (SOLVE_STAGE = 32 KB: 5 CTAs per
   // SM; measured 8 K / 16 K doubles slower on configs 4 and 5 — fewer resident CTAs):
@@ -976,6 +987,7 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   up32(&c->d_R, Rall);
   up32(&c->d_gptr, gptr);
   up32(&c->d_gidx, gidx);
+  up32(&c->d_g2, g2);
   up32(&c->d_items, items);
   up32(&c->d_nitem, nblk);
   up32(&c->d_qmeta, qmeta);
@@ -1035,6 +1047,7 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   sd.goff = c->d_sn_goff;
   sd.gptr = c->d_gptr;
   sd.gidx = c->d_gidx;
+  sd.g2 = reinterpret_cast<const int2*>(c->d_g2);
   sd.uoff = c->d_sn_uoff;
   sd.roff = c->d_sn_roff;
   sd.R = c->d_R;

@@ -42,6 +42,7 @@ struct SolveDev {
   const int4* items;           // 5 x int4 per item (factor.cpp)
   int n_items, n_sn;
   const int32_t *w, *r, *c0, *goff, *gptr, *gidx, *uoff, *roff, *R;
+  const int2* g2;              // front gather lists inline (<= 2 entries; factor.cpp)
   const int64_t* aoff;         // per supernode offset of its stacked [D_s; G_s] panel
   const int32_t *nblk;         // [2][n_sn] 32-blocks per phase (0 forward, 1 backward)
   const int32_t *chptr, *chidx, *parent;
@@ -137,7 +138,7 @@ struct sc_ctx {
   int64_t* d_sn_aoff = nullptr;
   int32_t *d_sn_roff = nullptr, *d_sn_uoff = nullptr, *d_sn_goff = nullptr;
   int32_t* d_R = nullptr;             // row structures (ND c indices)
-  int32_t *d_gptr = nullptr, *d_gidx = nullptr;
+  int32_t *d_gptr = nullptr, *d_gidx = nullptr, *d_g2 = nullptr;
   int32_t* d_items = nullptr;         // int4 work items
   int32_t *d_nitem = nullptr, *d_chptr = nullptr, *d_chidx = nullptr, *d_parent = nullptr;
   int32_t* d_qmeta = nullptr;         // ready-queue metadata (solve.cu)

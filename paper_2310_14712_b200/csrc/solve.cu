@@ -190,6 +190,20 @@ __device__ __forceinline__ void fetch_desc(const SolveDev& a, int it, int4* dst)
   for (int k = 0; k < 5; ++k) dst[k] = d[k];
 }
 
+// sum of the children's update entries at front position t (inline list, else CSR)
+__device__ __forceinline__ double child_sum(const SolveDev& a, int t) {
+  const int2 g = a.g2[t];
+  if (g.x >= 0) {
+    double v = __ldcg(a.U + g.x);
+    if (g.y >= 0) v += __ldcg(a.U + g.y);
+    return v;
+  }
+  double v = 0.0;
+  if (g.x <= -2)
+    for (int q = -2 - g.x; q < a.gptr[t + 1]; ++q) v += __ldcg(a.U + a.gidx[q]);
+  return v;
+}
+
 __device__ __forceinline__ Item load_item(const int4* d) {
   const int4 d0 = d[0], d1 = d[1], d2 = d[2], d3 = d[3], d4 = d[4];
   Item m;
@@ -284,9 +298,7 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
       // v_j = b_j - sum of the children's update entries at column position j
       for (int j = tid; j < m.nc; j += NT) {
         const int pj = m.c0 + j;
-        double v = a.b[m.dof0 + pj];
-        for (int q = a.gptr[go + pj]; q < a.gptr[go + pj + 1]; ++q) v -= __ldcg(a.U + a.gidx[q]);
-        vs[j] = v;
+        vs[j] = a.b[m.dof0 + pj] - child_sum(a, go + pj);
       }
     } else {
       const int rr = min(m.nr, m.r - m.r0);   // real (unpadded) rows of this tile
@@ -302,8 +314,7 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
       crv[k] = 0.0;
       const int i = m.r0 + tid + k * NT;
       if (fwd && tid + k * NT < m.nr && i >= m.wp && i < m.wp + m.r) {
-        const int kk = m.w + (i - m.wp);
-        for (int q = a.gptr[go + kk]; q < a.gptr[go + kk + 1]; ++q) crv[k] += __ldcg(a.U + a.gidx[q]);
+        crv[k] = child_sum(a, go + m.w + (i - m.wp));
       }
     }
     if (a.trace && tid == 0) a.trace[5 * (size_t)it + 2] = gtimer();
@@ -323,7 +334,7 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
           for (int t = 0; t < NCR; ++t)
             if (t == kq) v += crv[t];
         } else {
-          for (int q = a.gptr[go + m.w + k]; q < a.gptr[go + m.w + k + 1]; ++q) v += __ldcg(a.U + a.gidx[q]);
+          v += child_sum(a, go + m.w + k);
         }
         a.U[m.uoff + k] = v;
       }
