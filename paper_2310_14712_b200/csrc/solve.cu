@@ -402,14 +402,19 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
       if (warp == 0) stage_item(a, load_item(s_desc2), stg, &bar, lane);
     }
     if (m.ntb > 1) {
-      // partials of this tile written; the last tile of the group sums them in tile order
-      __threadfence();
+      // partials of this tile written; the last tile of the group sums them in tile order.
+      // One thread fences after the barrier (cumulative release of the CTA's stores) and,
+      // when it draws the last ticket, again before the barrier that releases the readers
+      // (acquire of the other tiles' partials)
       __syncthreads();
-      if (tid == 0) s_last = (atomicAdd(a.bcnt + m.bctr, 1) == m.ntb - 1);
+      if (tid == 0) {
+        __threadfence();
+        s_last = (atomicAdd(a.bcnt + m.bctr, 1) == m.ntb - 1);
+        if (s_last) __threadfence();
+      }
       __syncthreads();
       last = s_last;
       if (last) {
-        __threadfence();
         const int outs = fwd ? m.nr : m.nc;
         const int stride = fwd ? m.nr : 32;
         for (int o = tid; o < outs; o += NT) {
