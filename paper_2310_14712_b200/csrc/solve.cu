@@ -36,7 +36,8 @@ namespace {
 
 enum { IT_F = 0, IT_B = 1 };
 constexpr int NT = 256;               // threads per CTA
-constexpr int NW = NT / 32;
+constexpr int NWC = NT / 32 - 1;      // compute warps (the last warp is the control warp)
+constexpr int NTC = NWC * 32;
 constexpr int VS = SOLVE_BROWS > SOLVE_TILE ? SOLVE_BROWS : SOLVE_TILE;   // gathered vector
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -105,14 +106,16 @@ __device__ __forceinline__ void complete_block(const SolveDev& a, int ph, int s,
   int act = 0;   // 0 nothing, 1 phase complete (forward: 2 parent ready, 3 root)
   if (lane == 0) {
     __threadfence();
-    if (atomicAdd(a.cnt + ph * n_sn + s, 1) == a.nblk[ph * n_sn + s] - 1) {
+    // a single-block phase / a single child needs no counter: this block completes it
+    const int nb = a.nblk[ph * n_sn + s];
+    if (nb == 1 || atomicAdd(a.cnt + ph * n_sn + s, 1) == nb - 1) {
       __threadfence();
       act = 1;
       if (ph == 0) {
         const int p = a.parent[s];
         if (p < 0) {
           act = 3;
-        } else if (atomicAdd(a.done_ch + p, 1) == a.nch[p] - 1) {
+        } else if (a.nch[p] == 1 || atomicAdd(a.done_ch + p, 1) == a.nch[p] - 1) {
           __threadfence();
           act = 2;
         }
@@ -243,77 +246,115 @@ __device__ __forceinline__ void stage_item(const SolveDev& a, const Item& m, dou
     bulk_g2s(st + j * nr, Ap + (size_t)(m.c0 + j) * m.ld + row0, nr * 8, bar);
 }
 
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+// named barriers: READY (control -> compute: next item's descriptor in smem, its copy issued),
+// FREE (compute -> control: staging buffer consumed), DONE+b (compute -> control: the results
+// of the item in descriptor buffer b written; one barrier per buffer, so the compute warps can
+// finish the next item before the control warp has consumed this one), CB (compute warps only)
+enum { BAR_READY = 1, BAR_FREE = 2, BAR_DONE = 3, BAR_CB = 5 };
+
+// control warp: take the next queue slot, stage its descriptor into dst (lane 0); returns the
+// item (-1 past the end), broadcast to the warp
+__device__ __forceinline__ int claim(const SolveDev& a, int4* dst, int* s_it, int lane) {
+  int it = 0;
+  if (lane == 0) {
+    const unsigned long long t0 = a.trace ? gtimer() : 0;
+    it = slot_item(a, atomicAdd(a.head, 1));
+    if (it >= 0) fetch_desc(a, it, dst);
+    *s_it = it;
+    if (a.trace && it >= 0) {
+      a.trace[5 * (size_t)it] = t0;
+      a.trace[5 * (size_t)it + 1] = gtimer();
+    }
+  }
+  return __shfl_sync(0xffffffffu, it, 0);
+}
+
+// Warp-specialised persistent CTA: NWC compute warps contract the staged tiles; the control
+// warp claims items, issues their panel copies and publishes completions, so the claim of item
+// k+1 and the publication of item k overlap the compute warps' gathers / contractions.
 __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
   extern __shared__ __align__(128) double stg[];   // c->solve_stage doubles (factor.cpp)
   __shared__ double vs[VS];
-  __shared__ double red[NT];
+  __shared__ double red[NTC];
   __shared__ __align__(8) uint64_t bar;
-  __shared__ int s_item, s_next, s_issued, s_last;
-  __shared__ int4 s_desc[5], s_desc2[5];
+  __shared__ int s_it[2], s_last[2];
+  __shared__ int4 s_desc[2][5];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    mbar_init(&bar);
-    s_next = -2;   // -2: nothing claimed ahead
-  }
-  unsigned phase = 0;
-  while (true) {
-    __syncthreads();   // previous item fully consumed (stage buffer and vs free)
-    // the item: either claimed during the previous item (queue backlog) — its descriptor
-    // staged in s_desc and its panel copy already issued — or claimed now
-    unsigned long long tclaim = 0;
-    if (tid == 0) {
-      if (a.trace) tclaim = gtimer();
-      if (s_next != -2) {
-        s_item = s_next;
-        s_issued = 1;
-        s_next = -2;
-      } else {
-        s_item = slot_item(a, atomicAdd(a.head, 1));
-        s_issued = 0;
-        if (s_item >= 0) fetch_desc(a, s_item, s_desc);
+  if (tid == 0) mbar_init(&bar);
+  __syncthreads();
+  if (warp == NWC) {
+    // ---------------- control warp ----------------
+    int buf = 0;
+    int it = claim(a, s_desc[0], &s_it[0], lane);
+    if (it >= 0) stage_item(a, load_item(s_desc[0]), stg, &bar, lane);
+    named_arrive(BAR_READY, NT);
+    while (it >= 0) {
+      const int4 d0 = s_desc[buf][0];   // type, s
+      // claim ahead when the queue backlog exceeds one item per CTA (the slot is then already
+      // pushed, so the wait is short and cannot depend on this CTA's unpublished item)
+      int nx = -2;
+      int ahead = 0;
+      if (lane == 0) ahead = a.n_init + ld_relaxed(a.tail) > ld_relaxed(a.head) + (int)gridDim.x;
+      if (__shfl_sync(0xffffffffu, ahead, 0)) nx = claim(a, s_desc[buf ^ 1], &s_it[buf ^ 1], lane);
+      named_sync(BAR_FREE, NT);   // the staging buffer is consumed
+      if (nx != -2) {
+        if (nx >= 0) stage_item(a, load_item(s_desc[buf ^ 1]), stg, &bar, lane);
+        named_arrive(BAR_READY, NT);
       }
+      if (buf) named_sync(BAR_DONE + 1, NT);
+      else named_sync(BAR_DONE, NT);   // results of item `it` written (cumulative: fence below)
+      if (s_last[buf]) complete_block(a, d0.x == IT_F ? 0 : 1, d0.y, lane);
+      if (a.trace && lane == 0) a.trace[5 * (size_t)it + 4] = gtimer();
+      if (nx == -2) {
+        nx = claim(a, s_desc[buf ^ 1], &s_it[buf ^ 1], lane);
+        if (nx >= 0) stage_item(a, load_item(s_desc[buf ^ 1]), stg, &bar, lane);
+        named_arrive(BAR_READY, NT);
+      }
+      buf ^= 1;
+      it = nx;
     }
-    __syncthreads();
-    const int it = s_item;
+    return;
+  }
+  // ---------------- compute warps (tid < NTC) ----------------
+  unsigned phase = 0;
+  int buf = 0;
+  while (true) {
+    named_sync(BAR_READY, NT);
+    const int it = s_it[buf];
     if (it < 0) return;
-    const Item m = load_item(s_desc);
+    const Item m = load_item(s_desc[buf]);
+    const int mb = buf;
+    buf ^= 1;
     const bool fwd = (m.type == IT_F);
-    if (a.trace && tid == 0) {
-      a.trace[5 * (size_t)it] = tclaim;
-      a.trace[5 * (size_t)it + 1] = gtimer();
-    }
-    // ---- stream the panel tile (TMA) unless already in flight; gather the input vector
-    // meanwhile (every producer of it completed before this item was pushed; L1 bypass)
-    if (warp == 0 && !s_issued) stage_item(a, m, stg, &bar, lane);
-    // ---- early claim of the next item when the queue backlog exceeds one item per CTA (the
-    // throughput-bound regime; a latency-bound solve never parks a ready item behind a busy
-    // CTA): its panel copy is issued as soon as this item's contraction releases the buffer
-    if (tid == NT - 32 && a.n_init + ld_relaxed(a.tail) > ld_relaxed(a.head) + (int)gridDim.x) {
-      const int nx = slot_item(a, atomicAdd(a.head, 1));
-      if (nx >= 0) fetch_desc(a, nx, s_desc2);
-      s_next = nx;
-    }
     const int go = m.goff;
+    // gather the input vector while the panel copy is in flight (every producer of it
+    // completed before this item was pushed; L1 bypass)
     if (fwd) {
       // v_j = b_j - sum of the children's update entries at column position j
-      for (int j = tid; j < m.nc; j += NT) {
+      for (int j = tid; j < m.nc; j += NTC) {
         const int pj = m.c0 + j;
         vs[j] = a.b[m.dof0 + pj] - child_sum(a, go + pj);
       }
     } else {
       const int rr = min(m.nr, m.r - m.r0);   // real (unpadded) rows of this tile
-      for (int i = tid; i < rr; i += NT) vs[i] = __ldcg(a.x + a.R[m.roff + m.r0 + i]);
+      for (int i = tid; i < rr; i += NTC) vs[i] = __ldcg(a.x + a.R[m.roff + m.r0 + i]);
       if (tid == 0 && rr < m.nr && rr >= 0) vs[rr] = 0.0;   // padding row
     }
     // forward: the children's contributions to the update rows this thread will emit (rows
-    // r0 + tid + k NT), gathered now so they overlap the panel copy instead of following it
+    // r0 + tid + k NTC), gathered now so they overlap the panel copy instead of following it
     constexpr int NCR = 4;
     double crv[NCR];
 #pragma unroll
     for (int k = 0; k < NCR; ++k) {
       crv[k] = 0.0;
-      const int i = m.r0 + tid + k * NT;
-      if (fwd && tid + k * NT < m.nr && i >= m.wp && i < m.wp + m.r) {
+      const int i = m.r0 + tid + k * NTC;
+      if (fwd && tid + k * NTC < m.nr && i >= m.wp && i < m.wp + m.r) {
         crv[k] = child_sum(a, go + m.w + (i - m.wp));
       }
     }
@@ -322,8 +363,8 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
     }
     phase ^= 1;
     if (a.trace && tid == 0) a.trace[5 * (size_t)it + 3] = gtimer();
-    __syncthreads();
-    // panel row i (= r0 + tid + kq NT) of the forward phase -> q_s or U_s
+    named_sync(BAR_CB, NTC);   // vs complete
+    // panel row i (= r0 + tid + kq NTC) of the forward phase -> q_s or U_s
     auto emit_f = [&](int i, double v, int kq) {
       if (i < m.w) {
         a.q[m.dof0 + i] = v;
@@ -343,12 +384,11 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
       if (j < m.w) a.x[m.dof0 + j] = __ldcg(a.q + m.dof0 + j) - v;
     };
     double* P = a.part + m.pslot;
-    bool last = true;
     if (fwd) {
-      // rows i of the tile: nr rows, nc columns; G threads per row when nr < NT
+      // rows i of the tile: nr rows, nc columns; G threads per row when nr < NTC
       const int nr = m.nr, nc = m.nc;
-      if (nr >= NT) {
-        for (int i = tid; i < nr; i += NT) {
+      if (nr >= NTC) {
+        for (int i = tid; i < nr; i += NTC) {
           double a0 = 0.0, a1 = 0.0;
           int j = 0;
           for (; j + 1 < nc; j += 2) {
@@ -356,17 +396,19 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
             a1 += stg[(j + 1) * nr + i] * vs[j + 1];
           }
           if (j < nc) a0 += stg[j * nr + i] * vs[j];
-          if (m.ntb == 1) emit_f(m.r0 + i, a0 + a1, (i - tid) / NT);
+          if (m.ntb == 1) emit_f(m.r0 + i, a0 + a1, (i - tid) / NTC);
           else P[m.t * nr + i] = a0 + a1;
         }
+        named_arrive(BAR_FREE, NT);
       } else {
-        const int G = NT / nr;   // nr >= 2
+        const int G = NTC / nr;   // nr >= 2
         const int i = tid % nr, g = tid / nr;
         double acc = 0.0;
         if (g < G)
           for (int j = g; j < nc; j += G) acc += stg[j * nr + i] * vs[j];
         red[tid] = acc;
-        __syncthreads();
+        named_arrive(BAR_FREE, NT);
+        named_sync(BAR_CB, NTC);
         if (tid < nr) {
           double v = 0.0;
           for (int k = 0; k < G; ++k) v += red[k * nr + tid];
@@ -375,9 +417,9 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
         }
       }
     } else {
-      // outputs: nc columns of G_s, warp w handles columns w, w + NW, ...; lanes stride rows
+      // outputs: nc columns of G_s, warp w handles columns w, w + NWC, ...; lanes stride rows
       const int nr = m.nr;
-      for (int cc = warp; cc < m.nc; cc += NW) {
+      for (int cc = warp; cc < m.nc; cc += NWC) {
         double v0 = 0.0, v1 = 0.0;
         int i = lane;
         for (; i + 32 < nr; i += 64) {
@@ -393,43 +435,37 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
           else P[m.t * 32 + cc] = v;
         }
       }
-    }
-    // the staging buffer is free once every thread has contracted: start the next item's copy
-    __syncthreads();
-    if (s_next >= 0) {
-      if (tid < 20) reinterpret_cast<int*>(s_desc)[tid] = reinterpret_cast<const int*>(s_desc2)[tid];
-      __syncwarp();
-      if (warp == 0) stage_item(a, load_item(s_desc2), stg, &bar, lane);
+      named_arrive(BAR_FREE, NT);
     }
     if (m.ntb > 1) {
       // partials of this tile written; the last tile of the group sums them in tile order.
-      // One thread fences after the barrier (cumulative release of the CTA's stores) and,
-      // when it draws the last ticket, again before the barrier that releases the readers
+      // One thread fences after the barrier (cumulative release of the compute warps' stores)
+      // and, when it draws the last ticket, again before the barrier that releases the readers
       // (acquire of the other tiles' partials)
-      __syncthreads();
+      named_sync(BAR_CB, NTC);
       if (tid == 0) {
         __threadfence();
-        s_last = (atomicAdd(a.bcnt + m.bctr, 1) == m.ntb - 1);
-        if (s_last) __threadfence();
+        s_last[mb] = (atomicAdd(a.bcnt + m.bctr, 1) == m.ntb - 1);
+        if (s_last[mb]) __threadfence();
       }
-      __syncthreads();
-      last = s_last;
-      if (last) {
+      named_sync(BAR_CB, NTC);
+      if (s_last[mb]) {
         const int outs = fwd ? m.nr : m.nc;
         const int stride = fwd ? m.nr : 32;
-        for (int o = tid; o < outs; o += NT) {
+        for (int o = tid; o < outs; o += NTC) {
           double v = 0.0;
           for (int k = 0; k < m.ntb; ++k) v += __ldcg(P + k * stride + o);
-          if (fwd) emit_f(m.r0 + o, v, (o - tid) / NT);
+          if (fwd) emit_f(m.r0 + o, v, (o - tid) / NTC);
           else emit_b(m.c0 + o, v);
         }
       }
+    } else if (tid == 0) {
+      s_last[mb] = 1;
     }
-    if (last) {
-      __syncthreads();   // the CTA's result stores precede lane 0's releasing fence (cumulative)
-      if (warp == 0) complete_block(a, fwd ? 0 : 1, m.s, lane);
-    }
-    if (a.trace && tid == 0) a.trace[5 * (size_t)it + 4] = gtimer();
+    // the control warp reads s_last and publishes after this barrier (its fence is cumulative
+    // over the compute warps' result stores ordered before it)
+    if (mb) named_arrive(BAR_DONE + 1, NT);
+    else named_arrive(BAR_DONE, NT);
   }
 }
 
