@@ -36,7 +36,7 @@ namespace {
 
 enum { IT_F = 0, IT_B = 1 };
 constexpr int NT = 256;               // threads per CTA
-constexpr int NWC = NT / 32 - 1;      // compute warps (the last warp is the control warp)
+constexpr int NWC = NT / 32 - 2;      // compute warps (then the claimer and publisher warps)
 constexpr int NTC = NWC * 32;
 constexpr int VS = SOLVE_BROWS > SOLVE_TILE ? SOLVE_BROWS : SOLVE_TILE;   // gathered vector
 
@@ -50,16 +50,6 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
-}
-
-// poll with plain acquire loads (no RMW traffic on the L2 atomic units) and backoff
-__device__ __forceinline__ void wait_ge(const int* p, int target) {
-  if (target <= 0) return;
-  unsigned ns = 32;
-  while (ld_acquire(p) < target) {
-    __nanosleep(ns);
-    if (ns < 256) ns <<= 1;
-  }
 }
 
 __device__ __forceinline__ void st_relaxed(int* p, int v) {
@@ -252,13 +242,15 @@ __device__ __forceinline__ void named_sync(int id, int n) {
 __device__ __forceinline__ void named_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-// named barriers: READY (control -> compute: next item's descriptor in smem, its copy issued),
-// FREE (compute -> control: staging buffer consumed), DONE+b (compute -> control: the results
-// of the item in descriptor buffer b written; one barrier per buffer, so the compute warps can
-// finish the next item before the control warp has consumed this one), CB (compute warps only)
-enum { BAR_READY = 1, BAR_FREE = 2, BAR_DONE = 3, BAR_CB = 5 };
+// named barriers: READY (claimer -> compute: next item's descriptor in smem, its copy issued),
+// FREE (compute -> claimer: staging buffer consumed), DONE+b (compute -> publisher: the item
+// whose completion record is in s_pub[b] is written), CONS+b (publisher -> compute: s_pub[b]
+// consumed), CB (compute warps only).  Two records so the compute warps can run one item ahead
+// of the publisher.
+enum { BAR_READY = 1, BAR_FREE = 2, BAR_DONE = 3, BAR_CONS = 5, BAR_CB = 7 };
+constexpr int NTX = NTC + 32;   // threads taking part in a compute <-> control-warp barrier
 
-// control warp: take the next queue slot, stage its descriptor into dst (lane 0); returns the
+// claimer warp: take the next queue slot, stage its descriptor into dst (lane 0); returns the
 // item (-1 past the end), broadcast to the warp
 __device__ __forceinline__ int claim(const SolveDev& a, int4* dst, int* s_it, int lane) {
   int it = 0;
@@ -275,62 +267,74 @@ __device__ __forceinline__ int claim(const SolveDev& a, int4* dst, int* s_it, in
   return __shfl_sync(0xffffffffu, it, 0);
 }
 
-// Warp-specialised persistent CTA: NWC compute warps contract the staged tiles; the control
-// warp claims items, issues their panel copies and publishes completions, so the claim of item
-// k+1 and the publication of item k overlap the compute warps' gathers / contractions.
-__global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
+// Warp-specialised persistent CTA: NWC compute warps gather and contract the staged tiles; a
+// claimer warp takes items from the queue and issues their panel copies; a publisher warp
+// publishes completions.  The three chains (claim latency, contraction, publication fences and
+// atomics) overlap across consecutive items of the CTA.
+__global__ void __launch_bounds__(NT, 5) k_solve(SolveDev a) {   // 5 CTAs/SM (shared memory)
   extern __shared__ __align__(128) double stg[];   // c->solve_stage doubles (factor.cpp)
   __shared__ double vs[VS];
   __shared__ double red[NTC];
   __shared__ __align__(8) uint64_t bar;
-  __shared__ int s_it[2], s_last[2];
+  __shared__ int s_it[2], s_tk;
   __shared__ int4 s_desc[2][5];
+  __shared__ int4 s_pub[2];   // completion records: item, type, supernode, last block
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) mbar_init(&bar);
   __syncthreads();
   if (warp == NWC) {
-    // ---------------- control warp ----------------
+    // ---------------- claimer warp ----------------
     int buf = 0;
     int it = claim(a, s_desc[0], &s_it[0], lane);
     if (it >= 0) stage_item(a, load_item(s_desc[0]), stg, &bar, lane);
-    named_arrive(BAR_READY, NT);
+    named_arrive(BAR_READY, NTX);
     while (it >= 0) {
-      const int4 d0 = s_desc[buf][0];   // type, s
-      // claim ahead when the queue backlog exceeds one item per CTA (the slot is then already
-      // pushed, so the wait is short and cannot depend on this CTA's unpublished item)
-      int nx = -2;
+      // claim ahead when the queue backlog exceeds one item per CTA; otherwise only once the
+      // compute warps are free, so a latency-bound solve never parks a ready item behind a
+      // busy CTA
       int ahead = 0;
       if (lane == 0) ahead = a.n_init + ld_relaxed(a.tail) > ld_relaxed(a.head) + (int)gridDim.x;
+      int nx = -2;
       if (__shfl_sync(0xffffffffu, ahead, 0)) nx = claim(a, s_desc[buf ^ 1], &s_it[buf ^ 1], lane);
-      named_sync(BAR_FREE, NT);   // the staging buffer is consumed
-      if (nx != -2) {
-        if (nx >= 0) stage_item(a, load_item(s_desc[buf ^ 1]), stg, &bar, lane);
-        named_arrive(BAR_READY, NT);
-      }
-      if (buf) named_sync(BAR_DONE + 1, NT);
-      else named_sync(BAR_DONE, NT);   // results of item `it` written (cumulative: fence below)
-      if (s_last[buf]) complete_block(a, d0.x == IT_F ? 0 : 1, d0.y, lane);
-      if (a.trace && lane == 0) a.trace[5 * (size_t)it + 4] = gtimer();
-      if (nx == -2) {
-        nx = claim(a, s_desc[buf ^ 1], &s_it[buf ^ 1], lane);
-        if (nx >= 0) stage_item(a, load_item(s_desc[buf ^ 1]), stg, &bar, lane);
-        named_arrive(BAR_READY, NT);
-      }
+      named_sync(BAR_FREE, NTX);   // the staging buffer is consumed
+      if (nx == -2) nx = claim(a, s_desc[buf ^ 1], &s_it[buf ^ 1], lane);
+      if (nx >= 0) stage_item(a, load_item(s_desc[buf ^ 1]), stg, &bar, lane);
+      named_arrive(BAR_READY, NTX);
       buf ^= 1;
       it = nx;
     }
     return;
   }
+  if (warp == NWC + 1) {
+    // ---------------- publisher warp ----------------
+    named_arrive(BAR_CONS, NTX);
+    named_arrive(BAR_CONS + 1, NTX);
+    for (int buf = 0;; buf ^= 1) {
+      if (buf) named_sync(BAR_DONE + 1, NTX);
+      else named_sync(BAR_DONE, NTX);
+      const int4 r = s_pub[buf];
+      if (buf) named_arrive(BAR_CONS + 1, NTX);
+      else named_arrive(BAR_CONS, NTX);
+      if (r.x < 0) return;
+      // the compute warps' result stores precede DONE; lane 0's fence is cumulative over them
+      if (r.w) complete_block(a, r.y == IT_F ? 0 : 1, r.z, lane);
+      if (a.trace && lane == 0) a.trace[5 * (size_t)r.x + 4] = gtimer();
+    }
+  }
   // ---------------- compute warps (tid < NTC) ----------------
   unsigned phase = 0;
-  int buf = 0;
-  while (true) {
-    named_sync(BAR_READY, NT);
+  for (int buf = 0, pb = 0;; buf ^= 1, pb ^= 1) {
+    named_sync(BAR_READY, NTX);
     const int it = s_it[buf];
-    if (it < 0) return;
+    if (it < 0) {
+      if (pb) named_sync(BAR_CONS + 1, NTX);
+      else named_sync(BAR_CONS, NTX);
+      if (tid == 0) s_pub[pb] = make_int4(-1, 0, 0, 0);
+      if (pb) named_arrive(BAR_DONE + 1, NTX);
+      else named_arrive(BAR_DONE, NTX);
+      return;
+    }
     const Item m = load_item(s_desc[buf]);
-    const int mb = buf;
-    buf ^= 1;
     const bool fwd = (m.type == IT_F);
     const int go = m.goff;
     // gather the input vector while the panel copy is in flight (every producer of it
@@ -384,6 +388,7 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
       if (j < m.w) a.x[m.dof0 + j] = __ldcg(a.q + m.dof0 + j) - v;
     };
     double* P = a.part + m.pslot;
+    bool last = true;
     if (fwd) {
       // rows i of the tile: nr rows, nc columns; G threads per row when nr < NTC
       const int nr = m.nr, nc = m.nc;
@@ -399,7 +404,7 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
           if (m.ntb == 1) emit_f(m.r0 + i, a0 + a1, (i - tid) / NTC);
           else P[m.t * nr + i] = a0 + a1;
         }
-        named_arrive(BAR_FREE, NT);
+        named_arrive(BAR_FREE, NTX);
       } else {
         const int G = NTC / nr;   // nr >= 2
         const int i = tid % nr, g = tid / nr;
@@ -407,7 +412,7 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
         if (g < G)
           for (int j = g; j < nc; j += G) acc += stg[j * nr + i] * vs[j];
         red[tid] = acc;
-        named_arrive(BAR_FREE, NT);
+        named_arrive(BAR_FREE, NTX);
         named_sync(BAR_CB, NTC);
         if (tid < nr) {
           double v = 0.0;
@@ -435,7 +440,7 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
           else P[m.t * 32 + cc] = v;
         }
       }
-      named_arrive(BAR_FREE, NT);
+      named_arrive(BAR_FREE, NTX);
     }
     if (m.ntb > 1) {
       // partials of this tile written; the last tile of the group sums them in tile order.
@@ -445,11 +450,12 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
       named_sync(BAR_CB, NTC);
       if (tid == 0) {
         __threadfence();
-        s_last[mb] = (atomicAdd(a.bcnt + m.bctr, 1) == m.ntb - 1);
-        if (s_last[mb]) __threadfence();
+        s_tk = (atomicAdd(a.bcnt + m.bctr, 1) == m.ntb - 1);
+        if (s_tk) __threadfence();
       }
       named_sync(BAR_CB, NTC);
-      if (s_last[mb]) {
+      last = s_tk;
+      if (last) {
         const int outs = fwd ? m.nr : m.nc;
         const int stride = fwd ? m.nr : 32;
         for (int o = tid; o < outs; o += NTC) {
@@ -459,13 +465,14 @@ __global__ void __launch_bounds__(NT) k_solve(SolveDev a) {
           else emit_b(m.c0 + o, v);
         }
       }
-    } else if (tid == 0) {
-      s_last[mb] = 1;
     }
-    // the control warp reads s_last and publishes after this barrier (its fence is cumulative
-    // over the compute warps' result stores ordered before it)
-    if (mb) named_arrive(BAR_DONE + 1, NT);
-    else named_arrive(BAR_DONE, NT);
+    // completion record for the publisher (its fence is cumulative over the compute warps'
+    // result stores ordered before DONE); wait until the record slot is free
+    if (pb) named_sync(BAR_CONS + 1, NTX);
+    else named_sync(BAR_CONS, NTX);
+    if (tid == 0) s_pub[pb] = make_int4(it, m.type, m.s, last ? 1 : 0);
+    if (pb) named_arrive(BAR_DONE + 1, NTX);
+    else named_arrive(BAR_DONE, NTX);
   }
 }
 
