@@ -866,7 +866,7 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   // (r, goff, uoff, roff) (aoff lo, aoff hi, ld, wp).
   const int TILE = SOLVE_TILE;
   int stage = SOLVE_STAGE;
-  if (const char* v = getenv("SC_SOLVE_STAGE")) stage = std::max(SOLVE_STAGE, std::min(4 * SOLVE_STAGE, atoi(v)));
+  if (const char* v = getenv("SC_SOLVE_STAGE")) stage = std::max(1024, std::min(4 * SOLVE_STAGE, atoi(v)));
   c->solve_stage = stage;
   std::vector<int32_t> items;
   std::vector<int32_t> nblk(2 * (size_t)nsn, 0);
@@ -892,7 +892,7 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   };
   auto fwd_items = [&](int s) {
     const int w = wv[s], ld = panel_ld(w, rv[s]);
-    const int C = std::min(w, TILE);
+    const int C = std::min({w, TILE, stage / 32});
     int R = 32;
     while (2 * R * C <= stage && R < ((ld + 31) / 32) * 32) R *= 2;
     const int ntb = (w + C - 1) / C;

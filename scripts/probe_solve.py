@@ -49,10 +49,10 @@ def analyse(path):
             m = (ph == p_) & (height[items[:, 1]] == h)
             if not m.any():
                 continue
-            ent = (w[items[m, 1]].astype(np.int64) * (w + r)[items[m, 1]]).sum()
+            nbytes = 8 * (items[m, 7].astype(np.int64) * items[m, 9]).sum()
             levels.append({"phase": "F" if p_ == 0 else "B", "h": h, "start": round(float(tr[m, 1].min() / 1e3), 1),
                            "end": round(float(tr[m, 2].max() / 1e3), 1), "items": int(m.sum()),
-                           "fused": int((m & fused).sum()),
+                           "fused": int((m & fused).sum()), "MB": round(float(nbytes) / 1e6, 1),
                            "max_work_us": round(float((tr[m, 2] - tr[m, 1]).max() / 1e3), 2)})
     out["levels"] = levels
     print(json.dumps(out))
