@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsc.so")
+LIB_PATH = os.environ.get("SC_LIB", os.path.join(_HERE, "libsc.so"))   # SC_LIB: variant builds (experiments)
 
 SC_OK, SC_ERR_CONFIG, SC_ERR_NUMERIC = 0, 2, 3
 SC_VOID_ELLIPSOID, SC_VOID_HALFSPACE = 1, 2

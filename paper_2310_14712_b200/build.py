@@ -6,8 +6,9 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "libsc.so")
-BUILD = os.path.join(HERE, "_build")
+OUT = os.environ.get("SC_BUILD_OUT", os.path.join(HERE, "libsc.so"))   # experiments: variant builds
+BUILD = os.path.join(HERE, "_build" + os.environ.get("SC_BUILD_TAG", ""))
+DEFS = os.environ.get("SC_NVCC_DEFS", "").split()   # experiments: e.g. -DSOLVE_NT=256
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU = ["setup.cu", "step.cu", "solve.cu"]
@@ -43,12 +44,12 @@ def build(force=False, verbose=False):
     logs = []
     for f in CU:
         o = os.path.join(BUILD, f + ".o")
-        logs.append(_run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+        logs.append(_run([NVCC, *ARCH, *DEFS, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                           "--expt-relaxed-constexpr", "-Xptxas", "-v", "-c", os.path.join(CSRC, f), "-o", o]))
         objs.append(o)
     for f in CPP:
         o = os.path.join(BUILD, f + ".o")
-        logs.append(_run([NVCC, *ARCH, "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-fopenmp,-ffp-contract=off",
+        logs.append(_run([NVCC, *ARCH, *DEFS, "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-fopenmp,-ffp-contract=off",
                           "-c", os.path.join(CSRC, f), "-o", o]))
         objs.append(o)
     tmp = OUT + ".tmp"

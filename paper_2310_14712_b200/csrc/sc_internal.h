@@ -15,7 +15,15 @@
 // forward tiles have at most SOLVE_TILE columns, backward tiles at most SOLVE_BROWS rows
 #define SOLVE_TILE 128
 #define SOLVE_STAGE 4096
-#define SOLVE_BROWS 1024
+#ifndef SOLVE_BROWS
+#define SOLVE_BROWS 512
+#endif
+#ifndef SOLVE_NT
+#define SOLVE_NT 192     // k_solve threads: 4 compute warps + claimer + publisher
+#endif
+#ifndef SOLVE_MINB
+#define SOLVE_MINB 6     // resident k_solve CTAs per SM (shared memory: 32 KB stage + 4 KB)
+#endif
 
 // ---------------------------------------------------------------- device-side data
 struct DVoid {

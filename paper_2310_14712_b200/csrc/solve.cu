@@ -35,10 +35,10 @@
 namespace {
 
 enum { IT_F = 0, IT_B = 1 };
-constexpr int NT = 256;               // threads per CTA
+constexpr int NT = SOLVE_NT;          // threads per CTA
 constexpr int NWC = NT / 32 - 2;      // compute warps (then the claimer and publisher warps)
 constexpr int NTC = NWC * 32;
-constexpr int VS = SOLVE_BROWS > SOLVE_TILE ? SOLVE_BROWS : SOLVE_TILE;   // gathered vector
+constexpr int VS = SOLVE_BROWS > SOLVE_TILE + NTC ? SOLVE_BROWS : SOLVE_TILE + NTC;   // gathered vector
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -271,10 +271,10 @@ __device__ __forceinline__ int claim(const SolveDev& a, int4* dst, int* s_it, in
 // claimer warp takes items from the queue and issues their panel copies; a publisher warp
 // publishes completions.  The three chains (claim latency, contraction, publication fences and
 // atomics) overlap across consecutive items of the CTA.
-__global__ void __launch_bounds__(NT, 5) k_solve(SolveDev a) {   // 5 CTAs/SM (shared memory)
+__global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTAs/SM (shared memory)
   extern __shared__ __align__(128) double stg[];   // c->solve_stage doubles (factor.cpp)
   __shared__ double vs[VS];
-  __shared__ double red[NTC];
+  double* red = vs + SOLVE_TILE;   // forward reductions (the gathered vector has <= SOLVE_TILE entries)
   __shared__ __align__(8) uint64_t bar;
   __shared__ int s_it[2], s_tk;
   __shared__ int4 s_desc[2][5];
@@ -485,6 +485,7 @@ void launch_solve(sc_ctx* c, const Factor& f, cudaStream_t st) {
   const int smem = (int)(sizeof(double) * c->solve_stage);
   if (c->solve_grid == 0) {
     SC_CUDA(cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    SC_CUDA(cudaFuncSetAttribute(k_solve, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     int per_sm = 0, sms = 0, dev = 0;
     SC_CUDA(cudaGetDevice(&dev));
     SC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
