@@ -324,8 +324,17 @@ struct Tile3 {
   static constexpr int E = P <= 2 ? 8 : (P == 3 ? 7 : (P == 4 ? 5 : 3));
   static constexpr int EZ = 8;    // default element layers per tile (+1 warm-up layer)
   static constexpr int NT = P == 3 ? 224 : (P == 4 ? 160 : 256);
-  static constexpr int MINB = P == 3 ? 2 : (P == 4 ? 2 : (P <= 2 ? 2 : 1));
-  static constexpr bool SPV = (P == 3 || P == 4);   // u_{n-1} staged through shared memory
+// p = 4: 3 CTAs/SM with u_{n-1} prefetched into registers (128 registers, 72 KB shared) beat
+// 2 CTAs/SM with u_{n-1} staged in shared memory (162 registers, 107 KB): config 5 explicit
+// 4.17 vs 4.53 ms (profiles/r1_solve_variants.txt, explicit section)
+#ifndef EXP4_MINB
+#define EXP4_MINB 3
+#endif
+#ifndef EXP4_SPV
+#define EXP4_SPV 0
+#endif
+  static constexpr int MINB = P == 3 ? 2 : (P == 4 ? EXP4_MINB : (P <= 2 ? 2 : 1));
+  static constexpr bool SPV = P == 3 || (P == 4 && EXP4_SPV);   // u_{n-1} staged through shared memory
   static constexpr int RX = (E + 1) * P + 1;
   static constexpr int TY = E * P + 1;
   static constexpr size_t smem = sizeof(double) * (2 * (P + 1) * RX * RX + 4 * TY * RX + 4 * (E + 1) * RX +
