@@ -189,6 +189,13 @@ sc_status sc_exchange_local(sc_ctx* const* ctxs, int32_t world);
  * Clobbers the state: call sc_set_state before stepping again.  One rank only. */
 sc_status sc_estimate_dt(sc_ctx* ctx, int32_t iters, double* lambda_max, double* dt_crit);
 
+/* Elastic energy E = 1/2 u_n^T K u_n of the current state (PAPER.md P:758,
+ * the quantity of fig:springCoupledMassesElastic) into *energy (host).  Computed by the step
+ * kernels with zero CDM coefficients (M^{-1} K u on the d rows, K u on the c rows through the
+ * c-element products) and a fixed-order reduction: bit-reproducible.  Does not change the
+ * state; synchronises.  One rank only (SC_ERR_CONFIG otherwise). */
+sc_status sc_elastic_energy(sc_ctx* ctx, double* energy);
+
 /* Receivers (the paper's receiver traces, fig:solutions3D):
  * record u(x_r, t_{n+1}) = sum_i N_i(x_r) u_i (basis of the lowest-index non-empty cell
  * containing x_r) after every step; xyz: n points (x, y, z) each (unused dims ignored);

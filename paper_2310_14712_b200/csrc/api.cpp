@@ -390,6 +390,21 @@ extern "C" sc_status sc_exchange_local(sc_ctx* const* ctxs, int32_t world) {
   }
 }
 
+extern "C" sc_status sc_elastic_energy(sc_ctx* c, double* energy) {
+  if (!c || !energy) return SC_ERR_STATE;
+  if (c->world > 1) {
+    c->err = "sc_elastic_energy: one rank";
+    return SC_ERR_CONFIG;
+  }
+  try {
+    SC_CUDA(cudaSetDevice(c->device));
+    *energy = elastic_energy(c);
+    return SC_OK;
+  } catch (const ScError& e) {
+    return fail(c, e);
+  }
+}
+
 extern "C" sc_status sc_estimate_dt(sc_ctx* c, int32_t iters, double* lambda_max, double* dt_crit) {
   if (!c) return SC_ERR_STATE;
   if (iters < 1 || c->world > 1 || c->integrator == 2) {

@@ -258,6 +258,7 @@ void enqueue_pack(sc_ctx* c, const double* u, cudaStream_t st);
 void enqueue_unpack(sc_ctx* c, double* u, cudaStream_t st);
 void gather_owned(sc_ctx* c, const double* d_lat, double* d_dst);
 double estimate_lambda(sc_ctx* c, int iters);
+double elastic_energy(sc_ctx* c);
 // factor (factor.cpp)
 void setup_factor(sc_ctx* c, const std::vector<double>& Mcut_host);
 void point_weights(const sc_ctx* c, const double* x, bool with_alpha,

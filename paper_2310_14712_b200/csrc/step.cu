@@ -854,6 +854,58 @@ __global__ void k_scale_into(double* x, const double* __restrict__ y, const doub
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) x[i] = y[i] * sc[1];
 }
+// elastic energy E = 1/2 u^T K u: the terms u_i (K u)_i summed in a
+// fixed order (grid-stride per thread, warp shuffles, one partial per block, one final thread):
+//   tensor-d rows  (K u)_i = M_i Y_i,  Y = M^{-1} K u from the explicit kernel,
+//                  M_i = rho prod_k (h_k/2) wt(i_k)  (the lumped mass the kernel divides by)
+//   irregular rows (K u)_i = Y_i / invm_i            (k_irregular with a zero load)
+//   c rows         (K u)_i = -b_i                    (c-element products, k_crhs, zero load)
+__global__ void k_energy_terms(const double* __restrict__ U, const double* __restrict__ Y,
+                               const uint8_t* __restrict__ nt, GridP g, double mscale,
+                               const int32_t* __restrict__ irr_lat, const double* __restrict__ irr_invm,
+                               long long n_irr, const int32_t* __restrict__ c_lat,
+                               const double* __restrict__ bc, long long n_c, long long n, double* part) {
+  __shared__ double sh[32];
+  double a = 0.0;
+  const long long tot = n + n_irr + n_c;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot;
+       t += (long long)gridDim.x * blockDim.x) {
+    if (t < n) {
+      const uint8_t ty = nt[t];
+      if (ty == 1 || ty == 4) {
+        long long rem = t;
+        double m = mscale;
+        for (int k = 0; k < g.dim; ++k) {
+          const int ik = (int)(rem % g.nl[k]);
+          rem /= g.nl[k];
+          m *= wt(ik, g.N[k], g.p);
+        }
+        a += U[t] * (m * Y[t]);
+      }
+    } else if (t < n + n_irr) {
+      const long long j = t - n;
+      const int32_t L = irr_lat[j];
+      a += U[L] * (Y[L] / irr_invm[j]);
+    } else {
+      const long long j = t - n - n_irr;
+      a -= U[c_lat[j]] * bc[j];
+    }
+  }
+  for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sh[w] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) b += sh[k];
+    part[blockIdx.x] = b;
+  }
+}
+__global__ void k_half_sum(const double* part, int nblk, double* out) {
+  double a = 0.0;
+  for (int k = 0; k < nblk; ++k) a += part[k];
+  out[0] = 0.5 * a;
+}
 }  // namespace
 
 double estimate_lambda(sc_ctx* c, int iters) {
@@ -897,4 +949,38 @@ double estimate_lambda(sc_ctx* c, int iters) {
   cudaFree(scratch);
   c->far_ready = false;
   return h[0];
+}
+
+// E = 1/2 u_n^T K u_n of the current state (one rank): the step kernels with zero CDM
+// coefficients give M^{-1} K u on the d rows and K u on the c rows (k_energy_terms above)
+double elastic_energy(sc_ctx* c) {
+  const GridP& g = c->g;
+  const long long n = c->n_lat;
+  const double* U = c->d_u[c->cur];
+  double *Y = nullptr, *bc = nullptr, *part = nullptr;
+  const int nblk = 148 * 4;
+  SC_CUDA(cudaMalloc(&Y, sizeof(double) * std::max<long long>(1, n)));
+  SC_CUDA(cudaMalloc(&bc, sizeof(double) * std::max<long long>(1, c->n_cl)));
+  SC_CUDA(cudaMalloc(&part, sizeof(double) * (nblk + 1)));
+  launch_explicit(c, U, U, Y, 0.0, 0.0, -1.0, 5, c->stream);
+  launch_irregular(c, U, U, Y, 0.0, 0.0, -1.0, c->stream, 0.0);
+  if (c->n_cl > 0) {
+    launch_celem(c, 1, U, U, c->stream);
+    k_crhs<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, c->stream>>>(bc, c->d_fxc, c->d_rhs_ptr, c->d_rhs_idx, c->d_Y,
+                                                                       (int)c->n_cl, c->d_ft, c->n_t, c->d_step, 0,
+                                                                       nullptr, 0.0);
+  }
+  double ms = c->rho;
+  for (int k = 0; k < g.dim; ++k) ms *= 0.5 * g.h[k];
+  k_energy_terms<<<nblk, 256, 0, c->stream>>>(U, Y, c->d_ntype, g, ms, c->d_irr_lat, c->d_irr_invm, c->n_irr,
+                                              c->d_c_lat, bc, c->n_cl, n, part);
+  k_half_sum<<<1, 1, 0, c->stream>>>(part, nblk, part + nblk);
+  SC_CUDA(cudaGetLastError());
+  double e = 0.0;
+  SC_CUDA(cudaMemcpyAsync(&e, part + nblk, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  SC_CUDA(cudaStreamSynchronize(c->stream));
+  cudaFree(Y);
+  cudaFree(bc);
+  cudaFree(part);
+  return e;
 }
