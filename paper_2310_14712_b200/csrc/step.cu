@@ -613,6 +613,7 @@ void setup_step_structures(sc_ctx* c) {
     g.ezl = 16;
     explicit_tiling(g, ext, tg);
     if ((int64_t)tg[0] * tg[1] * tg[2] < 4 * 2 * 148) g.ezl = 8;
+    if (const char* v = getenv("SC_EZL")) g.ezl = std::max(1, atoi(v));   // experiments
   }
   explicit_tiling(g, ext, tg);
   // tile lists of the node types this rank updates: near-d (type 4) always, far-d (type 1)
