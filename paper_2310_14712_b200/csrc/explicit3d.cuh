@@ -317,26 +317,38 @@ __global__ void __launch_bounds__(NT, MINB) k_explicit_3d(const double* __restri
   }
 }
 
-// tile shapes: the z+y phase has RX*(E+1) column items and the x phase (E*P+1) rows of
-// (E+1) lanes; NT is chosen so that both keep >= 84% of the threads busy (one item each)
-template <int P>
-struct Tile3 {
-  static constexpr int E = P <= 2 ? 8 : (P == 3 ? 7 : (P == 4 ? 5 : 3));
-  static constexpr int EZ = 8;    // default element layers per tile (+1 warm-up layer)
-  static constexpr int NT = P == 3 ? 224 : (P == 4 ? 160 : 256);
-// p = 4: 3 CTAs/SM with u_{n-1} prefetched into registers (128 registers, 72 KB shared) beat
-// 2 CTAs/SM with u_{n-1} staged in shared memory (162 registers, 107 KB): config 5 explicit
-// 4.17 vs 4.53 ms (profiles/r1_solve_variants.txt, explicit section)
+// Tile shapes (EX = E along x, EY along y): the z+y phase has RX*(EY+1) column items and the
+// x phase (EY*P+1) rows of (E+1) lanes; NT is chosen so that both keep >= 84% of the threads
+// busy (one item each).  p = 4 (config 5; profiles/r1_solve_variants.txt, explicit section):
+// E = EY = 6, NT = 224, 2 CTAs/SM, u_{n-1} prefetched into registers: 3.92 ms; E = 5, NT = 160
+// at 3 CTAs/SM 4.17 ms (u_{n-1} staged in shared memory at 2 CTAs/SM: 4.53 ms); E = 4 at
+// 4 CTAs/SM 4.50 ms — the low-side halo element costs (E+1)^2/E^2 of the z+y work.
+#ifndef EXP4_E
+#define EXP4_E 6
+#endif
+#ifndef EXP4_EY
+#define EXP4_EY EXP4_E
+#endif
+#ifndef EXP4_NT
+#define EXP4_NT 224
+#endif
 #ifndef EXP4_MINB
-#define EXP4_MINB 3
+#define EXP4_MINB 2
 #endif
 #ifndef EXP4_SPV
 #define EXP4_SPV 0
 #endif
+template <int P>
+struct Tile3 {
+  static constexpr int E = P <= 2 ? 8 : (P == 3 ? 7 : (P == 4 ? EXP4_E : 3));
+  static constexpr int EY = P == 4 ? EXP4_EY : E;
+  static constexpr int EZ = 8;    // default element layers per tile (+1 warm-up layer)
+  static constexpr int NT = P == 3 ? 224 : (P == 4 ? EXP4_NT : 256);
   static constexpr int MINB = P == 3 ? 2 : (P == 4 ? EXP4_MINB : (P <= 2 ? 2 : 1));
   static constexpr bool SPV = P == 3 || (P == 4 && EXP4_SPV);   // u_{n-1} staged through shared memory
   static constexpr int RX = (E + 1) * P + 1;
-  static constexpr int TY = E * P + 1;
-  static constexpr size_t smem = sizeof(double) * (2 * (P + 1) * RX * RX + 4 * TY * RX + 4 * (E + 1) * RX +
+  static constexpr int RY = (EY + 1) * P + 1;
+  static constexpr int TY = EY * P + 1;
+  static constexpr size_t smem = sizeof(double) * (2 * (P + 1) * RX * RY + 4 * TY * RX + 4 * (EY + 1) * RX +
                                                    (SPV ? 2 * (P + 1) * TY * (E * P + 1) : 0));
 };

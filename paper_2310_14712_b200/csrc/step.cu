@@ -361,7 +361,8 @@ void tiling_p(const GridP& g, int ext[3], int tg[3]) {
     ext[0] = ext[1] = Tile2v<P>::E;
   } else if (g.dim == 3) {
     if constexpr (P <= 6) {
-      ext[0] = ext[1] = Tile3<P>::E;
+      ext[0] = Tile3<P>::E;
+      ext[1] = Tile3<P>::EY;
       ext[2] = g.ezl > 0 ? g.ezl : Tile3<P>::EZ;
     }
   }
@@ -391,7 +392,7 @@ void launch_explicit_p(sc_ctx* c, const double* U, const double* Pv, double* out
   } else {
     if constexpr (P <= 6) {
       using T = Tile3<P>;
-      auto kern = k_explicit_3d<P, T::E, T::E, T::NT, T::MINB, T::SPV>;
+      auto kern = k_explicit_3d<P, T::E, T::EY, T::NT, T::MINB, T::SPV>;
       static bool attr = false;
       if (!attr) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::smem);
