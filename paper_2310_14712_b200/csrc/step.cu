@@ -164,6 +164,12 @@ __global__ void k_irregular(const double* __restrict__ U, const double* Pv, doub
 // ------------------------------------------------------------------ c elements
 // mode 0 (step): w = predictor u~^c on c nodes, u^d_{n+1} (buffer B) elsewhere;
 // mode 1 (start): w = A everywhere.   Y[e][i] = sum_j K_e[i][j] w_j (K_e symmetric).
+#ifndef CELEM_U
+#define CELEM_U 8
+#endif
+#ifndef CELEM_CS
+#define CELEM_CS 0
+#endif
 __global__ void k_celem(int mode, const double* __restrict__ A, const double* __restrict__ B,
                         const double* __restrict__ vc, const double* __restrict__ ac, double dt,
                         const int32_t* __restrict__ ecell, const int32_t* __restrict__ ekidx,
@@ -207,19 +213,25 @@ __global__ void k_celem(int mode, const double* __restrict__ A, const double* __
   if (!ok) return;
   const int kidx = ekidx[e];
   const double* K = kidx >= 0 ? Kcut + (size_t)kidx * nb * nb : Kref;
-  for (int r = i; r < nb; r += tpe) {
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    int j = 0;
-    for (; j + 8 <= nb; j += 8) {   // 8 independent loads in flight (HBM-bound GEMV)
-      double x[8];
+  auto gemv = [&](auto ld) {
+    for (int r = i; r < nb; r += tpe) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      int j = 0;
+      for (; j + CELEM_U <= nb; j += CELEM_U) {   // CELEM_U independent loads in flight (HBM-bound GEMV)
+        double x[CELEM_U];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) x[k] = __ldg(K + (size_t)(j + k) * nb + r);
+        for (int k = 0; k < CELEM_U; ++k) x[k] = ld(K + (size_t)(j + k) * nb + r);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) acc[k & 3] += x[k] * w[j + k];
+        for (int k = 0; k < CELEM_U; ++k) acc[k & 3] += x[k] * w[j + k];
+      }
+      for (; j < nb; ++j) acc[0] += ld(K + (size_t)j * nb + r) * w[j];
+      Y[(size_t)e * nb + r] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
     }
-    for (; j < nb; ++j) acc[0] += __ldg(K + (size_t)j * nb + r) * w[j];
-    Y[(size_t)e * nb + r] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-  }
+  };
+  // cut-cell matrices are streamed once per step (evict-first); the shared uncut reference
+  // matrix stays cached
+  if (CELEM_CS && kidx >= 0) gemv([](const double* p) { return __ldcs(p); });
+  else gemv([](const double* p) { return __ldg(p); });
 }
 
 __global__ void k_crhs(double* __restrict__ b, const double* __restrict__ fxc, const int32_t* __restrict__ ptr,
