@@ -1073,7 +1073,6 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   sd.init = c->d_qmeta + 5 * (size_t)nsn;
   sd.n_init = c->n_init;
   sd.tile = TILE;
-  sd.prefetch = getenv("SC_SOLVE_PREFETCH") ? atoi(getenv("SC_SOLVE_PREFETCH")) : 0;
   sd.trace = nullptr;
   if (getenv("SC_TRACE")) {
     SC_CUDA(cudaMalloc(&c->d_trace, sizeof(unsigned long long) * 5 * std::max(1, c->n_items)));

@@ -69,7 +69,6 @@ struct SolveDev {
   int n_init;
   int tile;                    // reduction-tile length (SOLVE_TILE)
   int stage;                   // staging buffer (doubles; two per CTA)
-  int prefetch;                // SC_SOLVE_PREFETCH=1: L2 bulk prefetch of a phase's panel at push
   unsigned long long* trace;   // optional (SC_TRACE): per item [claim, item, gathered, staged, done] ns
 };
 

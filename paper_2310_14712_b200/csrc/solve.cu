@@ -56,43 +56,39 @@ __device__ __forceinline__ void st_relaxed(int* p, int v) {
   asm volatile("st.relaxed.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
 
-__device__ __forceinline__ void bulk_prefetch_l2(const void* p, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
-// L2 prefetch (TMA bulk prefetch) of the panel data of phase ph of supernode s (warp), so the
-// items' staging copies hit L2: forward streams the whole panel, backward the G_s parts
-__device__ __forceinline__ void prefetch_phase(const SolveDev& a, int ph, int s, int lane) {
-  const int first = a.item_first[ph * a.n_sn + s];
-  const int4 d2 = a.items[5 * (size_t)first + 2], d3 = a.items[5 * (size_t)first + 3],
-             d4 = a.items[5 * (size_t)first + 4];
-  const int w = d2.w, r = d3.x, ld = d4.z, wp = d4.w;
-  const double* Ap = a.A + ((int64_t)(uint32_t)d4.x | ((int64_t)d4.y << 32));
-  if (ph == 0) {
-    const size_t bytes = (size_t)ld * w * 8;
-    for (size_t o = (size_t)lane << 16; o < bytes; o += (size_t)32 << 16)
-      bulk_prefetch_l2(reinterpret_cast<const char*>(Ap) + o, (unsigned)min((size_t)1 << 16, bytes - o));
-  } else if (r > 0) {
-    const unsigned bytes = (unsigned)(((r + 1) & ~1) * 8);
-    for (int j = lane; j < w; j += 32) bulk_prefetch_l2(Ap + (size_t)j * ld + wp, bytes);
-  }
-}
-
-// make the items of phase ph of supernode s ready (warp 0; the caller fenced after observing
-// the completion it reacts to, so relaxed slot stores publish everything before the fence)
-__device__ __forceinline__ void push_phase(const SolveDev& a, int ph, int s, int lane) {
-  const int first = a.item_first[ph * a.n_sn + s], cnt = a.item_cnt[ph * a.n_sn + s];
+// push cnt items starting at first (warp; the caller fenced after observing the completion
+// it reacts to, so relaxed slot stores publish everything before the fence)
+__device__ __forceinline__ void push_items(const SolveDev& a, int first, int cnt, int lane) {
   int slot = 0;
-  if (lane == 0) slot = atomicAdd(a.tail, cnt);
+  if (lane == 0 && cnt) slot = atomicAdd(a.tail, cnt);
   slot = __shfl_sync(0xffffffffu, slot, 0);
   for (int k = lane; k < cnt; k += 32) st_relaxed(a.ready + slot + k, first + k + 1);
-  if (a.prefetch) prefetch_phase(a, ph, s, lane);
 }
 
-// one block of phase ph of supernode s is published (warp 0, after the block's results were
-// written and fenced); the warp completing the phase pushes its dependents
+// one block of phase ph of supernode s is published (publisher warp, after the block's
+// results were written); the warp completing the phase pushes its dependents.  The item
+// ranges of the dependents (read-only metadata) are loaded by all lanes BEFORE lane 0's
+// fence and atomics, so they are not on the publication's dependent-latency chain; the
+// backward children are pushed with one tail reservation for all of them.
 __device__ __forceinline__ void complete_block(const SolveDev& a, int ph, int s, int lane) {
   const int n_sn = a.n_sn;
+  int pf = 0, pc = 0, nchp = 0, p = -1;      // forward: the parent's (or own backward) range
+  int ch0 = 0, nchl = 0, cf = 0, cc = 0;     // backward: children (lane q: child q)
+  if (ph == 0) {
+    p = a.parent[s];
+    const int ps = p >= 0 ? p : n_sn + s;
+    pf = a.item_first[ps];
+    pc = a.item_cnt[ps];
+    if (p >= 0) nchp = a.nch[p];
+  } else {
+    ch0 = a.chptr[s];
+    nchl = a.chptr[s + 1] - ch0;
+    if (lane < nchl) {
+      const int ch = a.chidx[ch0 + lane];
+      cf = a.item_first[n_sn + ch];
+      cc = a.item_cnt[n_sn + ch];
+    }
+  }
   int act = 0;   // 0 nothing, 1 phase complete (forward: 2 parent ready, 3 root)
   if (lane == 0) {
     __threadfence();
@@ -102,10 +98,9 @@ __device__ __forceinline__ void complete_block(const SolveDev& a, int ph, int s,
       __threadfence();
       act = 1;
       if (ph == 0) {
-        const int p = a.parent[s];
         if (p < 0) {
           act = 3;
-        } else if (a.nch[p] == 1 || atomicAdd(a.done_ch + p, 1) == a.nch[p] - 1) {
+        } else if (nchp == 1 || atomicAdd(a.done_ch + p, 1) == nchp - 1) {
           __threadfence();
           act = 2;
         }
@@ -115,10 +110,29 @@ __device__ __forceinline__ void complete_block(const SolveDev& a, int ph, int s,
   act = __shfl_sync(0xffffffffu, act, 0);
   if (!act) return;
   if (ph == 0) {
-    if (act == 3) push_phase(a, 1, s, lane);
-    else if (act == 2) push_phase(a, 0, a.parent[s], lane);
-  } else {
-    for (int q = a.chptr[s]; q < a.chptr[s + 1]; ++q) push_phase(a, 1, a.chidx[q], lane);
+    if (act >= 2) push_items(a, pf, pc, lane);   // parent forward (2) or own backward (3)
+    return;
+  }
+  for (int base = 0; base < nchl; base += 32) {
+    if (base > 0) {   // more than 32 children (not produced by the bisection ordering)
+      cf = cc = 0;
+      if (base + lane < nchl) {
+        const int ch = a.chidx[ch0 + base + lane];
+        cf = a.item_first[n_sn + ch];
+        cc = a.item_cnt[n_sn + ch];
+      }
+    }
+    int incl = cc;   // inclusive scan of the children's item counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    int slot = 0;
+    if (lane == 0 && total) slot = atomicAdd(a.tail, total);
+    slot = __shfl_sync(0xffffffffu, slot, 0) + incl - cc;
+    for (int k = 0; k < cc; ++k) st_relaxed(a.ready + slot + k, cf + k + 1);
   }
 }
 
@@ -350,6 +364,13 @@ __global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTA
       for (int i = tid; i < rr; i += NTC) vs[i] = __ldcg(a.x + a.R[m.roff + m.r0 + i]);
       if (tid == 0 && rr < m.nr && rr >= 0) vs[rr] = 0.0;   // padding row
     }
+    // backward, single-tile group: q of the output column warp + lane * NWC, loaded now (off
+    // the path after the contraction); lane k of the warp emits its k-th column
+    double qpre = 0.0;
+    if (!fwd && m.ntb == 1) {
+      const int j = m.c0 + warp + lane * NWC;
+      if (warp + lane * NWC < m.nc && j < m.w) qpre = __ldcg(a.q + m.dof0 + j);
+    }
     // forward: the children's contributions to the update rows this thread will emit (rows
     // r0 + tid + k NTC), gathered now so they overlap the panel copy instead of following it
     constexpr int NCR = 4;
@@ -362,7 +383,9 @@ __global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTA
         crv[k] = child_sum(a, go + m.w + (i - m.wp));
       }
     }
+#ifndef SC_TRACE_COMPUTED
     if (a.trace && tid == 0) a.trace[5 * (size_t)it + 2] = gtimer();
+#endif
     while (!mbar_try(&bar, phase)) {
     }
     phase ^= 1;
@@ -424,7 +447,7 @@ __global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTA
     } else {
       // outputs: nc columns of G_s, warp w handles columns w, w + NWC, ...; lanes stride rows
       const int nr = m.nr;
-      for (int cc = warp; cc < m.nc; cc += NWC) {
+      for (int cc = warp, k = 0; cc < m.nc; cc += NWC, ++k) {
         double v0 = 0.0, v1 = 0.0;
         int i = lane;
         for (; i + 32 < nr; i += 64) {
@@ -435,9 +458,10 @@ __global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTA
         double v = v0 + v1;
 #pragma unroll
         for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) {
-          if (m.ntb == 1) emit_b(m.c0 + cc, v);
-          else P[m.t * 32 + cc] = v;
+        if (m.ntb == 1) {
+          if (lane == k && m.c0 + cc < m.w) a.x[m.dof0 + m.c0 + cc] = qpre - v;
+        } else if (lane == 0) {
+          P[m.t * 32 + cc] = v;
         }
       }
       named_arrive(BAR_FREE, NTX);
@@ -471,6 +495,9 @@ __global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTA
     if (pb) named_sync(BAR_CONS + 1, NTX);
     else named_sync(BAR_CONS, NTX);
     if (tid == 0) s_pub[pb] = make_int4(it, m.type, m.s, last ? 1 : 0);
+#ifdef SC_TRACE_COMPUTED
+    if (a.trace && tid == 0) a.trace[5 * (size_t)it + 2] = gtimer();   // experiment: compute done
+#endif
     if (pb) named_arrive(BAR_DONE + 1, NTX);
     else named_arrive(BAR_DONE, NTX);
   }

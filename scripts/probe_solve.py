@@ -42,6 +42,15 @@ def analyse(path):
            "fused_work_us_mean": float((tr[fused, 2] - tr[fused, 1]).mean() / 1e3) if fused.any() else None,
            "tiled_work_us_mean": float((tr[~fused, 2] - tr[~fused, 1]).mean() / 1e3) if (~fused).any() else None,
            "wait_us_mean": float((tr[:, 1] - tr[:, 0]).mean() / 1e3)}
+    # stage medians per (phase, single-tile) group
+    groups = {}
+    for p_ in (0, 1):
+        for fz in (True, False):
+            m = (ph == p_) & (fused == fz)
+            if m.any():
+                groups[("F" if p_ == 0 else "B") + ("-fused" if fz else "-tiled")] = [
+                    int(m.sum())] + [round(float(np.median(d[m, i])), 2) for i in range(4)]
+    out["stage_median_by_group"] = groups
     levels = []
     H = int(height.max()) + 1
     for p_ in (0, 1):
