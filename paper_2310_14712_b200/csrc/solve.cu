@@ -25,7 +25,7 @@
 // Small supernodes (whole panel <= one staging buffer) are one item per phase.
 // Progress: a slot is only awaited by a CTA that holds no item; if every CTA waits, every
 // pushed item is finished and its completion pushed its dependents, so the queue advances
-// until all n_items slots are filled.  Publication: results, __threadfence, counter atomics
+// until all n_items slots are filled.  Publication: results, fence.acq_rel, counter atomics
 // (release); the pusher fences after observing the final count and then stores the slots
 // (fence + relaxed store = release); the consumer acquire-loads the slot.
 #include <cstdlib>
@@ -51,6 +51,10 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+
+// release / acquire fence at GPU scope (fence.acq_rel: the publication patterns here are
+// release -> relaxed RMW/store and relaxed RMW -> acquire; no SC fence is needed)
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 __device__ __forceinline__ void st_relaxed(int* p, int v) {
   asm volatile("st.relaxed.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
@@ -89,19 +93,27 @@ __device__ __forceinline__ void complete_block(const SolveDev& a, int ph, int s,
       cc = a.item_cnt[n_sn + ch];
     }
   }
+  const int nb = a.nblk[ph * n_sn + s];
   int act = 0;   // 0 nothing, 1 phase complete (forward: 2 parent ready, 3 root)
   if (lane == 0) {
-    __threadfence();
-    // a single-block phase / a single child needs no counter: this block completes it
-    const int nb = a.nblk[ph * n_sn + s];
-    if (nb == 1 || atomicAdd(a.cnt + ph * n_sn + s, 1) == nb - 1) {
-      __threadfence();
+    fence_acq_rel();   // release: the compute warps' results (ordered before DONE)
+    // a single-block phase / a single child needs no counter: this block completes it.  After
+    // an observed counter, one fence acquires the other blocks' results and releases them to
+    // the next counter / the pushed slots.
+    bool done = true;
+    if (nb > 1) {
+      done = atomicAdd(a.cnt + ph * n_sn + s, 1) == nb - 1;
+      if (done) fence_acq_rel();
+    }
+    if (done) {
       act = 1;
       if (ph == 0) {
         if (p < 0) {
           act = 3;
-        } else if (nchp == 1 || atomicAdd(a.done_ch + p, 1) == nchp - 1) {
-          __threadfence();
+        } else if (nchp == 1) {
+          act = 2;
+        } else if (atomicAdd(a.done_ch + p, 1) == nchp - 1) {
+          fence_acq_rel();
           act = 2;
         }
       }
@@ -246,6 +258,10 @@ __device__ __forceinline__ void stage_item(const SolveDev& a, const Item& m, dou
   __syncwarp();
   if (nr == 0) return;
   const size_t row0 = (m.type == IT_F) ? (size_t)m.r0 : (size_t)m.wp + m.r0;
+  if (row0 == 0 && nr == m.ld) {   // whole columns: the tile is one contiguous range
+    if (lane == 0) bulk_g2s(st, Ap + (size_t)m.c0 * m.ld, (unsigned)(m.nc * nr * 8), bar);
+    return;
+  }
   for (int j = lane; j < m.nc; j += 32)
     bulk_g2s(st + j * nr, Ap + (size_t)(m.c0 + j) * m.ld + row0, nr * 8, bar);
 }
@@ -289,32 +305,67 @@ __global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTA
   extern __shared__ __align__(128) double stg[];   // c->solve_stage doubles (factor.cpp)
   __shared__ double vs[VS];
   double* red = vs + SOLVE_TILE;   // forward reductions (the gathered vector has <= SOLVE_TILE entries)
-  __shared__ __align__(8) uint64_t bar;
-  __shared__ int s_it[2], s_tk;
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ int s_it[2], s_tk, s_off[2];
   __shared__ int4 s_desc[2][5];
   __shared__ int4 s_pub[2];   // completion records: item, type, supernode, last block
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) mbar_init(&bar);
+  if (tid == 0) {
+    mbar_init(&bar[0]);
+    mbar_init(&bar[1]);
+  }
   __syncthreads();
   if (warp == NWC) {
     // ---------------- claimer warp ----------------
-    int buf = 0;
+    // Item k is staged at offset s_off[k & 1] of the staging buffer and completes on mbarrier
+    // bar[k & 1].  In the throughput regime the next item is claimed while item k is
+    // contracted, and its copy is issued at once if it fits beside item k (after it, or before
+    // it from offset 0); otherwise after FREE (item k contracted).  Each iteration consumes
+    // exactly one FREE (item k's) before READY(k+1), so READY runs at most one item ahead of
+    // the compute warps and only item k can be live in the buffer.
+    const int STG = a.stage;
+    int buf = 0, off = 0, size = 0;
     int it = claim(a, s_desc[0], &s_it[0], lane);
-    if (it >= 0) stage_item(a, load_item(s_desc[0]), stg, &bar, lane);
+    if (it >= 0) {
+      const Item m0 = load_item(s_desc[0]);
+      size = m0.nc * m0.nr;
+      if (lane == 0) s_off[0] = 0;
+      stage_item(a, m0, stg, &bar[0], lane);
+    }
     named_arrive(BAR_READY, NTX);
     while (it >= 0) {
+      const int nb = buf ^ 1;
       // claim ahead when the queue backlog exceeds one item per CTA; otherwise only once the
       // compute warps are free, so a latency-bound solve never parks a ready item behind a
       // busy CTA
       int ahead = 0;
       if (lane == 0) ahead = a.n_init + ld_relaxed(a.tail) > ld_relaxed(a.head) + (int)gridDim.x;
-      int nx = -2;
-      if (__shfl_sync(0xffffffffu, ahead, 0)) nx = claim(a, s_desc[buf ^ 1], &s_it[buf ^ 1], lane);
-      named_sync(BAR_FREE, NTX);   // the staging buffer is consumed
-      if (nx == -2) nx = claim(a, s_desc[buf ^ 1], &s_it[buf ^ 1], lane);
-      if (nx >= 0) stage_item(a, load_item(s_desc[buf ^ 1]), stg, &bar, lane);
+      bool freed = false;
+      if (!__shfl_sync(0xffffffffu, ahead, 0)) {
+        named_sync(BAR_FREE, NTX);
+        freed = true;
+      }
+      const int nx = claim(a, s_desc[nb], &s_it[nb], lane);
+      if (nx >= 0) {
+        const Item mn = load_item(s_desc[nb]);
+        const int nsize = mn.nc * mn.nr;
+        int noff = 0;
+        if (!freed) {
+          if (off + size + nsize <= STG) {
+            noff = off + size;
+          } else if (nsize > off) {   // fits nowhere beside item k: wait until it is contracted
+            named_sync(BAR_FREE, NTX);
+            freed = true;
+          }
+        }
+        if (lane == 0) s_off[nb] = noff;
+        stage_item(a, mn, stg + noff, &bar[nb], lane);
+        off = noff;
+        size = nsize;
+      }
+      if (!freed) named_sync(BAR_FREE, NTX);
       named_arrive(BAR_READY, NTX);
-      buf ^= 1;
+      buf = nb;
       it = nx;
     }
     return;
@@ -336,7 +387,7 @@ __global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTA
     }
   }
   // ---------------- compute warps (tid < NTC) ----------------
-  unsigned phase = 0;
+  unsigned phase = 0;   // mbarrier parity per item parity (bit b)
   for (int buf = 0, pb = 0;; buf ^= 1, pb ^= 1) {
     named_sync(BAR_READY, NTX);
     const int it = s_it[buf];
@@ -349,6 +400,7 @@ __global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTA
       return;
     }
     const Item m = load_item(s_desc[buf]);
+    const double* stg_b = stg + s_off[buf];
     const bool fwd = (m.type == IT_F);
     const int go = m.goff;
     // gather the input vector while the panel copy is in flight (every producer of it
@@ -386,9 +438,9 @@ __global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTA
 #ifndef SC_TRACE_COMPUTED
     if (a.trace && tid == 0) a.trace[5 * (size_t)it + 2] = gtimer();
 #endif
-    while (!mbar_try(&bar, phase)) {
+    while (!mbar_try(&bar[buf], (phase >> buf) & 1)) {
     }
-    phase ^= 1;
+    phase ^= 1u << buf;
     if (a.trace && tid == 0) a.trace[5 * (size_t)it + 3] = gtimer();
     named_sync(BAR_CB, NTC);   // vs complete
     // panel row i (= r0 + tid + kq NTC) of the forward phase -> q_s or U_s
@@ -420,10 +472,10 @@ __global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTA
           double a0 = 0.0, a1 = 0.0;
           int j = 0;
           for (; j + 1 < nc; j += 2) {
-            a0 += stg[j * nr + i] * vs[j];
-            a1 += stg[(j + 1) * nr + i] * vs[j + 1];
+            a0 += stg_b[j * nr + i] * vs[j];
+            a1 += stg_b[(j + 1) * nr + i] * vs[j + 1];
           }
-          if (j < nc) a0 += stg[j * nr + i] * vs[j];
+          if (j < nc) a0 += stg_b[j * nr + i] * vs[j];
           if (m.ntb == 1) emit_f(m.r0 + i, a0 + a1, (i - tid) / NTC);
           else P[m.t * nr + i] = a0 + a1;
         }
@@ -433,7 +485,7 @@ __global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTA
         const int i = tid % nr, g = tid / nr;
         double acc = 0.0;
         if (g < G)
-          for (int j = g; j < nc; j += G) acc += stg[j * nr + i] * vs[j];
+          for (int j = g; j < nc; j += G) acc += stg_b[j * nr + i] * vs[j];
         red[tid] = acc;
         named_arrive(BAR_FREE, NTX);
         named_sync(BAR_CB, NTC);
@@ -451,10 +503,10 @@ __global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTA
         double v0 = 0.0, v1 = 0.0;
         int i = lane;
         for (; i + 32 < nr; i += 64) {
-          v0 += stg[cc * nr + i] * vs[i];
-          v1 += stg[cc * nr + i + 32] * vs[i + 32];
+          v0 += stg_b[cc * nr + i] * vs[i];
+          v1 += stg_b[cc * nr + i + 32] * vs[i + 32];
         }
-        if (i < nr) v0 += stg[cc * nr + i] * vs[i];
+        if (i < nr) v0 += stg_b[cc * nr + i] * vs[i];
         double v = v0 + v1;
 #pragma unroll
         for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -473,9 +525,9 @@ __global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTA
       // (acquire of the other tiles' partials)
       named_sync(BAR_CB, NTC);
       if (tid == 0) {
-        __threadfence();
+        fence_acq_rel();
         s_tk = (atomicAdd(a.bcnt + m.bctr, 1) == m.ntb - 1);
-        if (s_tk) __threadfence();
+        if (s_tk) fence_acq_rel();
       }
       named_sync(BAR_CB, NTC);
       last = s_tk;
