@@ -35,9 +35,17 @@
 namespace {
 
 enum { IT_F = 0, IT_B = 1 };
+// SC_TRACE_COMPUTE (experiment builds): the trace records the compute warps' chain instead —
+// [READY passed, gathered, staged, contracted, record slot free]
+#ifdef SC_TRACE_COMPUTE
+#define TRC(k) if (a.trace && tid == 0) a.trace[5 * (size_t)it + (k)] = gtimer()
+#else
+#define TRC(k)
+#endif
 constexpr int NT = SOLVE_NT;          // threads per CTA
 constexpr int NWC = NT / 32 - 2;      // compute warps (then the claimer and publisher warps)
 constexpr int NTC = NWC * 32;
+static_assert(NWC * 8 >= 32, "backward tiles: <= 32 columns, <= 8 per compute warp");
 constexpr int VS = SOLVE_BROWS > SOLVE_TILE + NTC ? SOLVE_BROWS : SOLVE_TILE + NTC;   // gathered vector
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -289,7 +297,11 @@ __device__ __forceinline__ int claim(const SolveDev& a, int4* dst, int* s_it, in
     it = slot_item(a, atomicAdd(a.head, 1));
     if (it >= 0) fetch_desc(a, it, dst);
     *s_it = it;
+#ifdef SC_TRACE_COMPUTE
+    if (false) {
+#else
     if (a.trace && it >= 0) {
+#endif
       a.trace[5 * (size_t)it] = t0;
       a.trace[5 * (size_t)it + 1] = gtimer();
     }
@@ -383,7 +395,9 @@ __global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTA
       if (r.x < 0) return;
       // the compute warps' result stores precede DONE; lane 0's fence is cumulative over them
       if (r.w) complete_block(a, r.y == IT_F ? 0 : 1, r.z, lane);
+#ifndef SC_TRACE_COMPUTE
       if (a.trace && lane == 0) a.trace[5 * (size_t)r.x + 4] = gtimer();
+#endif
     }
   }
   // ---------------- compute warps (tid < NTC) ----------------
@@ -400,6 +414,7 @@ __global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTA
       return;
     }
     const Item m = load_item(s_desc[buf]);
+    TRC(0);
     const double* stg_b = stg + s_off[buf];
     const bool fwd = (m.type == IT_F);
     const int go = m.goff;
@@ -416,12 +431,12 @@ __global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTA
       for (int i = tid; i < rr; i += NTC) vs[i] = __ldcg(a.x + a.R[m.roff + m.r0 + i]);
       if (tid == 0 && rr < m.nr && rr >= 0) vs[rr] = 0.0;   // padding row
     }
-    // backward, single-tile group: q of the output column warp + lane * NWC, loaded now (off
-    // the path after the contraction); lane k of the warp emits its k-th column
+    // backward, single-tile group: q of the output column of lanes 4k (column warp + k NWC),
+    // loaded now (off the path after the contraction); those lanes emit
     double qpre = 0.0;
-    if (!fwd && m.ntb == 1) {
-      const int j = m.c0 + warp + lane * NWC;
-      if (warp + lane * NWC < m.nc && j < m.w) qpre = __ldcg(a.q + m.dof0 + j);
+    if (!fwd && m.ntb == 1 && (lane & 3) == 0) {
+      const int cc = warp + (lane >> 2) * NWC;
+      if (cc < m.nc && m.c0 + cc < m.w) qpre = __ldcg(a.q + m.dof0 + m.c0 + cc);
     }
     // forward: the children's contributions to the update rows this thread will emit (rows
     // r0 + tid + k NTC), gathered now so they overlap the panel copy instead of following it
@@ -435,13 +450,17 @@ __global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTA
         crv[k] = child_sum(a, go + m.w + (i - m.wp));
       }
     }
-#ifndef SC_TRACE_COMPUTED
+#if !defined(SC_TRACE_COMPUTED) && !defined(SC_TRACE_COMPUTE)
     if (a.trace && tid == 0) a.trace[5 * (size_t)it + 2] = gtimer();
 #endif
+    TRC(1);
     while (!mbar_try(&bar[buf], (phase >> buf) & 1)) {
     }
     phase ^= 1u << buf;
+#ifndef SC_TRACE_COMPUTE
     if (a.trace && tid == 0) a.trace[5 * (size_t)it + 3] = gtimer();
+#endif
+    TRC(2);
     named_sync(BAR_CB, NTC);   // vs complete
     // panel row i (= r0 + tid + kq NTC) of the forward phase -> q_s or U_s
     auto emit_f = [&](int i, double v, int kq) {
@@ -469,24 +488,35 @@ __global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTA
       const int nr = m.nr, nc = m.nc;
       if (nr >= NTC) {
         for (int i = tid; i < nr; i += NTC) {
-          double a0 = 0.0, a1 = 0.0;
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;   // 4 independent chains
           int j = 0;
-          for (; j + 1 < nc; j += 2) {
+          for (; j + 3 < nc; j += 4) {
             a0 += stg_b[j * nr + i] * vs[j];
             a1 += stg_b[(j + 1) * nr + i] * vs[j + 1];
+            a2 += stg_b[(j + 2) * nr + i] * vs[j + 2];
+            a3 += stg_b[(j + 3) * nr + i] * vs[j + 3];
           }
-          if (j < nc) a0 += stg_b[j * nr + i] * vs[j];
-          if (m.ntb == 1) emit_f(m.r0 + i, a0 + a1, (i - tid) / NTC);
-          else P[m.t * nr + i] = a0 + a1;
+          for (; j < nc; ++j) a0 += stg_b[j * nr + i] * vs[j];
+          const double v = (a0 + a1) + (a2 + a3);
+          if (m.ntb == 1) emit_f(m.r0 + i, v, (i - tid) / NTC);
+          else P[m.t * nr + i] = v;
         }
         named_arrive(BAR_FREE, NTX);
       } else {
         const int G = NTC / nr;   // nr >= 2
         const int i = tid % nr, g = tid / nr;
-        double acc = 0.0;
-        if (g < G)
-          for (int j = g; j < nc; j += G) acc += stg_b[j * nr + i] * vs[j];
-        red[tid] = acc;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;   // 4 independent chains
+        if (g < G) {
+          int j = g;
+          for (; j + 3 * G < nc; j += 4 * G) {
+            a0 += stg_b[j * nr + i] * vs[j];
+            a1 += stg_b[(j + G) * nr + i] * vs[j + G];
+            a2 += stg_b[(j + 2 * G) * nr + i] * vs[j + 2 * G];
+            a3 += stg_b[(j + 3 * G) * nr + i] * vs[j + 3 * G];
+          }
+          for (; j < nc; j += G) a0 += stg_b[j * nr + i] * vs[j];
+        }
+        red[tid] = (a0 + a1) + (a2 + a3);
         named_arrive(BAR_FREE, NTX);
         named_sync(BAR_CB, NTC);
         if (tid < nr) {
@@ -497,27 +527,43 @@ __global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTA
         }
       }
     } else {
-      // outputs: nc columns of G_s, warp w handles columns w, w + NWC, ...; lanes stride rows
+      // outputs: nc <= 32 columns of G_s; warp w handles columns w + k NWC (k < 8) all at once
+      // (one vs load per row, 8 independent chains), lanes stride rows; a transposing
+      // butterfly (9 shuffles) leaves column k's sum in lanes 4k .. 4k+3
       const int nr = m.nr;
-      for (int cc = warp, k = 0; cc < m.nc; cc += NWC, ++k) {
-        double v0 = 0.0, v1 = 0.0;
-        int i = lane;
-        for (; i + 32 < nr; i += 64) {
-          v0 += stg_b[cc * nr + i] * vs[i];
-          v1 += stg_b[cc * nr + i + 32] * vs[i + 32];
-        }
-        if (i < nr) v0 += stg_b[cc * nr + i] * vs[i];
-        double v = v0 + v1;
+      double acc[8];
 #pragma unroll
-        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      for (int k = 0; k < 8; ++k) acc[k] = 0.0;
+      for (int i = lane; i < nr; i += 32) {
+        const double v = vs[i];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int cc = warp + k * NWC;
+          if (cc < m.nc) acc[k] += stg_b[cc * nr + i] * v;
+        }
+      }
+      const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+      double r4[4], r2[2];
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        r4[t] = (h16 ? acc[t + 4] : acc[t]) + __shfl_xor_sync(0xffffffffu, h16 ? acc[t] : acc[t + 4], 16);
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+        r2[t] = (h8 ? r4[t + 2] : r4[t]) + __shfl_xor_sync(0xffffffffu, h8 ? r4[t] : r4[t + 2], 8);
+      double v = (h4 ? r2[1] : r2[0]) + __shfl_xor_sync(0xffffffffu, h4 ? r2[0] : r2[1], 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      const int cc = warp + (lane >> 2) * NWC;   // this lane's column (lanes 4k .. 4k+3: column k)
+      if ((lane & 3) == 0 && cc < m.nc) {
         if (m.ntb == 1) {
-          if (lane == k && m.c0 + cc < m.w) a.x[m.dof0 + m.c0 + cc] = qpre - v;
-        } else if (lane == 0) {
+          if (m.c0 + cc < m.w) a.x[m.dof0 + m.c0 + cc] = qpre - v;
+        } else {
           P[m.t * 32 + cc] = v;
         }
       }
       named_arrive(BAR_FREE, NTX);
     }
+    TRC(3);
     if (m.ntb > 1) {
       // partials of this tile written; the last tile of the group sums them in tile order.
       // One thread fences after the barrier (cumulative release of the compute warps' stores)
@@ -546,6 +592,7 @@ __global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTA
     // result stores ordered before DONE); wait until the record slot is free
     if (pb) named_sync(BAR_CONS + 1, NTX);
     else named_sync(BAR_CONS, NTX);
+    TRC(4);
     if (tid == 0) s_pub[pb] = make_int4(it, m.type, m.s, last ? 1 : 0);
 #ifdef SC_TRACE_COMPUTED
     if (a.trace && tid == 0) a.trace[5 * (size_t)it + 2] = gtimer();   // experiment: compute done
