@@ -19,9 +19,10 @@
 // holding an item, all resident CTAs work.  Per item: take the next queue slot, stream the
 // item's panel tile into shared memory with bulk (TMA) copies completing on an mbarrier,
 // gather the produced vector entries meanwhile, contract, publish.
-// Tiles: forward 32 panel rows x SOLVE_TILE columns, backward 32 outputs x SOLVE_TILE rows.  A
-// block whose reduction spans several tiles writes per-tile partials; the LAST tile (atomic
-// ticket) sums them in fixed tile order -> deterministic results regardless of the schedule.
+// Tiles: forward 32*2^k panel rows x <= SOLVE_TILE columns, backward <= 32 outputs x <=
+// SOLVE_BROWS rows.  A block whose reduction spans several tiles writes per-tile partials; the
+// publisher of the LAST tile (atomic ticket) sums them in fixed tile order -> deterministic
+// results regardless of the schedule.
 // Small supernodes (whole panel <= one staging buffer) are one item per phase.
 // Progress: a slot is only awaited by a CTA that holds no item; if every CTA waits, every
 // pushed item is finished and its completion pushed its dependents, so the queue advances
@@ -309,6 +310,50 @@ __device__ __forceinline__ int claim(const SolveDev& a, int4* dst, int* s_it, in
   return __shfl_sync(0xffffffffu, it, 0);
 }
 
+// publisher warp, record of a tile of a multi-tile group (its partials written and ordered
+// before DONE): draw the group's ticket; the LAST tile's publisher sums the ntb partials in
+// tile order (deterministic) and emits the group's outputs — forward: q_s rows / U_s rows
+// (+ the children's update entries), backward: x_s = q_s - G_s^T x_R.  Returns whether this
+// tile completed its group (the caller then publishes the block).
+__device__ __forceinline__ bool tile_ticket(const SolveDev& a, int it, int lane) {
+  int4 d[5];
+  const int4* src = a.items + 5 * (size_t)it;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) d[k] = src[k];
+  const Item m = load_item(d);
+  int last = 0;
+  if (lane == 0) {
+    fence_acq_rel();   // release this tile's partials
+    last = atomicAdd(a.bcnt + m.bctr, 1) == m.ntb - 1;
+    if (last) fence_acq_rel();   // acquire the other tiles' partials
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return false;
+  const double* P = a.part + m.pslot;
+  if (m.type == IT_F) {
+    for (int o = lane; o < m.nr; o += 32) {
+      double v = 0.0;
+      for (int k = 0; k < m.ntb; ++k) v += __ldcg(P + k * m.nr + o);
+      const int i = m.r0 + o;
+      if (i < m.w) {
+        a.q[m.dof0 + i] = v;
+      } else if (i >= m.wp && i < m.wp + m.r) {
+        const int k = i - m.wp;
+        a.U[m.uoff + k] = v + child_sum(a, m.goff + m.w + k);
+      }
+    }
+  } else {
+    for (int o = lane; o < m.nc; o += 32) {
+      double v = 0.0;
+      for (int k = 0; k < m.ntb; ++k) v += __ldcg(P + k * 32 + o);
+      const int j = m.c0 + o;
+      if (j < m.w) a.x[m.dof0 + j] = __ldcg(a.q + m.dof0 + j) - v;
+    }
+  }
+  __syncwarp();   // the lanes' emits precede lane 0's releasing fence in complete_block
+  return true;
+}
+
 // Warp-specialised persistent CTA: NWC compute warps gather and contract the staged tiles; a
 // claimer warp takes items from the queue and issues their panel copies; a publisher warp
 // publishes completions.  The three chains (claim latency, contraction, publication fences and
@@ -318,9 +363,9 @@ __global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTA
   __shared__ double vs[VS];
   double* red = vs + SOLVE_TILE;   // forward reductions (the gathered vector has <= SOLVE_TILE entries)
   __shared__ __align__(8) uint64_t bar[2];
-  __shared__ int s_it[2], s_tk, s_off[2];
+  __shared__ int s_it[2], s_off[2];
   __shared__ int4 s_desc[2][5];
-  __shared__ int4 s_pub[2];   // completion records: item, type, supernode, last block
+  __shared__ int4 s_pub[2];   // completion records: item, type, supernode, 1 single tile / 2 tile of a group
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
     mbar_init(&bar[0]);
@@ -394,7 +439,8 @@ __global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTA
       else named_arrive(BAR_CONS, NTX);
       if (r.x < 0) return;
       // the compute warps' result stores precede DONE; lane 0's fence is cumulative over them
-      if (r.w) complete_block(a, r.y == IT_F ? 0 : 1, r.z, lane);
+      if (r.w == 2 && !tile_ticket(a, r.x, lane)) continue;   // a tile of a group, not the last
+      complete_block(a, r.y == IT_F ? 0 : 1, r.z, lane);
 #ifndef SC_TRACE_COMPUTE
       if (a.trace && lane == 0) a.trace[5 * (size_t)r.x + 4] = gtimer();
 #endif
@@ -478,11 +524,7 @@ __global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTA
         a.U[m.uoff + k] = v;
       }
     };
-    auto emit_b = [&](int j, double v) {   // j: G column (output) index
-      if (j < m.w) a.x[m.dof0 + j] = __ldcg(a.q + m.dof0 + j) - v;
-    };
     double* P = a.part + m.pslot;
-    bool last = true;
     if (fwd) {
       // rows i of the tile: nr rows, nc columns; G threads per row when nr < NTC
       const int nr = m.nr, nc = m.nc;
@@ -564,36 +606,12 @@ __global__ void __launch_bounds__(NT, SOLVE_MINB) k_solve(SolveDev a) {   // CTA
       named_arrive(BAR_FREE, NTX);
     }
     TRC(3);
-    if (m.ntb > 1) {
-      // partials of this tile written; the last tile of the group sums them in tile order.
-      // One thread fences after the barrier (cumulative release of the compute warps' stores)
-      // and, when it draws the last ticket, again before the barrier that releases the readers
-      // (acquire of the other tiles' partials)
-      named_sync(BAR_CB, NTC);
-      if (tid == 0) {
-        fence_acq_rel();
-        s_tk = (atomicAdd(a.bcnt + m.bctr, 1) == m.ntb - 1);
-        if (s_tk) fence_acq_rel();
-      }
-      named_sync(BAR_CB, NTC);
-      last = s_tk;
-      if (last) {
-        const int outs = fwd ? m.nr : m.nc;
-        const int stride = fwd ? m.nr : 32;
-        for (int o = tid; o < outs; o += NTC) {
-          double v = 0.0;
-          for (int k = 0; k < m.ntb; ++k) v += __ldcg(P + k * stride + o);
-          if (fwd) emit_f(m.r0 + o, v, (o - tid) / NTC);
-          else emit_b(m.c0 + o, v);
-        }
-      }
-    }
     // completion record for the publisher (its fence is cumulative over the compute warps'
     // result stores ordered before DONE); wait until the record slot is free
     if (pb) named_sync(BAR_CONS + 1, NTX);
     else named_sync(BAR_CONS, NTX);
     TRC(4);
-    if (tid == 0) s_pub[pb] = make_int4(it, m.type, m.s, last ? 1 : 0);
+    if (tid == 0) s_pub[pb] = make_int4(it, m.type, m.s, m.ntb > 1 ? 2 : 1);
 #ifdef SC_TRACE_COMPUTED
     if (a.trace && tid == 0) a.trace[5 * (size_t)it + 2] = gtimer();   // experiment: compute done
 #endif
