@@ -14,6 +14,11 @@ Restated from BASELINE.json ``configs`` with the readings of DESIGN.md §3
 5. 3D, 160^3 cells, p=4, 200 seeded ellipsoids (semi-axes U[0.01,0.03]),
    D=2, alpha=1e-6, Ricker f0=15 at (0.1,0.5,0.5) (C14), 1000 steps.
 
+Config 6 is NOT a BASELINE config: the high-cut-fraction stress case of SURVEY NEXT-1(1b)
+(the paper's pillar has 51% cut DOFs; configs 2-5 have 1-4%): 2D, 128^2 cells, p=4,
+400 seeded ellipses (semi-axes U[0.006,0.015]) -> 31% c DOFs, D=3, alpha=1e-6, Ricker f0=20
+at (0, 0.5), 5000 steps.
+
 rho = c = 1 (C10); homogeneous Neumann on the box; lattice_s = 4 (C6);
 fill_eps = 1e-10.  dt = 0.9 x the uncut cell-wise critical step
 (C12), written here as full-precision literals produced by
@@ -25,11 +30,11 @@ import numpy as np
 from .voids import generate_voids
 from .signals import ricker_series
 
-CONFIG_IDS = (1, 2, 3, 4, 5)
+CONFIG_IDS = (1, 2, 3, 4, 5)   # BASELINE configs; 6 = NEXT-1(1b) stress case
 
 # dt literals (reading C12): 0.9 * Delta t_crit^uncut (scripts/gen_dt_literals.py).
 _DT = {1: 0.004154166182068483, 2: 0.0015247322583105771, 3: 0.0003811830645776443,
-       4: 0.002096313728906055, 5: 0.0004979754702963185}
+       4: 0.002096313728906055, 5: 0.0004979754702963185, 6: 0.0007623661291552886}
 
 
 def _base(cid, dim, n, p, alpha, depth, steps):
@@ -42,7 +47,7 @@ def _base(cid, dim, n, p, alpha, depth, steps):
 
 
 def get_config(cid, steps=None):
-    """Return the explicit input dict of BASELINE config ``cid`` (1..5)."""
+    """Return the explicit input dict of BASELINE config ``cid`` (1..5) or the stress case 6."""
     if cid == 1:
         cfg = _base(1, 1, 32, 4, 1e-5, 3, 2000)
         cfg["voids"] = [{"kind": "halfspace", "n": [1.0, 0.0, 0.0], "b": 0.937}]
@@ -72,6 +77,12 @@ def get_config(cid, steps=None):
         cfg["voids"] = generate_voids(5, 3, 200, 0.01, 0.03, "ellipsoid", 1.0 / 160, src)
         cfg["source"] = {"x": src, "f0": 15.0}
         cfg["name"] = "3D-ellipsoids-160^3xp4"
+    elif cid == 6:
+        cfg = _base(6, 2, 128, 4, 1e-6, 3, 5000)
+        src = [0.0, 0.5, 0.0]
+        cfg["voids"] = generate_voids(6, 2, 400, 0.006, 0.015, "ellipse", 1.0 / 128, src)
+        cfg["source"] = {"x": src, "f0": 20.0}
+        cfg["name"] = "2D-dense-voids-128x128xp4 (stress, 31% c DOFs)"
     else:
         raise ValueError(f"unknown config {cid}")
     if steps is not None:

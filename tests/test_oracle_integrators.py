@@ -212,7 +212,7 @@ def test_dalembert_and_p_convergence():
 def test_config_dt():
     """C12: each config's dt literal equals 0.9 x the oracle's uncut
     cell-wise critical step."""
-    spec = {1: (1, 4, 32), 2: (2, 4, 64), 3: (2, 4, 256), 4: (3, 3, 64), 5: (3, 4, 160)}
+    spec = {1: (1, 4, 32), 2: (2, 4, 64), 3: (2, 4, 256), 4: (3, 3, 64), 5: (3, 4, 160), 6: (2, 4, 128)}
     for cid, (d, p, n) in spec.items():
         dt = sc_inputs.get_config(cid)["dt"]
         ref = 0.9 * dt_crit_uncut(d, p, 1.0 / n)
