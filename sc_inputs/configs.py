@@ -28,7 +28,7 @@ fill_eps = 1e-10.  dt = 0.9 x the uncut cell-wise critical step
 import numpy as np
 
 from .voids import generate_voids
-from .signals import ricker_series
+from .signals import ricker_series, signal_series
 
 CONFIG_IDS = (1, 2, 3, 4, 5)   # BASELINE configs; 6 = NEXT-1(1b) stress case
 
@@ -111,7 +111,10 @@ def source_signal(cfg, n_values=None):
         return None
     if n_values is None:
         n_values = cfg["steps"] + 1
-    return ricker_series(cfg["source"]["f0"], cfg["dt"], n_values)
+    kind = cfg["source"].get("signal", "ricker")
+    if kind == "ricker":
+        return ricker_series(cfg["source"]["f0"], cfg["dt"], n_values)
+    return signal_series(kind, cfg["source"]["f0"], cfg["dt"], n_values)
 
 
 def describe(cfg):

@@ -49,3 +49,25 @@ def test_receiver_traces_match_oracle(pkg, dim, cells, p, recv):
     ref = np.array(ref)
     err = np.linalg.norm(tr - ref) / np.linalg.norm(ref)
     assert np.abs(ref).max() > 0 and err < 1e-10, err
+
+
+def test_paper_excitations_match_oracle(pkg):
+    """The paper's own temporal signals (Gaussian derivative; two-cycle sine burst,
+    P:1759-1764) through the same path: device state after 40 steps vs the oracle's IMEX."""
+    from oracle.run import run_config
+    for sig, f0 in (("gauss_deriv", 6.0), ("sine_burst", 12.0)):
+        steps = 40
+        cfg = sc_inputs.small_config(2, [10, 9], 3, depth=2, steps=steps,
+                                     voids=[{"kind": "ellipsoid", "c": [0.55, 0.45, 0.0],
+                                             "A": [40.0, 60.0, 0.0, 5.0, 0.0, 0.0]}],
+                                     source={"x": [0.25, 0.3, 0.3], "f0": f0, "signal": sig})
+        cfg["dt"] = 0.9 * dt_crit_uncut(2, 3, 1.0 / 10)
+        f_t = sc_inputs.source_signal(cfg, steps + 2)
+        assert np.abs(f_t).max() > 0
+        s = pkg.from_config(cfg, f_t=f_t)
+        s.step(steps)
+        u = s.read()
+        s.close()
+        ref, _ = run_config(cfg, sysm=build_system(cfg, "sparse"), f_t=f_t)
+        err = np.linalg.norm(u - ref) / np.linalg.norm(ref)
+        assert np.linalg.norm(ref) > 0 and err < 1e-10, (sig, err)
