@@ -189,7 +189,7 @@ void make_panel(const double* F, int n, int w, double* P) {
 static void nested_dissection(Builder& b, int comp, std::vector<int>& nodes, std::vector<int>& roots,
                               int& next_col, std::vector<int>& order_out) {
   const GridP& g = b.c->g;
-  static const int LEAF = getenv("SC_ND_LEAF") ? atoi(getenv("SC_ND_LEAF")) : 64;   // max nodes of an ND leaf
+  static const int LEAF = getenv("SC_ND_LEAF") ? atoi(getenv("SC_ND_LEAF")) : 32;   // max nodes of an ND leaf (r1_solve_variants.txt)
   std::function<void(std::vector<int>&, std::vector<int>&)> rec = [&](std::vector<int>& nd,
                                                                       std::vector<int>& out_roots) {
     if (nd.empty()) return;
