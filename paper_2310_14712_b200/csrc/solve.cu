@@ -24,9 +24,14 @@
 // publisher of the LAST tile (atomic ticket) sums them in fixed tile order -> deterministic
 // results regardless of the schedule.
 // Small supernodes (whole panel <= one staging buffer) are one item per phase.
-// Progress: a slot is only awaited by a CTA that holds no item; if every CTA waits, every
-// pushed item is finished and its completion pushed its dependents, so the queue advances
-// until all n_items slots are filled.  Publication: results, fence.acq_rel, counter atomics
+// CTA roles (warp specialisation, k_solve below): a claimer warp takes queue slots and issues
+// the panel copies, 4 compute warps gather / contract / emit, a publisher warp draws tile
+// tickets, sums partials and publishes completions (fences, counters, pushes).
+// Progress: a slot that may still be empty is only awaited by a CTA whose compute warps hold
+// no item (a CTA claims ahead of its current item only when the queue backlog exceeds one
+// item per CTA, so that slot is already pushed); if every CTA waits, every pushed item is
+// finished and its completion pushed its dependents, so the queue advances until all n_items
+// slots are filled.  Publication: results, fence.acq_rel, counter atomics
 // (release); the pusher fences after observing the final count and then stores the slots
 // (fence + relaxed store = release); the consumer acquire-loads the slot.
 #include <cstdlib>
