@@ -112,73 +112,101 @@ def sub_box(cfg, frac):
     return c
 
 
-def cpu_sample_cfg(cfg, frac=0.125):
+def cpu_sample_cfg(cfg, frac=0.0625):
     """Config 5 (2.6e8 DOFs) is out of the oracle's reach in minutes: sample the corner
-    sub-box of `frac` of the edge (default 1/8: 20^3 cells; same h, p, alpha, depth, dt,
-    voids meeting the box)."""
+    sub-box of `frac` of the edge (default 1/16: 10^3 cells; same h, p, alpha, depth, dt,
+    voids meeting the box).  The reference arm and cpu_baseline use the SAME sample."""
     if cfg["id"] == 5:
         n = int(round(cfg["cells"][0] * frac))
         return sub_box(cfg, frac), f"sub-box [0,{frac:g}]^3 ({n}^3 cells)"
     return cfg, "full size"
 
 
+ORACLE_THREADS = 1   # the oracle's time loop (scipy sparse matvec + SuperLU solves) is serial
+
+
 def oracle_sample(cfg, steps):
-    """Time the oracle's IMEX loop (as it stands) on `steps` steps of `cfg`."""
+    """Time the oracle's IMEX loop (as it stands) on `steps` steps of `cfg`, with the BLAS /
+    OpenMP pools limited to ORACLE_THREADS so that the reported core count is exact."""
     import oracle.assembly as OA
     from oracle.integrators import from_system, imex
     from oracle.run import initial_field
     n_dof_cells = np.prod(cfg["cells"]) * (cfg["p"] + 1) ** (2 * cfg["dim"])
     mode = "sparse" if n_dof_cells < 1.2e8 else "ebe"
-    t0 = time.perf_counter()
-    sysm = OA.build_system(cfg, mode)
-    t_setup = time.perf_counter() - t0
-    pr = from_system(sysm)
-    f_t = sc_inputs.source_signal(cfg, steps + 1)
-    u0 = initial_field(cfg, sysm)
-    t0 = time.perf_counter()
-    imex(pr, cfg["dt"], steps, f_t, u0, None)
-    t = time.perf_counter() - t0
+    try:
+        from threadpoolctl import threadpool_limits
+        lim = threadpool_limits(ORACLE_THREADS)
+    except Exception:
+        lim = None
+    try:
+        t0 = time.perf_counter()
+        sysm = OA.build_system(cfg, mode)
+        t_setup = time.perf_counter() - t0
+        pr = from_system(sysm)
+        f_t = sc_inputs.source_signal(cfg, steps + 1)
+        u0 = initial_field(cfg, sysm)
+        t0 = time.perf_counter()
+        imex(pr, cfg["dt"], steps, f_t, u0, None)
+        t = time.perf_counter() - t0
+    finally:
+        if lim is not None:
+            lim.restore_original_limits()
     return sysm.n_dof * steps / t, t, t_setup, sysm.n_dof, mode
 
 
-def _cores():
-    try:
-        import threadpoolctl
-        info = threadpoolctl.threadpool_info()
-        return max([i.get("num_threads", 1) for i in info] + [1])
-    except Exception:
-        return os.cpu_count() or 1
+def _cpu_line(args, steps):
+    cfg = sc_inputs.get_config(args.config)
+    scfg, what = cpu_sample_cfg(cfg)
+    value, t, t_setup, n_dof, mode = oracle_sample(scfg, steps)
+    sample = (f"config {args.config} {what} ({n_dof} DOFs, {mode} assembly), oracle IMEX time loop of "
+              f"{steps} steps ({t:.2f} s; setup {t_setup:.1f} s untimed), {ORACLE_THREADS} thread")
+    return {"value": value, "unit": UNIT, "cores": ORACLE_THREADS, "kind": "oracle", "sample": sample}, t
 
 
 def run_reference(args, rank):
     if rank != 0:
         return 0
     cfg = sc_inputs.get_config(args.config)
-    # bounded sample: the oracle's IMEX time loop (setup untimed), one oracle step per timed
-    # step on a sample sized so that the whole run stays within a few minutes (config 5: the
-    # corner 10^3-cell sub-box, ~0.2 s per oracle step on the host)
+    # bounded sample: the oracle's IMEX time loop (setup untimed), ref_steps oracle steps per
+    # timed step on the same sample as cpu_baseline (config 5: the corner 10^3-cell sub-box,
+    # ~0.04 s per oracle step), so that the whole run stays within a few minutes
     nsteps = max(1, args.steps) * max(1, args.ref_steps)
-    scfg, what = cpu_sample_cfg(cfg, 0.0625)
-    value, t, t_setup, n_dof, mode = oracle_sample(scfg, nsteps)
-    sample = (f"config {args.config} {what} ({n_dof} DOFs, {mode} assembly), oracle IMEX time loop of "
-              f"{nsteps} steps ({t:.1f} s; setup {t_setup:.1f} s untimed)")
+    cpu, t = _cpu_line(args, nsteps)
+    value = cpu["value"]
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / nsteps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": _config_dict(cfg, n_dof),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": _cores(), "kind": "oracle", "sample": sample},
+            "data": "synthetic", "config": _config_dict(cfg), "cpu_baseline": cpu,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def _config_dict(cfg, n_dof, extra=None):
-    d = {"workload": f"config{cfg['id']}: {cfg['name']}", "dim": cfg["dim"], "cells": cfg["cells"],
-         "p": cfg["p"], "n_voids": len(cfg["voids"]), "alpha": cfg["alpha"], "tree_depth": cfg["tree_depth"],
-         "dt": cfg["dt"], "n_dof": int(n_dof)}
-    if extra:
-        d.update(extra)
-    return d
+def _config_dict(cfg):
+    """The workload descriptor (identical for both arms; sizes found by the setup are reported
+    outside it, under "problem")."""
+    return {"workload": f"config{cfg['id']}: {cfg['name']}", "dim": cfg["dim"], "cells": cfg["cells"],
+            "p": cfg["p"], "n_voids": len(cfg["voids"]), "alpha": cfg["alpha"], "tree_depth": cfg["tree_depth"],
+            "dt": cfg["dt"], "steps_per_job": "--steps", "source": "Ricker point source" if cfg["source"] else "none",
+            "l2": "per-step working set larger than L2 (no flush)" if cfg["id"] in (4, 5) else
+                  "L2-resident working set (no flush)"}
+
+
+def _relaunch(args):
+    """--gpus N > 1 without a torchrun environment: launch N ranks (one per GPU) of this script
+    under torch.distributed.run on 127.0.0.1; rank 0 prints the line."""
+    import socket
+    import torch
+    if torch.cuda.device_count() < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but {torch.cuda.device_count()} CUDA devices visible"}),
+              flush=True)
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -189,7 +217,7 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-steps", type=int, default=1, help="oracle steps per timed step (reference arm)")
-    ap.add_argument("--cpu-steps", type=int, default=3, help="oracle steps for cpu_baseline")
+    ap.add_argument("--cpu-steps", type=int, default=300, help="oracle steps for cpu_baseline")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
@@ -197,6 +225,10 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, rank)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _relaunch(args)
+    if world != args.gpus:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
 
     import torch
     import torch.distributed as dist
@@ -285,48 +317,42 @@ def main():
     u0t = torch.zeros(n_dof, dtype=torch.float64).pin_memory()
     if cfg.get("u0") == "gaussian_pulse":
         u0t.copy_(torch.from_numpy(sc_inputs.gaussian_pulse(s.dof_coords()[:, 0])))
-    v0t = torch.zeros(n_dof, dtype=torch.float64).pin_memory()
     uht = torch.empty(n_dof, dtype=torch.float64).pin_memory()
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     with torch.cuda.stream(stream):
         e0.record(stream)
-        s.set_state(u0t.numpy(), v0t.numpy())
+        s.set_state(u0t.numpy(), None)   # v0 = 0 (every config starts at rest)
         s.step(K)
         s.read(uht.numpy())
         e1.record(stream)
     torch.cuda.synchronize()
     t_e2e = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([t_e2e], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
     e2e = {"value": n_dof * K / (t_e2e / 1e3), "unit": UNIT,
-           "h2d_bytes_per_step": 16.0 * n_dof / K, "d2h_bytes_per_step": 8.0 * n_dof / K,
-           "job": f"sc_set_state(u0,v0 pinned host) + sc_step({K}) + sc_read(u pinned host)"}
+           "h2d_bytes_per_step": 8.0 * n_dof / K, "d2h_bytes_per_step": 8.0 * n_dof / K,
+           "job": f"sc_set_state(u0 pinned host, v0 = 0) + sc_step({K}) + sc_read(u pinned host)"}
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            scfg, what = cpu_sample_cfg(cfg)
-            v, t, t_setup, nd, mode = oracle_sample(scfg, args.cpu_steps)
-            cpu = {"value": v, "unit": UNIT, "cores": _cores(), "kind": "oracle",
-                   "sample": f"config {args.config} {what} ({nd} DOFs, {mode}), {args.cpu_steps} oracle IMEX "
-                             f"steps ({t:.1f} s; setup {t_setup:.1f} s untimed)"}
+            cpu, _ = _cpu_line(args, args.cpu_steps)
         except Exception as ex:  # report, do not fail the bench
-            cpu = {"value": None, "unit": UNIT, "cores": _cores(), "kind": "oracle", "sample": f"failed: {ex}"}
+            cpu = {"value": None, "unit": UNIT, "cores": ORACLE_THREADS, "kind": "oracle", "sample": f"failed: {ex}"}
     if rank == 0:
-        l2 = ("per-step working set larger than L2 (no flush)" if info["bytes_per_step"] > 126e6
-              else "L2-resident working set (no flush)")
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
                 "ms_per_step": t_ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": "f64", "data": "synthetic",
-                "config": _config_dict(cfg, n_dof, {"n_c": info["n_c"], "n_d": info["n_d"],
-                                                     "cells_cut": info["cells_cut"], "l2": l2,
-                                                     "n_components": info["n_components"],
-                                                     "n_supernodes": info["n_supernodes"],
-                                                     "nnz_factor": info["nnz_factor"],
-                                                     "factor_height": info["factor_height"],
-                                                     "kernels_per_step": info["kernels_per_step"],
-                                                     "parallelism": (f"z-slabs over {world} GPUs, NCCL exchange"
-                                                                     if world > 1 else "1 GPU"),
-                                                     "halo_values_per_step": info["halo_send"],
-                                                     "n_c_rank0": info["n_c_local"]}),
+                "dtype": "f64", "data": "synthetic", "config": _config_dict(cfg),
+                "problem": {"n_dof": n_dof, "n_c": info["n_c"], "n_d": info["n_d"], "cells_cut": info["cells_cut"],
+                            "n_components": info["n_components"], "n_supernodes": info["n_supernodes"],
+                            "nnz_factor": info["nnz_factor"], "factor_height": info["factor_height"],
+                            "kernels_per_step": info["kernels_per_step"],
+                            "parallelism": (f"z-slabs over {world} GPUs, NCCL exchange" if world > 1 else "1 GPU"),
+                            "halo_values_per_step": info["halo_send"], "n_c_rank0": info["n_c_local"]},
                 "roofline": roof, "kernels": breakdown, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
                 "gpu_launches": int(info["kernels_per_step"]) * K,
                 "step_bytes_algorithmic": info["bytes_per_step"],

@@ -69,7 +69,10 @@ typedef struct {
 
 /* Geometry and material.  tree_depth = spacetree depth D; lattice_s = s of the
  * cut-test lattice (reading C6, default 4); fill_eps = empty-cell threshold (P:866-868,
- * default 1e-10; reading C7); rho, c constant (reading C10); integrator below. */
+ * default 1e-10; reading C7: a cell is empty iff none of its Gauss points is physical, which
+ * equals eta < fill_eps because sc_setup rejects (SC_ERR_CONFIG) any dim/p/tree_depth whose
+ * smallest nonzero fill ratio (2^-D w_min/2)^dim is below fill_eps); rho, c constant (P:846,
+ * reading C10); integrator below. */
 typedef struct {
   int32_t n_voids;
   const sc_void* voids;
@@ -156,9 +159,13 @@ sc_status sc_setup(const sc_grid* grid, int32_t p, double alpha, const sc_geomet
                    double dt, const sc_source* src, const double* u0, const double* v0,
                    const sc_dist* dist, sc_ctx** out);
 
-/* Reset the state to (u0, v0) at t = 0 (host arrays, length n_dof, canonical order; NULL =>
- * zero) and recompute the start a_0 = M^-1 (f_t(0) f_x - K u0), u^d_-1 (reading C3). */
-sc_status sc_set_state(sc_ctx* ctx, const double* u0, const double* v0);
+/* Reset the state to (u0, v0) at t = 0 (host arrays of len entries in canonical order; NULL
+ * => zero) and recompute the start a_0 = M^-1 (f_t(0) f_x - K u0), u^d_-1 (reading C3;
+ * P:752 gives the initial displacement and velocity).  len must equal n_dof whenever u0 or v0
+ * is non-NULL (SC_ERR_CONFIG otherwise, nothing read).  The arrays are staged through
+ * context-owned device buffers (no allocation per call after the first v0); pinned host
+ * memory makes the copies asynchronous.  Synchronises the context stream. */
+sc_status sc_set_state(sc_ctx* ctx, const double* u0, const double* v0, int64_t len);
 
 /* Enqueue n >= 0 Newmark IMEX steps (steps (a1)-(a6) of DESIGN.md §2) on the
  * context stream.  Asynchronous: returns after enqueueing.  Blow-up (non-finite u) sets a

@@ -79,7 +79,7 @@ def load_library(path=LIB_PATH):
     lib.sc_setup.argtypes = [P(sc_grid), ctypes.c_int32, ctypes.c_double, P(sc_geometry), ctypes.c_double,
                              P(sc_source), P(ctypes.c_double), P(ctypes.c_double), P(sc_dist),
                              P(ctypes.c_void_p)]
-    lib.sc_set_state.argtypes = [ctypes.c_void_p, P(ctypes.c_double), P(ctypes.c_double)]
+    lib.sc_set_state.argtypes = [ctypes.c_void_p, P(ctypes.c_double), P(ctypes.c_double), ctypes.c_int64]
     lib.sc_step.argtypes = [ctypes.c_void_p, ctypes.c_int64]
     lib.sc_sync.argtypes = [ctypes.c_void_p]
     lib.sc_read.argtypes = [ctypes.c_void_p, P(ctypes.c_double), ctypes.c_int64]
@@ -190,9 +190,13 @@ class Solver:
         return {k: getattr(inf, k) for k, _ in sc_info._fields_}
 
     def set_state(self, u0=None, v0=None):
+        n = self.info["n_dof"]
         u0a = None if u0 is None else np.ascontiguousarray(u0, dtype=np.float64)
         v0a = None if v0 is None else np.ascontiguousarray(v0, dtype=np.float64)
-        self._check(self._lib.sc_set_state(self.ctx, _dptr(u0a), _dptr(v0a)))
+        for name, a in (("u0", u0a), ("v0", v0a)):
+            if a is not None and a.shape != (n,):
+                raise ValueError(f"set_state: {name} must have shape ({n},), got {a.shape}")
+        self._check(self._lib.sc_set_state(self.ctx, _dptr(u0a), _dptr(v0a), n))
 
     def step(self, n):
         self._check(self._lib.sc_step(self.ctx, int(n)))

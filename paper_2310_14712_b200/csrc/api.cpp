@@ -56,7 +56,7 @@ static void free_ctx(sc_ctx* c) {
                   c->d_sn_uoff, c->d_sn_goff, c->d_R, c->d_gptr, c->d_gidx, c->d_items, c->fS.A,
                   c->fM.A, c->fS.d, c->fM.d, c->d_tmp, c->d_nitem, c->d_chptr, c->d_chidx, c->d_parent, c->d_solve_cnt,
                   c->d_part, c->d_trace, c->d_near_tiles, c->d_qmeta, c->d_far_tiles, c->d_xs_idx, c->d_xr_idx,
-                  c->d_xs_buf, c->d_xr_buf, c->d_own_lat, c->d_own_dof, c->d_full, c->d_clean, c->d_rec_lat, c->d_rec_w,
+                  c->d_xs_buf, c->d_xr_buf, c->d_stage, c->d_vlat, c->d_own_lat, c->d_own_dof, c->d_full, c->d_clean, c->d_rec_lat, c->d_rec_w,
                   c->d_rec_trace, c->d_mc, c->d_g2};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -90,6 +90,22 @@ static void validate(const sc_grid* grid, int32_t p, double alpha, const sc_geom
   for (int i = 0; i < geom->n_voids; ++i) {
     const sc_void& v = geom->voids[i];
     if (v.kind != SC_VOID_ELLIPSOID && v.kind != SC_VOID_HALFSPACE) throw ScError(SC_ERR_CONFIG, "void kind");
+  }
+  // empty-cell rule (reading C7): a cell is EMPTY iff none of its Gauss
+  // points is physical.  That integer decision equals "eta < fill_eps" exactly when the smallest
+  // nonzero fill ratio a cell can have - one physical Gauss point of the smallest weight on a
+  // depth-D leaf, eta_min = (2^-D * w_min / 2)^dim - is >= fill_eps; deeper trees (or a larger
+  // fill_eps) would make the two rules differ, so they are rejected instead of silently ignored.
+  if (!(geom->fill_eps >= 0.0) || !(geom->fill_eps < 1.0)) throw ScError(SC_ERR_CONFIG, "fill_eps must be in [0, 1)");
+  {
+    std::vector<double> gx, gw;
+    host_gauss(p + 1, gx, gw);
+    double wmin = gw[0];
+    for (double w : gw) wmin = std::min(wmin, w);
+    const double eta_min = std::pow(std::ldexp(0.5 * wmin, -geom->tree_depth), grid->dim);
+    if (eta_min < geom->fill_eps)
+      throw ScError(SC_ERR_CONFIG, "fill_eps exceeds the smallest nonzero fill ratio of this tree_depth/p/dim "
+                                   "(the empty rule 'no physical Gauss point' would differ from eta < fill_eps)");
   }
 }
 
@@ -203,23 +219,12 @@ extern "C" sc_status sc_setup(const sc_grid* grid, int32_t p, double alpha, cons
       c->bytes_per_step = ex + 24.0 * (double)c->n_irr + ce + so +
                           56.0 * (double)c->n_cl;   // r^c gather + corrector state (u, v, a, x)
     }
-    if (u0 || v0) {
-      double *du = nullptr, *dv = nullptr;
-      const size_t nbytes = sizeof(double) * c->n_dof;
-      if (u0) {
-        SC_CUDA(cudaMalloc(&du, nbytes));
-        SC_CUDA(cudaMemcpy(du, u0, nbytes, cudaMemcpyHostToDevice));
-      }
-      if (v0) {
-        SC_CUDA(cudaMalloc(&dv, nbytes));
-        SC_CUDA(cudaMemcpy(dv, v0, nbytes, cudaMemcpyHostToDevice));
-      }
-      run_startup(c, du, dv);
-      if (du) cudaFree(du);
-      if (dv) cudaFree(dv);
-    } else {
-      run_startup(c, nullptr, nullptr);
+    if (u0) SC_CUDA(cudaMemcpy(c->d_out, u0, sizeof(double) * c->n_dof, cudaMemcpyHostToDevice));
+    if (v0) {
+      SC_CUDA(cudaMalloc(&c->d_stage, sizeof(double) * std::max<int64_t>(1, c->n_dof)));
+      SC_CUDA(cudaMemcpy(c->d_stage, v0, sizeof(double) * c->n_dof, cudaMemcpyHostToDevice));
     }
+    run_startup(c, u0 ? c->d_out : nullptr, v0 ? c->d_stage : nullptr);
     build_graphs(c);
     if (c->world > 1 && dist->nccl_unique_id) nccl_init(c, dist->nccl_unique_id);
     SC_CUDA(cudaStreamSynchronize(c->stream));
@@ -237,23 +242,22 @@ extern "C" sc_status sc_setup(const sc_grid* grid, int32_t p, double alpha, cons
   }
 }
 
-extern "C" sc_status sc_set_state(sc_ctx* c, const double* u0, const double* v0) {
+extern "C" sc_status sc_set_state(sc_ctx* c, const double* u0, const double* v0, int64_t len) {
   if (!c) return SC_ERR_STATE;
+  if ((u0 || v0) && len != c->n_dof) {
+    c->err = "sc_set_state: len must equal n_dof (" + std::to_string(c->n_dof) + ")";
+    return SC_ERR_CONFIG;
+  }
   try {
     SC_CUDA(cudaSetDevice(c->device));
-    double *du = nullptr, *dv = nullptr;
+    // staged through context-owned buffers (no per-call allocation): u0 -> d_out, v0 -> d_stage
     const size_t nbytes = sizeof(double) * c->n_dof;
-    if (u0) {
-      SC_CUDA(cudaMalloc(&du, nbytes));
-      SC_CUDA(cudaMemcpyAsync(du, u0, nbytes, cudaMemcpyHostToDevice, c->stream));
-    }
+    if (u0) SC_CUDA(cudaMemcpyAsync(c->d_out, u0, nbytes, cudaMemcpyHostToDevice, c->stream));
     if (v0) {
-      SC_CUDA(cudaMalloc(&dv, nbytes));
-      SC_CUDA(cudaMemcpyAsync(dv, v0, nbytes, cudaMemcpyHostToDevice, c->stream));
+      if (!c->d_stage) SC_CUDA(cudaMalloc(&c->d_stage, sizeof(double) * std::max<int64_t>(1, c->n_dof)));
+      SC_CUDA(cudaMemcpyAsync(c->d_stage, v0, nbytes, cudaMemcpyHostToDevice, c->stream));
     }
-    run_startup(c, du, dv);
-    if (du) cudaFree(du);
-    if (dv) cudaFree(dv);
+    run_startup(c, u0 ? c->d_out : nullptr, v0 ? c->d_stage : nullptr);
     return SC_OK;
   } catch (const ScError& e) {
     return fail(c, e);

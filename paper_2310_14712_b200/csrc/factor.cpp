@@ -189,7 +189,7 @@ void make_panel(const double* F, int n, int w, double* P) {
 static void nested_dissection(Builder& b, int comp, std::vector<int>& nodes, std::vector<int>& roots,
                               int& next_col, std::vector<int>& order_out) {
   const GridP& g = b.c->g;
-  static const int LEAF = getenv("SC_ND_LEAF") ? atoi(getenv("SC_ND_LEAF")) : 32;   // max nodes of an ND leaf (r1_solve_variants.txt)
+  static const int LEAF = sc_knob("SC_ND_LEAF") ? atoi(sc_knob("SC_ND_LEAF")) : 32;   // max nodes of an ND leaf (r1_solve_variants.txt)
   std::function<void(std::vector<int>&, std::vector<int>&)> rec = [&](std::vector<int>& nd,
                                                                       std::vector<int>& out_roots) {
     if (nd.empty()) return;
@@ -866,7 +866,7 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   // (r, goff, uoff, roff) (aoff lo, aoff hi, ld, wp).
   const int TILE = SOLVE_TILE;
   int stage = SOLVE_STAGE;
-  if (const char* v = getenv("SC_SOLVE_STAGE")) stage = std::max(1024, std::min(4 * SOLVE_STAGE, atoi(v)));
+  if (const char* v = sc_knob("SC_SOLVE_STAGE")) stage = std::max(1024, std::min(4 * SOLVE_STAGE, atoi(v)));
   c->solve_stage = stage;
   std::vector<int32_t> items;
   std::vector<int32_t> nblk(2 * (size_t)nsn, 0);

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <string>
 #include <utility>
@@ -116,7 +117,9 @@ struct sc_ctx {
   uint8_t* d_ntype = nullptr;
   int8_t* d_cell_class = nullptr;
   int64_t* d_dof_lat = nullptr;
-  double* d_out = nullptr;                 // n_dof gather buffer for sc_read
+  double* d_out = nullptr;                 // n_dof gather buffer for sc_read (and u0 staging)
+  double* d_stage = nullptr;               // n_dof staging buffer of v0 (allocated on first use)
+  double* d_vlat = nullptr;                // lattice v0 of the start (allocated on first use)
   double* d_ft = nullptr;                  // f_t series
   int64_t n_t = 0;
   long long* d_step = nullptr;             // device step counter
@@ -216,6 +219,19 @@ struct CompSpan {
 };
 
 // ---------------------------------------------------------------- helpers
+// Experiment knobs (schedule / ordering / variant switches): read from the environment ONLY in
+// experiment builds (SC_NVCC_DEFS=-DSC_EXPERIMENTS with an SC_BUILD_TAG / SC_BUILD_OUT).  The
+// product library ignores the environment except the SC_TRACE / SC_DEBUG diagnostics, which
+// change no result.
+inline const char* sc_knob(const char* name) {
+#ifdef SC_EXPERIMENTS
+  return getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
+
 #define SC_CUDA(call)                                                                  \
   do {                                                                                 \
     cudaError_t e__ = (call);                                                          \

@@ -641,7 +641,7 @@ void launch_solve(sc_ctx* c, const Factor& f, cudaStream_t st) {
     SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve, NT, smem));
     // cap the resident solve CTAs (room for the concurrent far-d update, step.cu)
     int cap = c->solve_cap;
-    if (const char* v = getenv("SC_SOLVE_CTAS_PER_SM")) cap = atoi(v);
+    if (const char* v = sc_knob("SC_SOLVE_CTAS_PER_SM")) cap = atoi(v);
     if (cap > 0) per_sm = std::max(1, std::min(per_sm, cap));
     c->solve_grid = std::max(1, std::min(c->n_items, per_sm * sms));
   }

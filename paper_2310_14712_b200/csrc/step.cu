@@ -519,7 +519,7 @@ static void enqueue_c_part(sc_ctx* c, const double* A, double* B, cudaStream_t s
     launch_celem(c, 0, A, B, st);
     k_crhs<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, st>>>(c->d_b, c->d_fxc, c->d_rhs_ptr, c->d_rhs_idx, c->d_Y,
                                                               (int)c->n_cl, c->d_ft, c->n_t, c->d_step, 1, c->fS.d);
-    if (!getenv("SC_DEBUG_NO_SOLVE")) launch_solve(c, c->fS, st);   // timing experiments only
+    if (!sc_knob("SC_DEBUG_NO_SOLVE")) launch_solve(c, c->fS, st);   // experiment builds only
     k_corrector<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, st>>>(A, B, c->d_vc, c->d_ac, c->d_x, c->d_c_lat,
                                                                   (int)c->n_cl, dt, c->d_flag, c->fS.d);
   }
@@ -567,7 +567,7 @@ void enqueue_step(sc_ctx* c, int parity, cudaStream_t st) {
   enqueue_c_part(c, A, B, c->s_hi);
   SC_CUDA(cudaEventRecord(c->ev_join, c->s_hi));
   // far-d nodes of step n+1 on a capped grid: the c part keeps SM resources
-  if (!getenv("SC_DEBUG_NO_FAR"))   // timing experiments only (wrong results when set)
+  if (!sc_knob("SC_DEBUG_NO_FAR"))   // experiment builds only (wrong results when set)
     launch_explicit(c, B, A, A, 2.0, -1.0, dt * dt, 1, st, c->far_cap);
   SC_CUDA(cudaStreamWaitEvent(st, c->ev_join, 0));
 }
@@ -586,12 +586,12 @@ void build_graphs(sc_ctx* c) {
   // resident CTAs per SM and SC_SOLVE_CTAS_PER_SM those of the persistent solve (solve.cu) so
   // both can co-reside.  Measured on config 4 (profiles/): caps trade solve latency for
   // overlap one-for-one, so both default to the occupancy limit.
-  if (const char* v = getenv("SC_FAR_CAP")) c->far_cap = std::max(0, atoi(v));
+  if (const char* v = sc_knob("SC_FAR_CAP")) c->far_cap = std::max(0, atoi(v));
   // SC_PIPELINE=1: fork the far-d update of step n+1 against the c part of step n (one rank
   // with c DOFs); default off: measured no gain and it costs a second
   // (near-node) explicit launch
-  c->pipelined = c->n_c > 0 && c->n_d > c->n_irr && c->world == 1 && c->integrator == 0 && getenv("SC_PIPELINE") &&
-                 atoi(getenv("SC_PIPELINE"));
+  c->pipelined = c->n_c > 0 && c->n_d > c->n_irr && c->world == 1 && c->integrator == 0 && sc_knob("SC_PIPELINE") &&
+                 atoi(sc_knob("SC_PIPELINE"));
   if (!c->s_hi) {
     int lo = 0, hi = 0;
     SC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -626,7 +626,7 @@ void setup_step_structures(sc_ctx* c) {
     g.ezl = 16;
     explicit_tiling(g, ext, tg);
     if ((int64_t)tg[0] * tg[1] * tg[2] < 4 * 2 * 148) g.ezl = 8;
-    if (const char* v = getenv("SC_EZL")) g.ezl = std::max(1, atoi(v));   // experiments
+    if (const char* v = sc_knob("SC_EZL")) g.ezl = std::max(1, atoi(v));   // experiments
   }
   explicit_tiling(g, ext, tg);
   // tile lists of the node types this rank updates: near-d (type 4) always, far-d (type 1)
@@ -759,7 +759,8 @@ void run_startup(sc_ctx* c, const double* u0, const double* v0) {
   if (u0 && c->n_dof) k_scatter<<<gb, 256, 0, c->stream>>>(u0, c->d_dof_lat, A, c->n_dof);
   double* vlat = nullptr;
   if (v0 && c->n_dof) {
-    SC_CUDA(cudaMalloc(&vlat, latb));
+    if (!c->d_vlat) SC_CUDA(cudaMalloc(&c->d_vlat, latb));
+    vlat = c->d_vlat;
     SC_CUDA(cudaMemsetAsync(vlat, 0, latb, c->stream));
     k_scatter<<<gb, 256, 0, c->stream>>>(v0, c->d_dof_lat, vlat, c->n_dof);
   }
@@ -790,7 +791,6 @@ void run_startup(sc_ctx* c, const double* u0, const double* v0) {
   }
   SC_CUDA(cudaGetLastError());
   SC_CUDA(cudaStreamSynchronize(c->stream));
-  if (vlat) cudaFree(vlat);
   c->host_step = 0;
   c->far_ready = false;
 }
