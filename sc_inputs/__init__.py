@@ -18,4 +18,4 @@ Both the oracle (``oracle/``) and the product path
 "same seeded inputs" holds by construction.
 """
 from .configs import get_config, CONFIG_IDS, small_config, source_signal, describe  # noqa: F401
-from .signals import ricker, gaussian_pulse, gaussian_derivative, sine_burst  # noqa: F401
+from .signals import ricker, gaussian_pulse, gaussian_derivative, sine_burst, compact_bump  # noqa: F401

@@ -16,6 +16,10 @@
 * Config-1 initial field u0(x) = exp(-(x-0.3)^2/0.002) (BASELINE.json
   configs[0]); both sides interpolate it nodally at their own node
   coordinates (reading C16).
+* Compactly supported initial displacement u0(x) = (1 - |x - x0|^2 / R^2)^4 for
+  |x - x0| < R, else 0 (a C^3 bump; P:752 gives the initial displacement as an input).  Its
+  exact zero outside the ball bounds the dependency region of a finite number of steps, so
+  a full-size run can be checked against the oracle on a sub-box (tests/subbox.py).
 """
 import numpy as np
 
@@ -62,3 +66,12 @@ def signal_series(kind, f0, dt, n_values):
     if kind == "sine_burst":
         return sine_burst(t, f0)
     raise ValueError(f"unknown signal {kind!r}")
+
+
+def compact_bump(X, x0, R):
+    """u0 at the points X (n x 3): (1 - r^2/R^2)^4 for r = |X - x0| < R, else exactly 0."""
+    X = np.asarray(X, dtype=np.float64)
+    x0 = np.asarray(x0, dtype=np.float64)
+    r2 = np.sum((X[:, :len(x0)] - x0[None, :]) ** 2, axis=1)
+    q = 1.0 - r2 / (R * R)
+    return np.where(q > 0.0, q ** 4, 0.0)

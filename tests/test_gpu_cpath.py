@@ -1,0 +1,120 @@
+"""Full-size parity of the implicit (c) path, BASELINE configs 3, 4 and 5 (the bench workload).
+
+The GPU runs the WHOLE configuration, in the launch configuration bench.py times, from a
+compactly supported u0 (sc_inputs.compact_bump) centred between neighbouring voids, with a
+zero load; the oracle runs the same steps on the dependency-closure box (tests/subbox.py,
+pinned oracle-vs-oracle in tests/test_oracle_subbox.py).  Asserted (north_star parity bar):
+* relative L2 <= 1e-10 over the box DOFs, and separately over the box's c DOFs;
+* the c DOFs carry >= 1e-2 of ||u|| (so a wrong implicit solve cannot hide);
+* every DOF outside the box is exactly 0 on the GPU;
+* bit-exact cell classification on the box cells away from the box faces.
+Achieved errors are appended to gpurun_out/parity_errors.jsonl (copied to profiles/)."""
+import json
+import os
+import time
+
+import numpy as np
+import pytest
+
+import sc_inputs
+from oracle.assembly import build_system, node_coords
+from oracle.integrators import from_system, imex
+from subbox import box_config, box_to_full_lattice, closure_box, interior_cells, void_radius
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2310_14712_b200.build import build
+    build()
+    import paper_2310_14712_b200 as p
+    p.load_library()
+    return p
+
+
+def _between_voids(cfg):
+    """The point between the two closest voids (weighted by their radii)."""
+    d = cfg["dim"]
+    C = np.array([v["c"][:d] for v in cfg["voids"]])
+    r = np.array([void_radius(v, d) for v in cfg["voids"]])
+    D = np.linalg.norm(C[:, None, :] - C[None, :, :], axis=2) - r[:, None] - r[None, :]
+    np.fill_diagonal(D, np.inf)
+    i, j = np.unravel_index(np.argmin(D), D.shape)
+    return list((C[i] * r[j] + C[j] * r[i]) / (r[i] + r[j]))
+
+
+def _log(rec):
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", "parity_errors.jsonl"), "a") as f:
+        f.write(json.dumps(rec) + "\n")
+
+
+def _cpath(pkg, cid, x0, R, steps, mode):
+    cfg = sc_inputs.get_config(cid)
+    lo, hi, used = closure_box(cfg, x0, R, steps)
+    bcfg = box_config(cfg, lo, hi)
+    t0 = time.time()
+    sysm = build_system(bcfg, mode)
+    u0b = sc_inputs.compact_bump(node_coords(bcfg, sysm.cl.lattice_index), x0, R)
+    ref = imex(from_system(sysm), cfg["dt"], steps, None, u0b, None)
+    t_oracle = time.time() - t0
+    # the full configuration on the GPU (bench launch configuration; the point source is
+    # present with f_t = 0)
+    s = pkg.from_config(cfg, f_t=np.zeros(steps + 2))
+    cc, isc, lat = s.classification()
+    lat_box = box_to_full_lattice(cfg, lo, sysm.cl.lattice_index, bcfg["cells"])
+    pos = np.searchsorted(lat, lat_box)
+    assert np.all(lat[pos] == lat_box), "box DOF missing from the GPU DOF set"
+    u0 = np.zeros(s.info["n_dof"])
+    u0[pos] = u0b
+    s.set_state(u0, None)
+    s.step(steps)
+    u = s.read()
+    info = s.info
+    s.close()
+    ub = u[pos]
+    c = sysm.cl.is_c
+    err = np.linalg.norm(ub - ref) / np.linalg.norm(ref)
+    err_c = np.linalg.norm(ub[c] - ref[c]) / np.linalg.norm(ref[c])
+    err_d = np.linalg.norm(ub[~c] - ref[~c]) / np.linalg.norm(ref[~c])
+    share_c = np.linalg.norm(ub[c]) / np.linalg.norm(ub)
+    outside = np.ones(len(u), dtype=bool)
+    outside[pos] = False
+    rec = {"test": "cpath", "config": cid, "box_cells": [lo, hi], "box_dofs": int(len(pos)),
+           "box_c_dofs": int(c.sum()), "voids_touched": len(used), "steps": steps, "x0": x0, "R": R,
+           "rel_l2": err, "rel_l2_c": err_c, "rel_l2_d": err_d, "c_share": share_c,
+           "max_abs_outside": float(np.abs(u[outside]).max()) if outside.any() else 0.0,
+           "oracle_s": t_oracle, "n_dof": int(info["n_dof"])}
+    _log(rec)
+    print(rec)
+    assert np.all(np.isfinite(u))
+    # classification of the box cells away from the box faces: bit-exact
+    fidx, bidx = interior_cells(cfg, lo, hi, bcfg["cells"])
+    assert np.array_equal(cc[fidx], sysm.cl.cell_class[bidx])
+    assert share_c >= 1e-2, rec
+    assert err <= TOL and err_c <= TOL, rec
+    assert np.all(u[outside] == 0.0), rec
+    return rec
+
+
+def test_config5_cpath_full_size(pkg):
+    # between voids 96 and 19 of config 5 (semi-axes 0.027 / 0.020, 0.036 apart): 8 steps reach
+    # 4 void components; the box is 44 x 53 x 34 cells (5.1e6 DOFs, 8.7e4 c DOFs)
+    _cpath(pkg, 5, [0.205, 0.30, 0.107], 0.03, 8, "ebe")
+
+
+def test_config4_cpath_full_size(pkg):
+    cfg = sc_inputs.get_config(4)
+    _cpath(pkg, 4, _between_voids(cfg), 0.05, 40, "ebe")
+
+
+def test_config3_cpath_full_size(pkg):
+    cfg = sc_inputs.get_config(3)
+    _cpath(pkg, 3, _between_voids(cfg), 0.02, 100, "sparse")
