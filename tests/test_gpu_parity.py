@@ -77,6 +77,29 @@ def test_3d_ragged(pkg, p):
     _check(pkg, cfg, 15)
 
 
+# 3D explicit kernel layouts (explicit3w.cuh): several x-warps per plane group (named-barrier
+# exchange of the element-boundary partials), several x segments (halo lane), y chunks with a
+# warm-up element, the domain-end x node, non-cubic cells (s0 != s1 != s2), voids on x-warp
+# boundaries (non-clean blocks).  cells, p, hi, void centre
+LAYOUTS = [
+    ([40, 3, 4], 2, [1.0, 0.15, 0.2], [0.80, 0.075, 0.1]),      # 2 x-warps, non-cubic
+    ([70, 2, 3], 4, [1.0, 0.04, 0.06], [0.457, 0.02, 0.03]),    # 3 x-warps (one partly idle)
+    ([64, 3, 2], 3, [1.0, 0.05, 0.03], [0.5, 0.025, 0.015]),    # exactly 2 full x-warps: end lane = lane 31
+    ([170, 2, 2], 4, [1.0, 0.0118, 0.0118], [0.75, 0.006, 0.006]),   # 2 x segments (halo lane)
+]
+
+
+@pytest.mark.parametrize("cells,p,hi,vc", LAYOUTS)
+def test_3d_kernel_layouts(pkg, cells, p, hi, vc):
+    h = min(hi[k] / cells[k] for k in range(3))
+    r = 1.6 * h
+    void = {"kind": "ellipsoid", "c": vc, "A": [1 / r ** 2, 1 / r ** 2, 1 / r ** 2, 0.0, 0.0, 0.0]}
+    cfg = sc_inputs.small_config(3, cells, p, voids=[void], depth=2, alpha=1e-5, steps=12, hi=hi,
+                                 source={"x": [0.31, hi[1] * 0.4, hi[2] * 0.6], "f0": 6.0})
+    cfg["dt"] = 0.9 * dt_crit_uncut(3, p, h)
+    _check(pkg, cfg, 12, mode="ebe")
+
+
 def test_1d_config1_full(pkg):
     # BASELINE configs[0] at its full 2000 steps
     _check(pkg, sc_inputs.get_config(1), 2000)
