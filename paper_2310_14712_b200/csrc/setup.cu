@@ -516,7 +516,11 @@ void setup_device_geometry(sc_ctx* c) {
     c->Mcut_host.resize(mat);
     SC_CUDA(cudaMemcpyAsync(c->Kcut_host.data(), c->d_Kcut, sizeof(double) * mat, cudaMemcpyDeviceToHost, c->stream));
     SC_CUDA(cudaMemcpyAsync(c->Mcut_host.data(), d_M, sizeof(double) * mat, cudaMemcpyDeviceToHost, c->stream));
+    // device copy for the step: tiled-symmetric storage (k_celem), the full matrices freed
+    double* d_full = c->d_Kcut;
+    c->d_Kcut = pack_sym(c, d_full, c->n_cut);
     SC_CUDA(cudaStreamSynchronize(c->stream));
+    cudaFree(d_full);
     cudaFree(d_cc);
     cudaFree(d_slots);
     cudaFree(d_gll);

@@ -162,27 +162,69 @@ __global__ void k_irregular(const double* __restrict__ U, const double* Pv, doub
 }
 
 // ------------------------------------------------------------------ c elements
+// Element matrices K_e are symmetric: stored as the upper triangle of an nt x nt
+// grid of T x T tiles (nt T >= nb, zero padded), tiles (I, J), I <= J, in row order, each
+// row-major with stride TS doubles (TS even: 16-byte aligned); (nt+1)/(2 nt) of the full bytes
+// (60% for 3D p = 4: nt = 5, T = 25).  Built once at setup (k_pack_sym).
+__global__ void k_pack_sym(const double* __restrict__ full, double* __restrict__ packed, long long n_mat, int nb,
+                           int T, int nt, int TS, long long ms) {
+  const long long per = (long long)(nt * (nt + 1) / 2) * TS;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n_mat * per;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long m = q / per;
+    const int r = (int)(q - m * per);
+    int tile = r / TS;
+    const int o = r - tile * TS;
+    int I = 0;
+    while (tile >= nt - I) {   // tiles of row I: J = I .. nt-1
+      tile -= nt - I;
+      ++I;
+    }
+    const int J = I + tile;
+    const int a = o / T, b = o - (o / T) * T;
+    const int i = I * T + a, j = J * T + b;
+    double v = 0.0;
+    if (o < T * T && i < nb && j < nb) v = full[(size_t)m * nb * nb + (size_t)i * nb + j];
+    packed[(size_t)m * ms + r] = v;
+  }
+}
+
+__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+
+// (a3)+(a4) c-element products Y[e][i] = sum_j K_e[i][j] w_j, one CTA per element.
 // mode 0 (step): w = predictor u~^c on c nodes, u^d_{n+1} (buffer B) elsewhere;
-// mode 1 (start): w = A everywhere.   Y[e][i] = sum_j K_e[i][j] w_j (K_e symmetric).
-#ifndef CELEM_U
-#define CELEM_U 8
-#endif
-#ifndef CELEM_CS
-#define CELEM_CS 0
-#endif
+// mode 1 (start): w = A everywhere.
+// The stored tiles stream through shared memory (cp.async, two buffers); thread t (block I =
+// t / T, row a = t % T) owns output t and adds, per tile (I0, J0): the row sum of row a when
+// I = I0 (K_IJ w_J) and the column sum of column a when I = J0 > I0 (K_JI^T w_J) - every
+// stored entry is read once from HBM and used twice; fixed order, no atomics.
 __global__ void k_celem(int mode, const double* __restrict__ A, const double* __restrict__ B,
                         const double* __restrict__ vc, const double* __restrict__ ac, double dt,
                         const int32_t* __restrict__ ecell, const int32_t* __restrict__ ekidx,
-                        const int32_t* __restrict__ ecidx, const double* __restrict__ Kcut,
-                        const double* __restrict__ Kref, double* __restrict__ Y, int ne, int nb, int tpe, GridP g) {
-  extern __shared__ double sw[];
-  const int epb = blockDim.x / tpe;
-  const int le = threadIdx.x / tpe, i = threadIdx.x % tpe;
-  const int e = blockIdx.x * epb + le;
-  const bool ok = e < ne;
-  const int n1 = g.p + 1;
-  double* w = sw + le * nb;
-  if (ok) {
+                        const int32_t* __restrict__ ecidx, const double* __restrict__ Kp,
+                        const double* __restrict__ Krefp, double* __restrict__ Y, int ne, int nb, int T, int nt,
+                        int TS, long long ms, GridP g) {
+  extern __shared__ double sm[];
+  const int wlen = (nt * T + 1) & ~1;
+  double* w = sm;              // [wlen]
+  double* tb = sm + wlen;      // [2][TS]
+  const int e = blockIdx.x;
+  if (e >= ne) return;
+  const int t = threadIdx.x, nthr = blockDim.x;
+  const int kidx = ekidx[e];
+  const double* K = kidx >= 0 ? Kp + (size_t)kidx * ms : Krefp;
+  auto stage = [&](int tile, int buf) {
+    const double* src = K + (size_t)tile * TS;
+    double* dst = tb + buf * TS;
+    for (int q = t; q < TS / 2; q += nthr) cpa16(dst + 2 * q, src + 2 * q);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  stage(0, 0);   // the first tile streams in while w is gathered
+  {
+    const int n1 = g.p + 1;
     const long long cell = ecell[e];
     long long ci[3];
     long long rem = cell;
@@ -194,44 +236,55 @@ __global__ void k_celem(int mode, const double* __restrict__ A, const double* __
         ci[k] = 0;
       }
     }
-    for (int j = i; j < nb; j += tpe) {
-      const int l0 = j % n1, l1 = (j / n1) % n1, l2 = j / (n1 * n1);
-      long long gl = ci[0] * g.p + l0;
-      if (g.dim > 1) gl += g.nl[0] * (ci[1] * g.p + l1);
-      if (g.dim > 2) gl += g.nl[0] * g.nl[1] * (ci[2] * g.p + l2);
-      double v;
-      if (mode == 1) {
-        v = A[gl];
-      } else {
-        const int cc = ecidx[(size_t)e * nb + j];
-        v = cc >= 0 ? A[gl] + dt * vc[cc] + 0.25 * dt * dt * ac[cc] : B[gl];
+    for (int j = t; j < wlen; j += nthr) {
+      double v = 0.0;
+      if (j < nb) {
+        const int l0 = j % n1, l1 = (j / n1) % n1, l2 = j / (n1 * n1);
+        long long gl = ci[0] * g.p + l0;
+        if (g.dim > 1) gl += g.nl[0] * (ci[1] * g.p + l1);
+        if (g.dim > 2) gl += g.nl[0] * g.nl[1] * (ci[2] * g.p + l2);
+        if (mode == 1) {
+          v = A[gl];
+        } else {
+          const int cc = ecidx[(size_t)e * nb + j];
+          v = cc >= 0 ? A[gl] + dt * vc[cc] + 0.25 * dt * dt * ac[cc] : B[gl];
+        }
       }
       w[j] = v;
     }
   }
-  __syncthreads();
-  if (!ok) return;
-  const int kidx = ekidx[e];
-  const double* K = kidx >= 0 ? Kcut + (size_t)kidx * nb * nb : Kref;
-  auto gemv = [&](auto ld) {
-    for (int r = i; r < nb; r += tpe) {
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      int j = 0;
-      for (; j + CELEM_U <= nb; j += CELEM_U) {   // CELEM_U independent loads in flight (HBM-bound GEMV)
-        double x[CELEM_U];
-#pragma unroll
-        for (int k = 0; k < CELEM_U; ++k) x[k] = ld(K + (size_t)(j + k) * nb + r);
-#pragma unroll
-        for (int k = 0; k < CELEM_U; ++k) acc[k & 3] += x[k] * w[j + k];
+  const int I = t / T, a = t - (t / T) * T;
+  double acc0 = 0.0, acc1 = 0.0;
+  const int ntiles = nt * (nt + 1) / 2;
+  int tile = 0;
+  for (int I0 = 0; I0 < nt; ++I0)
+    for (int J0 = I0; J0 < nt; ++J0, ++tile) {
+      if (tile + 1 < ntiles) {
+        stage(tile + 1, (tile + 1) & 1);
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
       }
-      for (; j < nb; ++j) acc[0] += ld(K + (size_t)j * nb + r) * w[j];
-      Y[(size_t)e * nb + r] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+      __syncthreads();   // tile staged (and, first time, w gathered)
+      const double* tt = tb + (tile & 1) * TS;
+      if (I == I0) {   // row a of K_IJ against w_J
+        const double* row = tt + a * T;
+        const double* wj = w + J0 * T;
+        for (int b = 0; b < T; b += 2) {
+          acc0 = fma(row[b], wj[b], acc0);
+          if (b + 1 < T) acc1 = fma(row[b + 1], wj[b + 1], acc1);
+        }
+      }
+      if (I == J0 && I0 != J0) {   // column a of K_(I0,J0) (= row a of its transpose) against w_I0
+        const double* wi = w + I0 * T;
+        for (int b = 0; b < T; b += 2) {
+          acc0 = fma(tt[b * T + a], wi[b], acc0);
+          if (b + 1 < T) acc1 = fma(tt[(b + 1) * T + a], wi[b + 1], acc1);
+        }
+      }
+      __syncthreads();   // buffer free for the tile after next
     }
-  };
-  // cut-cell matrices are streamed once per step (evict-first); the shared uncut reference
-  // matrix stays cached
-  if (CELEM_CS && kidx >= 0) gemv([](const double* p) { return __ldcs(p); });
-  else gemv([](const double* p) { return __ldg(p); });
+  if (t < nb) Y[(size_t)e * nb + t] = acc0 + acc1;
 }
 
 __global__ void k_crhs(double* __restrict__ b, const double* __restrict__ fxc, const int32_t* __restrict__ ptr,
@@ -477,14 +530,32 @@ void launch_explicit(sc_ctx* c, const double* U, const double* Pv, double* out, 
 
 static void launch_celem(sc_ctx* c, int mode, const double* A, const double* B, cudaStream_t st) {
   if (c->n_celem == 0) return;
-  const int nb = c->nb;
-  const int tpe = std::min(256, ((nb + 31) / 32) * 32);
-  const int epb = 256 / tpe;
-  const unsigned blocks = (unsigned)((c->n_celem + epb - 1) / epb);
-  k_celem<<<blocks, epb * tpe, sizeof(double) * epb * nb, st>>>(
-      mode, A, B, c->d_vc, c->d_ac, c->dt, c->d_celem_cell, c->d_celem_kidx, c->d_celem_cidx, c->d_Kcut,
-      c->d_Kref, c->d_Y, (int)c->n_celem, nb, tpe, c->g);
+  const int nthr = ((c->ct_nt * c->ct_T + 31) / 32) * 32;
+  const size_t smem = sizeof(double) * (((c->ct_nt * c->ct_T + 1) & ~1) + 2 * (size_t)c->ct_TS);
+  k_celem<<<(unsigned)c->n_celem, nthr, smem, st>>>(mode, A, B, c->d_vc, c->d_ac, c->dt, c->d_celem_cell,
+                                                     c->d_celem_kidx, c->d_celem_cidx, c->d_Kcut, c->d_Krefp, c->d_Y,
+                                                     (int)c->n_celem, c->nb, c->ct_T, c->ct_nt, c->ct_TS, c->ct_ms,
+                                                     c->g);
   SC_CUDA(cudaGetLastError());
+}
+
+// tiled-symmetric storage of the element matrices (k_celem): nt tiles per dimension of T rows
+void plan_sym_tiles(sc_ctx* c) {
+  const int nb = c->nb;
+  c->ct_nt = std::max(1, (nb + 12) / 25);   // tiles of ~25 rows: 3D p=4 -> 5 x 25, p=3 -> 3 x 22
+  c->ct_T = (nb + c->ct_nt - 1) / c->ct_nt;
+  c->ct_TS = (c->ct_T * c->ct_T + 1) & ~1;
+  c->ct_ms = (long long)(c->ct_nt * (c->ct_nt + 1) / 2) * c->ct_TS;
+}
+
+// full row-major matrices (device) -> tiled-symmetric storage (device, allocated here)
+double* pack_sym(sc_ctx* c, const double* d_full, long long n_mat) {
+  double* d_p = nullptr;
+  SC_CUDA(cudaMalloc(&d_p, sizeof(double) * std::max<long long>(1, n_mat * c->ct_ms)));
+  if (n_mat > 0)
+    k_pack_sym<<<148 * 8, 256, 0, c->stream>>>(d_full, d_p, n_mat, c->nb, c->ct_T, c->ct_nt, c->ct_TS, c->ct_ms);
+  SC_CUDA(cudaGetLastError());
+  return d_p;
 }
 
 static void launch_irregular(sc_ctx* c, const double* U, const double* Pv, double* out, double a1, double a2,
@@ -735,6 +806,9 @@ void device_upload_reference(sc_ctx* c) {
   SC_CUDA(cudaMemcpyToSymbol(c_iw2, &iw2, sizeof(double)));
   SC_CUDA(cudaMalloc(&c->d_Kref, sizeof(double) * c->Kref.size()));
   SC_CUDA(cudaMemcpy(c->d_Kref, c->Kref.data(), sizeof(double) * c->Kref.size(), cudaMemcpyHostToDevice));
+  plan_sym_tiles(c);
+  c->d_Krefp = pack_sym(c, c->d_Kref, 1);
+  SC_CUDA(cudaStreamSynchronize(c->stream));
 }
 
 void gather_dofs(sc_ctx* c, const double* d_lat, double* d_out) {
