@@ -196,6 +196,15 @@ sc_status sc_exchange_local(sc_ctx* const* ctxs, int32_t world);
  * Clobbers the state: call sc_set_state before stepping again.  One rank only. */
 sc_status sc_estimate_dt(sc_ctx* ctx, int32_t iters, double* lambda_max, double* dt_crit);
 
+/* Cell-wise critical time steps (Fig. fig:tCritsCircles,
+ * Table tab:criticaltimestepsizes): dt_cell[i] = 2 / sqrt(lambda_max(K_e, M_e)) of cell i (cells x
+ * fastest, len >= prod(cells)); uncut cells: the uncut cell-wise value (GLL-lumped mass,
+ * = sc_info.dt_crit_uncut); cut cells: which = 0 with the consistent cut-cell mass (the
+ * "consistent SCM"), which = 1 with the HRZ-lumped mass; empty cells: 0.  Computed
+ * on the device at setup (per cut cell: Cholesky of M_e and power iteration on
+ * L^-1 K_e L^-T to a 1e-15 relative Rayleigh-quotient change).  Host output; synchronises. */
+sc_status sc_cell_dt(sc_ctx* ctx, int32_t which, double* dt_cell, int64_t len);
+
 /* Elastic energy E = 1/2 u_n^T K u_n of the current state (PAPER.md P:758,
  * the quantity of fig:springCoupledMassesElastic) into *energy (host).  Computed by the step
  * kernels with zero CDM coefficients (M^{-1} K u on the d rows, K u on the c rows through the

@@ -53,3 +53,22 @@ def fill_ratio_cell_omega(eta, p, depth=13, rho_f=1e-6, s=4):
 
 
 __all__ = ["lambda_max", "dt_crit", "dt_crit_uncut", "fill_ratio_cell_omega", "build_tree"]
+
+
+def cell_dt_map(sysm, which="consistent"):
+    """Cell-wise critical time steps (Fig. fig:tCritsCircles, Table
+    tab:criticaltimestepsizes): dt_e = 2 / sqrt(lambda_max(K_e, M_e)) per cell, cells x
+    fastest; uncut cells with their GLL-lumped mass, cut cells with the consistent mass
+    (which="consistent") or the HRZ-lumped mass (which="hrz"); empty cells 0."""
+    from .assembly import hrz_element
+    from .geometry import UNCUT, CUT
+    cl = sysm.cl
+    out = np.zeros(len(cl.cell_class))
+    out[cl.cell_class == UNCUT] = dt_crit(sysm.Ke_uncut, sysm.Me_uncut)
+    cut = np.nonzero(cl.cell_class == CUT)[0]
+    for k, ci in enumerate(cut):
+        Me = sysm.cut_M[k]
+        if which == "hrz":
+            Me = hrz_element(Me)
+        out[ci] = dt_crit(sysm.cut_K[k], Me)
+    return out

@@ -61,7 +61,7 @@ class sc_info(ctypes.Structure):
 
 EXPORTS = ("sc_setup", "sc_set_state", "sc_step", "sc_sync", "sc_read", "sc_read_owned", "sc_read_c_state",
            "sc_query", "sc_read_classification", "sc_dof_coords", "sc_profile", "sc_exchange_local",
-           "sc_nccl_unique_id", "sc_estimate_dt", "sc_elastic_energy", "sc_set_receivers", "sc_read_traces", "sc_last_error",
+           "sc_nccl_unique_id", "sc_estimate_dt", "sc_cell_dt", "sc_elastic_energy", "sc_set_receivers", "sc_read_traces", "sc_last_error",
            "sc_destroy")
 
 _lib = None
@@ -88,6 +88,7 @@ def load_library(path=LIB_PATH):
     lib.sc_nccl_unique_id.argtypes = [ctypes.c_void_p]
     lib.sc_estimate_dt.argtypes = [ctypes.c_void_p, ctypes.c_int32, P(ctypes.c_double), P(ctypes.c_double)]
     lib.sc_elastic_energy.argtypes = [ctypes.c_void_p, P(ctypes.c_double)]
+    lib.sc_cell_dt.argtypes = [ctypes.c_void_p, ctypes.c_int32, P(ctypes.c_double), ctypes.c_int64]
     lib.sc_set_receivers.argtypes = [ctypes.c_void_p, P(ctypes.c_double), ctypes.c_int32, ctypes.c_int64]
     lib.sc_read_traces.argtypes = [ctypes.c_void_p, P(ctypes.c_double), ctypes.c_int64, P(ctypes.c_int64)]
     lib.sc_read_c_state.argtypes = [ctypes.c_void_p, P(ctypes.c_double), P(ctypes.c_double), ctypes.c_int64]
@@ -237,6 +238,13 @@ class Solver:
         lam, dt = ctypes.c_double(), ctypes.c_double()
         self._check(self._lib.sc_estimate_dt(self.ctx, int(iters), ctypes.byref(lam), ctypes.byref(dt)))
         return lam.value, dt.value
+
+    def cell_dt(self, which=0):
+        """Cell-wise critical time steps (cells x fastest): uncut cells the uncut cell-wise
+        value, cut cells with the consistent (which=0) or HRZ-lumped (which=1) mass, 0 if empty."""
+        out = np.empty(self._n_cells)
+        self._check(self._lib.sc_cell_dt(self.ctx, int(which), _dptr(out), len(out)))
+        return out
 
     def elastic_energy(self):
         """E = 1/2 u_n^T K u_n of the current state (device; state unchanged)."""

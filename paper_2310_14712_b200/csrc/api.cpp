@@ -51,7 +51,7 @@ static void free_ctx(sc_ctx* c) {
   void* ptrs[] = {c->d_voids, c->d_u[0], c->d_u[1], c->d_ntype, c->d_cell_class, c->d_dof_lat, c->d_out,
                   c->d_ft, c->d_step, c->d_flag, c->d_irr_lat, c->d_irr_invm, c->d_irr_fx, c->d_Kref,
                   c->d_c_lat, c->d_vc, c->d_ac, c->d_fxc, c->d_b, c->d_q, c->d_x, c->d_U,
-                  c->d_celem_cell, c->d_celem_kidx, c->d_celem_cidx, c->d_Kcut, c->d_Krefp, c->d_Y, c->d_rhs_ptr,
+                  c->d_celem_cell, c->d_celem_kidx, c->d_celem_cidx, c->d_Kcut, c->d_Krefp, c->d_cut_dt, c->d_Y, c->d_rhs_ptr,
                   c->d_rhs_idx, c->d_sn_c0, c->d_sn_w, c->d_sn_r, c->d_sn_aoff, c->d_sn_roff,
                   c->d_sn_uoff, c->d_sn_goff, c->d_R, c->d_gptr, c->d_gidx, c->d_items, c->fS.A,
                   c->fM.A, c->fS.d, c->fM.d, c->d_tmp, c->d_nitem, c->d_chptr, c->d_chidx, c->d_parent, c->d_solve_cnt,
@@ -510,6 +510,32 @@ extern "C" sc_status sc_read_c_state(sc_ctx* c, double* v_c, double* a_c, int64_
                               cudaMemcpyDeviceToHost, c->stream));
       SC_CUDA(cudaStreamSynchronize(c->stream));
       for (int64_t i = 0; i < c->n_cl; ++i) dst[c->c_canon[i]] = tmp[i];
+    }
+    return SC_OK;
+  } catch (const ScError& e) {
+    return fail(c, e);
+  }
+}
+
+extern "C" sc_status sc_cell_dt(sc_ctx* c, int32_t which, double* dt_cell, int64_t len) {
+  if (!c) return SC_ERR_STATE;
+  if (which != 0 && which != 1) {
+    c->err = "sc_cell_dt: which must be 0 (consistent mass) or 1 (HRZ-lumped mass)";
+    return SC_ERR_CONFIG;
+  }
+  if (!dt_cell || len < c->n_cells) {
+    c->err = "sc_cell_dt: output buffer too small (need prod(cells))";
+    return SC_ERR_CONFIG;
+  }
+  try {
+    SC_CUDA(cudaSetDevice(c->device));
+    std::vector<double> cut(2 * (size_t)c->n_cut);
+    if (c->n_cut)
+      SC_CUDA(cudaMemcpy(cut.data(), c->d_cut_dt, sizeof(double) * cut.size(), cudaMemcpyDeviceToHost));
+    size_t k = 0;   // cut cells in ascending cell order (c->cut_cells)
+    for (int64_t i = 0; i < c->n_cells; ++i) {
+      const int8_t cl = c->cell_class[i];
+      dt_cell[i] = cl == 0 ? c->dt_crit_uncut : (cl == 1 ? cut[2 * k++ + which] : 0.0);
     }
     return SC_OK;
   } catch (const ScError& e) {

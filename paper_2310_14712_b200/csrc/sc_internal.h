@@ -141,6 +141,7 @@ struct sc_ctx {
   int32_t* d_celem_cidx = nullptr;   // [e*nb + loc] c index (ND) or -1
   double* d_Kcut = nullptr;          // n_cut tiled-symmetric cut-cell K_e (step.cu k_celem; ct_ms doubles each)
   double* d_Krefp = nullptr;         // the uncut reference K_e, same storage
+  double* d_cut_dt = nullptr;        // [n_cut][2] cell-wise critical step (consistent, HRZ) of the cut cells
   int ct_T = 0, ct_nt = 0, ct_TS = 0;   // tiles: T rows, nt per dimension, TS doubles (stride)
   long long ct_ms = 0;                  // doubles per stored matrix
   double* d_Y = nullptr;             // n_celem x nb

@@ -414,6 +414,145 @@ static void upload_voids(sc_ctx* c) {
 
 // Classification, DOF partition, cut-cell matrices.  Fills host vectors in c and returns
 // the cut-cell mass matrices (host) for the factorisation.
+// ---- NEXT-2: cell-wise critical time steps (Fig.
+// fig:tCritsCircles, Table tab:criticaltimestepsizes): dt_e = 2 / sqrt(lambda_max(K_e, M_e))
+// of every cut cell, with its consistent mass (the "consistent SCM") and with its HRZ-lumped
+// mass (M~_ii = m_e / sum_k M_kk M_ii).  One CTA per cut cell, everything in
+// shared memory: HRZ: power iteration on D^-1/2 K D^-1/2; consistent: Cholesky M = L L^T
+// (packed), C = L^-1 K L^-T (two substitution sweeps), power iteration on C; the Rayleigh
+// quotient is iterated until it changes by <= 1e-15 relative for 8 consecutive iterations
+// (at most 20000).  out[2 e] = consistent, out[2 e + 1] = HRZ (0 if a pivot is not positive).
+__device__ double block_sum(double v, double* red) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += red[k];
+  return s;
+}
+
+// power iteration on the symmetric nb x nb matrix S (shared, row-major): lambda_max
+__device__ double power_max(const double* S, int nb, double* x, double* y, double* red) {
+  const int t = threadIdx.x;
+  for (int i = t; i < nb; i += blockDim.x) x[i] = 1.0 + 0.25 * (double)((i * 7919) % 97) / 97.0;
+  __syncthreads();
+  double lam = 0.0;
+  int stable = 0;
+  for (int it = 0; it < 20000 && stable < 8; ++it) {
+    double xy = 0.0, xx = 0.0, yy = 0.0;
+    for (int i = t; i < nb; i += blockDim.x) {
+      double a = 0.0;
+      for (int j = 0; j < nb; ++j) a = fma(S[i * nb + j], x[j], a);
+      y[i] = a;
+      xy += x[i] * a;
+      xx += x[i] * x[i];
+      yy += a * a;
+    }
+    xy = block_sum(xy, red);
+    xx = block_sum(xx, red + 8);
+    yy = block_sum(yy, red + 16);
+    const double l2 = xy / xx, sc = yy > 0.0 ? 1.0 / sqrt(yy) : 0.0;
+    stable = (fabs(l2 - lam) <= 1e-15 * fabs(l2)) ? stable + 1 : 0;
+    lam = l2;
+    for (int i = t; i < nb; i += blockDim.x) x[i] = y[i] * sc;
+    __syncthreads();
+  }
+  return lam;
+}
+
+__global__ void k_cell_dt(const double* __restrict__ Kfull, const double* __restrict__ Mfull, int nb, double* out) {
+  extern __shared__ double sh[];
+  const int np = nb * (nb + 1) / 2;
+  double* L = sh;                 // packed lower Cholesky factor, row i at i (i + 1) / 2
+  double* S = L + np;             // nb x nb
+  double* x = S + nb * nb;
+  double* y = x + nb;
+  double* d = y + nb;             // HRZ diagonal
+  double* red = d + nb;           // [24] reductions
+  const int e = blockIdx.x, t = threadIdx.x, nt = blockDim.x;
+  const double* K = Kfull + (size_t)e * nb * nb;
+  const double* M = Mfull + (size_t)e * nb * nb;
+  // ---- HRZ-lumped mass: m_e = sum_ij M_ij, trace = sum_k M_kk
+  double me = 0.0, tr = 0.0;
+  for (int q = t; q < nb * nb; q += nt) me += M[q];
+  for (int i = t; i < nb; i += nt) tr += M[(size_t)i * nb + i];
+  me = block_sum(me, red);
+  tr = block_sum(tr, red + 8);
+  for (int i = t; i < nb; i += nt) d[i] = 1.0 / sqrt(me / tr * M[(size_t)i * nb + i]);
+  __syncthreads();
+  for (int q = t; q < nb * nb; q += nt) S[q] = d[q / nb] * K[q] * d[q % nb];
+  __syncthreads();
+  const double lh = power_max(S, nb, x, y, red);
+  // ---- consistent mass: Cholesky of M (lower, packed), right-looking
+  for (int q = t; q < np; q += nt) {
+    int i = (int)((sqrt(8.0 * q + 1.0) - 1.0) * 0.5);
+    while (i * (i + 1) / 2 > q) --i;
+    while ((i + 1) * (i + 2) / 2 <= q) ++i;
+    const int j = q - i * (i + 1) / 2;
+    L[q] = M[(size_t)i * nb + j];
+  }
+  __syncthreads();
+  bool ok = true;
+  for (int k = 0; k < nb; ++k) {
+    const double pk = L[k * (k + 1) / 2 + k];
+    if (!(pk > 0.0)) ok = false;
+    const double lkk = sqrt(pk);
+    __syncthreads();
+    for (int i = k + 1 + t; i < nb; i += nt) L[i * (i + 1) / 2 + k] /= lkk;
+    if (t == 0) L[k * (k + 1) / 2 + k] = lkk;
+    __syncthreads();
+    // trailing update L_ij -= L_ik L_jk, k < j <= i
+    const int m = nb - k - 1;
+    for (int q = t; q < m * (m + 1) / 2; q += nt) {
+      int a = (int)((sqrt(8.0 * q + 1.0) - 1.0) * 0.5);
+      while (a * (a + 1) / 2 > q) --a;
+      while ((a + 1) * (a + 2) / 2 <= q) ++a;
+      const int b = q - a * (a + 1) / 2;
+      const int i = k + 1 + a, j = k + 1 + b;
+      L[i * (i + 1) / 2 + j] -= L[i * (i + 1) / 2 + k] * L[j * (j + 1) / 2 + k];
+    }
+    __syncthreads();
+  }
+  double lc = 0.0;
+  if (ok) {
+    for (int q = t; q < nb * nb; q += nt) S[q] = K[q];
+    __syncthreads();
+    // S <- L^-1 S (forward substitution, one column per thread)
+    for (int j = t; j < nb; j += nt)
+      for (int i = 0; i < nb; ++i) {
+        double a = S[i * nb + j];
+        for (int k = 0; k < i; ++k) a -= L[i * (i + 1) / 2 + k] * S[k * nb + j];
+        S[i * nb + j] = a / L[i * (i + 1) / 2 + i];
+      }
+    __syncthreads();
+    // S <- S L^-T (forward substitution on the rows, one row per thread)
+    for (int i = t; i < nb; i += nt)
+      for (int j = 0; j < nb; ++j) {
+        double a = S[i * nb + j];
+        for (int k = 0; k < j; ++k) a -= S[i * nb + k] * L[j * (j + 1) / 2 + k];
+        S[i * nb + j] = a / L[j * (j + 1) / 2 + j];
+      }
+    __syncthreads();
+    // symmetrise (rounding) and iterate
+    for (int q = t; q < nb * nb; q += nt) {
+      const int i = q / nb, j = q % nb;
+      if (i < j) {
+        const double a = 0.5 * (S[i * nb + j] + S[j * nb + i]);
+        S[i * nb + j] = a;
+        S[j * nb + i] = a;
+      }
+    }
+    __syncthreads();
+    lc = power_max(S, nb, x, y, red);
+  }
+  if (t == 0) {
+    out[2 * (size_t)e] = (ok && lc > 0.0) ? 2.0 / sqrt(lc) : 0.0;
+    out[2 * (size_t)e + 1] = lh > 0.0 ? 2.0 / sqrt(lh) : 0.0;
+  }
+}
+
 void setup_device_geometry(sc_ctx* c) {
   upload_voids(c);
   const GridP& g = c->g;
@@ -512,6 +651,14 @@ void setup_device_geometry(sc_ctx* c) {
         g, c->d_voids, nv, d_cc, d_slots, d_leaves, d_nleaves, cap, d_gll, d_gx, d_gw, d_tq, c->alpha, c->rho,
         c->c * c->c, nb, nbp, c->d_Kcut, d_M);
     SC_CUDA(cudaGetLastError());
+    // cell-wise critical steps of the cut cells (consistent, HRZ), 2 per cut cell
+    {
+      SC_CUDA(cudaMalloc(&c->d_cut_dt, sizeof(double) * 2 * c->n_cut));
+      const size_t sm = sizeof(double) * ((size_t)nb * (nb + 1) / 2 + (size_t)nb * nb + 3 * (size_t)nb + 24);
+      SC_CUDA(cudaFuncSetAttribute(k_cell_dt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      k_cell_dt<<<(unsigned)c->n_cut, 128, sm, c->stream>>>(c->d_Kcut, d_M, nb, c->d_cut_dt);
+      SC_CUDA(cudaGetLastError());
+    }
     c->Kcut_host.resize(mat);
     c->Mcut_host.resize(mat);
     SC_CUDA(cudaMemcpyAsync(c->Kcut_host.data(), c->d_Kcut, sizeof(double) * mat, cudaMemcpyDeviceToHost, c->stream));
