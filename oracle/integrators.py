@@ -194,6 +194,64 @@ def cdm_consistent(pr, dt, n_steps, f_t, u0, v0=None, observer=None):
     return u
 
 
+def _ft_frac(f_t, k, theta):
+    """f_t at t_k + theta dt from the supplied samples f_t(k dt): linear interpolation
+    (reading LF4; theta = 0 is the sample itself)."""
+    if theta == 0.0:
+        return _ft(f_t, k)
+    return (1.0 - theta) * _ft(f_t, k) + theta * _ft(f_t, k + 1)
+
+
+def leapfrog(pr, dt, n_steps, f_t, u0, m, coupling="interpolated", v0=None, observer=None):
+    """Leap-frog substepping of the cut DOFs ("the cut cells are integrated
+    in time with a finer time step size dt_fine = dt_coarse / m"; the details are deferred to
+    [NAC22, meineMA], not available - DESIGN.md readings LF1-LF4):
+    * LF1: the d DOFs take the CDM step of the IMEX method with dt (diagonal M^dd),
+      reading u_n (including u^c_n);
+    * LF2: the c DOFs take m CDM steps with dt_f = dt/m on the consistent M^cc (factored once,
+      P:583): u^c_{k+1} = 2u^c_k - u^c_{k-1} + dt_f^2 (M^cc)^-1 (f_t(t_k) f^c - (K w_k)_c),
+      w_k = [u^d(t_k); u^c_k];
+    * LF3 (the coupling rule, unstated): u^d(t_k) = u^d_n ("frozen") or the linear
+      interpolation u^d_n + (k/m)(u^d_{n+1} - u^d_n) ("interpolated");
+    * LF4: f_t at the fine times by linear interpolation of the supplied samples f_t(k dt).
+    Start: a_0 blockwise as imex (reading C3); u^d_{-1} with dt, u^c_{-1} with dt_f."""
+    n = pr.n
+    u = np.array(u0, dtype=np.float64, copy=True)
+    v0 = np.zeros(n) if v0 is None else np.asarray(v0, dtype=np.float64)
+    a0 = startup(pr, dt, f_t, u, v0)
+    Id, Ic = pr.I_d, pr.I_c
+    dtf = dt / m
+    u_prev_d = u[Id] - dt * v0[Id] + 0.5 * dt * dt * a0[Id]
+    uc = u[Ic].copy()
+    uc_prev = u[Ic] - dtf * v0[Ic] + 0.5 * dtf * dtf * a0[Ic]
+    solve_M = _factor(pr.M_cc) if len(Ic) else None
+    interp = coupling == "interpolated"
+    if coupling not in ("interpolated", "frozen"):
+        raise ValueError(coupling)
+    for k in range(n_steps):
+        # LF1: the d CDM step
+        r_d = _ft(f_t, k) * pr.f_x[Id] - pr.Ku(u)[Id]
+        u_d_new = 2.0 * u[Id] - u_prev_d + dt * dt * r_d / pr.M_dd
+        # LF2/LF3: m fine CDM steps of the c DOFs
+        if len(Ic):
+            w = np.empty(n)
+            for j in range(m):
+                th = j / m
+                w[Id] = u[Id] + th * (u_d_new - u[Id]) if interp else u[Id]
+                w[Ic] = uc
+                r_c = _ft_frac(f_t, k, th) * pr.f_x[Ic] - pr.Ku(w)[Ic]
+                uc_new = 2.0 * uc - uc_prev + dtf * dtf * solve_M(r_c)
+                uc_prev = uc
+                uc = uc_new
+        u_prev_d = u[Id].copy()
+        u[Id] = u_d_new
+        if len(Ic):
+            u[Ic] = uc
+        if observer is not None:
+            observer(k + 1, u)
+    return u
+
+
 def trapezoidal(pr, dt, n_steps, f_t, u0, v0=None, observer=None, return_v=False):
     """Implicit trapezoidal Newmark on all DOFs (reading C2)."""
     n = pr.n
