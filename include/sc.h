@@ -88,7 +88,13 @@ typedef struct {
                          2 trapezoidal Newmark on all DOFs (every DOF implicit, S
                            factored over the whole mesh: small problems);
                          3 CDM on the consistent SCM (M^cc solved each step
-                           with its factor; dt below the consistent critical step) */
+                           with its factor; dt below the consistent critical step);
+                         4 leap-frog substepping: the d DOFs as in 0 (CDM, dt), the c
+                           DOFs lf_m CDM steps of dt/lf_m on the consistent M^cc per step
+                           (readings LF1-LF4) */
+  int32_t lf_m;        /* integrator 4: substeps m >= 1 (ignored otherwise) */
+  int32_t lf_coupling; /* integrator 4: d values during the substeps, 0 = linear interpolation
+                          between u^d_n and u^d_{n+1}, 1 = frozen at u^d_n (reading LF3) */
 } sc_geometry;
 
 /* Separable point source f(x,t) = f_t(t) delta(x - x_s) (reading C11):

@@ -31,7 +31,7 @@ class sc_geometry(ctypes.Structure):
     _fields_ = [("n_voids", ctypes.c_int32), ("voids", ctypes.POINTER(sc_void)),
                 ("tree_depth", ctypes.c_int32), ("lattice_s", ctypes.c_int32),
                 ("fill_eps", ctypes.c_double), ("rho", ctypes.c_double), ("c", ctypes.c_double),
-                ("integrator", ctypes.c_int32)]
+                ("integrator", ctypes.c_int32), ("lf_m", ctypes.c_int32), ("lf_coupling", ctypes.c_int32)]
 
 
 class sc_source(ctypes.Structure):
@@ -148,8 +148,9 @@ class Solver:
                 arr[i].b = v["b"]
         geo = sc_geometry(len(vs), arr, geometry.get("tree_depth", 2), geometry.get("lattice_s", 4),
                           geometry.get("fill_eps", 1e-10), geometry.get("rho", 1.0), geometry.get("c", 1.0),
-                          {"imex": 0, "cdm_hrz": 1, "trapezoidal": 2, "cdm_consistent": 3}[
-                              geometry.get("integrator", "imex")])
+                          {"imex": 0, "cdm_hrz": 1, "trapezoidal": 2, "cdm_consistent": 3, "leapfrog": 4}[
+                              geometry.get("integrator", "imex")], int(geometry.get("lf_m", 1)),
+                          {"interpolated": 0, "frozen": 1}[geometry.get("lf_coupling", "interpolated")])
         src = None
         self._ft = None
         if source is not None:
@@ -331,6 +332,8 @@ def from_config(cfg, f_t=None, stream=None, device=None, set_initial=True, rank=
         src = {"x": cfg["source"]["x"], "f_t": f_t}
     geo = {k: cfg[k] for k in ("voids", "tree_depth", "lattice_s", "fill_eps", "rho", "c")}
     geo["integrator"] = cfg.get("integrator", "imex")
+    geo["lf_m"] = cfg.get("lf_m", 1)
+    geo["lf_coupling"] = cfg.get("lf_coupling", "interpolated")
     s = Solver(cfg, cfg["p"], cfg["alpha"], geo, cfg["dt"], source=src, stream=stream, device=device,
                rank=rank, world=world, nccl_id=nccl_id)
     s._n_cells = int(np.prod(cfg["cells"]))

@@ -167,8 +167,15 @@ extern "C" sc_status sc_setup(const sc_grid* grid, int32_t p, double alpha, cons
     c->c = geom->c;
     c->dt = dt;
     c->fill_eps = geom->fill_eps;
-    if (geom->integrator < 0 || geom->integrator > 3) throw ScError(SC_ERR_CONFIG, "integrator must be 0..3");
+    if (geom->integrator < 0 || geom->integrator > 4) throw ScError(SC_ERR_CONFIG, "integrator must be 0..4");
     c->integrator = geom->integrator;
+    if (c->integrator == 4) {
+      if (geom->lf_m < 1 || geom->lf_m > 64) throw ScError(SC_ERR_CONFIG, "leap-frog: lf_m must be in [1, 64]");
+      if (geom->lf_coupling != 0 && geom->lf_coupling != 1) throw ScError(SC_ERR_CONFIG, "leap-frog: lf_coupling 0 or 1");
+      if (dist && dist->world > 1) throw ScError(SC_ERR_CONFIG, "leap-frog: one rank only");
+      c->lf_m = geom->lf_m;
+      c->lf_coupling = geom->lf_coupling;
+    }
     for (int i = 0; i < geom->n_voids; ++i) {
       DVoid v;
       std::memset(&v, 0, sizeof(v));

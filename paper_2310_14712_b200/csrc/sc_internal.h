@@ -88,7 +88,9 @@ struct sc_ctx {
   GridP g;
   int nb = 0;               // (p+1)^dim
   double alpha = 0, rho = 1, c = 1, dt = 0, fill_eps = 1e-10;
-  int integrator = 0;       // 0 Newmark IMEX; 1 CDM with HRZ-lumped cut cells (NEXT-1(c))
+  int integrator = 0;       // 0 Newmark IMEX; 1 CDM with HRZ-lumped cut cells (NEXT-1(c)); 4 leap-frog
+  int lf_m = 1;             // integrator 4: substeps of the cut DOFs per step
+  int lf_coupling = 0;      // integrator 4: 0 interpolated d values, 1 frozen (reading LF3)
   double* d_mc = nullptr;   // integrator 1: HRZ-lumped mass of the c DOFs (ND order)
   std::vector<DVoid> voids;
   int64_t n_cells = 0, n_lat = 0;

@@ -196,7 +196,9 @@ __device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
 
 // (a3)+(a4) c-element products Y[e][i] = sum_j K_e[i][j] w_j, one CTA per element.
 // mode 0 (step): w = predictor u~^c on c nodes, u^d_{n+1} (buffer B) elsewhere;
-// mode 1 (start): w = A everywhere.
+// mode 1 (start): w = A everywhere;
+// mode 2 (leap-frog substep, integrator 4): w = u^c_k (compact, vc) on c nodes, the d values
+// A + theta (B - A) elsewhere (reading LF3: theta = k/m interpolated, 0 frozen).
 // The stored tiles stream through shared memory (cp.async, two buffers); thread t (block I =
 // t / T, row a = t % T) owns output t and adds, per tile (I0, J0): the row sum of row a when
 // I = I0 (K_IJ w_J) and the column sum of column a when I = J0 > I0 (K_JI^T w_J) - every
@@ -206,7 +208,7 @@ __global__ void k_celem(int mode, const double* __restrict__ A, const double* __
                         const int32_t* __restrict__ ecell, const int32_t* __restrict__ ekidx,
                         const int32_t* __restrict__ ecidx, const double* __restrict__ Kp,
                         const double* __restrict__ Krefp, double* __restrict__ Y, int ne, int nb, int T, int nt,
-                        int TS, long long ms, GridP g) {
+                        int TS, long long ms, GridP g, double theta) {
   extern __shared__ double sm[];
   const int wlen = (nt * T + 1) & ~1;
   double* w = sm;              // [wlen]
@@ -245,6 +247,9 @@ __global__ void k_celem(int mode, const double* __restrict__ A, const double* __
         if (g.dim > 2) gl += g.nl[0] * g.nl[1] * (ci[2] * g.p + l2);
         if (mode == 1) {
           v = A[gl];
+        } else if (mode == 2) {
+          const int cc = ecidx[(size_t)e * nb + j];
+          v = cc >= 0 ? vc[cc] : fma(theta, B[gl] - A[gl], A[gl]);
         } else {
           const int cc = ecidx[(size_t)e * nb + j];
           v = cc >= 0 ? A[gl] + dt * vc[cc] + 0.25 * dt * dt * ac[cc] : B[gl];
@@ -290,12 +295,15 @@ __global__ void k_celem(int mode, const double* __restrict__ A, const double* __
 __global__ void k_crhs(double* __restrict__ b, const double* __restrict__ fxc, const int32_t* __restrict__ ptr,
                        const int32_t* __restrict__ idx, const double* __restrict__ Y, int nc,
                        const double* __restrict__ ft, long long n_t, const long long* step, int off,
-                       const double* __restrict__ dscale, double fsc = 1.0) {
+                       const double* __restrict__ dscale, double fsc = 1.0, double theta = 0.0) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nc) return;
   double s = 0.0;
   for (int q = ptr[i]; q < ptr[i + 1]; ++q) s += Y[idx[q]];
-  const double r = fsc * ft_at(ft, n_t, step, off) * fxc[i] - s;
+  // f_t at t_{n+off} (+ theta dt: linear interpolation of the samples, leap-frog reading LF4)
+  const double f0 = ft_at(ft, n_t, step, off);
+  const double ftv = theta == 0.0 ? f0 : (1.0 - theta) * f0 + theta * ft_at(ft, n_t, step, off + 1);
+  const double r = fsc * ftv * fxc[i] - s;
   b[i] = dscale ? dscale[i] * r : r;   // D r^c (scaled system) or r^c
 }
 
@@ -343,6 +351,36 @@ __global__ void k_start_hrz(const double* __restrict__ A, double* __restrict__ B
   if (i >= nc) return;
   const int32_t L = clat[i];
   B[L] = A[L] - (vlat ? dt * vlat[L] : 0.0) + 0.5 * dt * dt * r[i] / mc[i];
+}
+
+// leap-frog substep of the c DOFs (integrator 4, reading LF2): u^c_{k+1} = 2u^c_k - u^c_{k-1}
+// + dt_f^2 a_k with M^cc a_k = r^c (the solve returns x, a = D x); uc = u^c_k, up = u^c_{k-1}
+__global__ void k_lf_sub(double* __restrict__ uc, double* __restrict__ up, const double* __restrict__ x,
+                         const double* __restrict__ dscale, int nc, double dtf2, int* flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nc) return;
+  const double cur = uc[i];
+  const double un = 2.0 * cur - up[i] + dtf2 * (dscale[i] * x[i]);
+  up[i] = cur;
+  uc[i] = un;
+  if (!isfinite(un)) atomicExch(flag, 1);
+}
+// u^c_{n+1} into the lattice buffer
+__global__ void k_lf_store(const double* __restrict__ uc, double* __restrict__ B, const int32_t* __restrict__ clat,
+                           int nc) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nc) B[clat[i]] = uc[i];
+}
+// start of integrator 4 at the c DOFs (fine level): u^c_0 and u^c_{-1} = u^c_0 - dt_f v_0 +
+// dt_f^2/2 a_0 (a_0 = D x from the M solve of the start)
+__global__ void k_start_lf(const double* __restrict__ A, double* __restrict__ uc, double* __restrict__ up,
+                           const double* __restrict__ x, const double* __restrict__ dscale,
+                           const double* __restrict__ vlat, const int32_t* __restrict__ clat, int nc, double dtf) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nc) return;
+  const int32_t L = clat[i];
+  uc[i] = A[L];
+  up[i] = A[L] - (vlat ? dtf * vlat[L] : 0.0) + 0.5 * dtf * dtf * (dscale[i] * x[i]);
 }
 
 // M^{-1} K x at the c DOFs with the consistent M^cc (power iteration of integrator 3):
@@ -528,14 +566,15 @@ void launch_explicit(sc_ctx* c, const double* U, const double* Pv, double* out, 
   SC_CUDA(cudaGetLastError());
 }
 
-static void launch_celem(sc_ctx* c, int mode, const double* A, const double* B, cudaStream_t st) {
+static void launch_celem(sc_ctx* c, int mode, const double* A, const double* B, cudaStream_t st,
+                         double theta = 0.0, const double* vc = nullptr) {
   if (c->n_celem == 0) return;
   const int nthr = ((c->ct_nt * c->ct_T + 31) / 32) * 32;
   const size_t smem = sizeof(double) * (((c->ct_nt * c->ct_T + 1) & ~1) + 2 * (size_t)c->ct_TS);
-  k_celem<<<(unsigned)c->n_celem, nthr, smem, st>>>(mode, A, B, c->d_vc, c->d_ac, c->dt, c->d_celem_cell,
+  k_celem<<<(unsigned)c->n_celem, nthr, smem, st>>>(mode, A, B, vc ? vc : c->d_vc, c->d_ac, c->dt, c->d_celem_cell,
                                                      c->d_celem_kidx, c->d_celem_cidx, c->d_Kcut, c->d_Krefp, c->d_Y,
                                                      (int)c->n_celem, c->nb, c->ct_T, c->ct_nt, c->ct_TS, c->ct_ms,
-                                                     c->g);
+                                                     c->g, theta);
   SC_CUDA(cudaGetLastError());
 }
 
@@ -578,6 +617,21 @@ static void enqueue_c_part(sc_ctx* c, const double* A, double* B, cudaStream_t s
                                                               (int)c->n_cl, c->d_ft, c->n_t, c->d_step, 0, nullptr);
     k_cdm_c<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, st>>>(A, B, c->d_b, c->d_mc, c->d_c_lat, (int)c->n_cl,
                                                                dt * dt, c->d_flag);
+  } else if (c->n_cl > 0 && c->integrator == 4) {
+    // leap-frog: m CDM substeps of the c DOFs with dt_f = dt/m on the consistent M^cc
+    // (readings LF2-LF4); B already holds u^d_{n+1}; vc = u^c_k, ac = u^c_{k-1} (fine level)
+    const int m = c->lf_m;
+    const double dtf = dt / m;
+    const unsigned gb = (unsigned)((c->n_cl + 255) / 256);
+    for (int j = 0; j < m; ++j) {
+      const double th = (double)j / m;
+      launch_celem(c, 2, A, B, st, c->lf_coupling == 0 ? th : 0.0, c->d_vc);
+      k_crhs<<<gb, 256, 0, st>>>(c->d_b, c->d_fxc, c->d_rhs_ptr, c->d_rhs_idx, c->d_Y, (int)c->n_cl, c->d_ft, c->n_t,
+                                 c->d_step, 0, c->fM.d, 1.0, th);
+      launch_solve(c, c->fM, st);
+      k_lf_sub<<<gb, 256, 0, st>>>(c->d_vc, c->d_ac, c->d_x, c->fM.d, (int)c->n_cl, dtf * dtf, c->d_flag);
+    }
+    k_lf_store<<<gb, 256, 0, st>>>(c->d_vc, B, c->d_c_lat, (int)c->n_cl);
   } else if (c->n_cl > 0 && c->integrator == 3) {
     // CDM on the consistent SCM: M^cc a^c_n = f_t(t_n) f_x^c - (K u_n)_c with the M factor
     launch_celem(c, 1, A, A, st);
@@ -682,7 +736,10 @@ void build_graphs(sc_ctx* c) {
   }
   // kernels per step: explicit (+ near when pipelined) + irregular + advance + c part (+ pack)
   c->kernels_per_step = 1 + (c->pipelined && c->n_near > 0 ? 1 : 0) + (c->n_irr > 0) + 1 + (c->world > 1);
-  if (c->n_c > 0) c->kernels_per_step += c->integrator == 1 ? 3 : 3 + (c->n_items > 0 ? 1 : 0);
+  if (c->n_c > 0)
+    c->kernels_per_step += c->integrator == 1   ? 3
+                           : c->integrator == 4 ? 4 * c->lf_m + 1
+                                                : 3 + (c->n_items > 0 ? 1 : 0);
 }
 
 // near-d tile list: tiles of the explicit kernel that own at least one type-4 node (a tile
@@ -860,8 +917,12 @@ void run_startup(sc_ctx* c, const double* u0, const double* v0) {
     if (c->integrator == 3)
       k_start_cons<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, c->stream>>>(A, B, c->d_x, c->fM.d, vlat, c->d_c_lat,
                                                                              (int)c->n_cl, dt);
-    k_start_c<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, c->stream>>>(c->d_ac, c->d_vc, c->d_x, vlat, c->d_c_lat,
-                                                                         (int)c->n_cl, c->fM.d);
+    if (c->integrator == 4)   // leap-frog: u^c_0, u^c_{-1} at the fine level
+      k_start_lf<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, c->stream>>>(A, c->d_vc, c->d_ac, c->d_x, c->fM.d, vlat,
+                                                                           c->d_c_lat, (int)c->n_cl, dt / c->lf_m);
+    else
+      k_start_c<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, c->stream>>>(c->d_ac, c->d_vc, c->d_x, vlat, c->d_c_lat,
+                                                                           (int)c->n_cl, c->fM.d);
   }
   SC_CUDA(cudaGetLastError());
   SC_CUDA(cudaStreamSynchronize(c->stream));
