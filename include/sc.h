@@ -97,15 +97,20 @@ typedef struct {
                           between u^d_n and u^d_{n+1}, 1 = frozen at u^d_n (reading LF3) */
 } sc_geometry;
 
-/* Separable point source f(x,t) = f_t(t) delta(x - x_s) (reading C11):
- * f_x,i = alpha(x_s) N_i(x_s) in the lowest-index non-empty cell containing x_s.
- * f_t[k] = f_t(k*dt) for k < n_t (host array, copied); f_t = 0 beyond n_t.
- * kind 0 = no source (f_t ignored), 1 = point source. */
+/* Separable source f(x,t) = f_t(t) f_x(x), f_t[k] = f_t(k*dt) for k < n_t (host
+ * array, copied), f_t = 0 beyond n_t.  kind 0 = no source (f_t ignored);
+ * kind 1 = point source at x (reading C11): f_x,i = alpha(x_s) N_i(x_s) in the lowest-index
+ *   non-empty cell containing x_s;
+ * kind 2 = the paper's Gaussian bell (Eq. eq:fx): f_x(x) = amp exp(-|x - x|^2 /
+ *   (2 sigma^2)), f_x,i = int alpha f_x N_i with (p+1)^d Gauss points per cell / spacetree leaf
+ *   (P:461-463), assembled in ascending cell order (deterministic); sigma > 0. */
 typedef struct {
   int32_t kind;
   double x[3];
   int64_t n_t;
   const double* f_t;
+  double sigma; /* kind 2 */
+  double amp;   /* kind 2 */
 } sc_source;
 
 /* Distribution: NULL => one GPU (current device, current stream semantics below).

@@ -159,6 +159,32 @@ def point_load(cfg, cl, x):
     raise ValueError("source point is outside every non-empty cell")
 
 
+def bell_load(cfg, cl):
+    """f_x,i = int alpha f_x N_i for the Gaussian bell f_x of PAPER.md P:851-853 (Eq. eq:fx),
+    amp exp(-|x - x_s|^2 / (2 sigma^2)), assembled over every non-empty cell (Gauss points on
+    the spacetree leaves of cut cells)."""
+    from .elements import cell_load, gaussian_bell
+    src = cfg["source"]
+    d = cfg["dim"]
+    xs = np.asarray(src["x"][:d], dtype=np.float64)
+    fx = lambda X: gaussian_bell(X, xs, src["sigma"], src["amp"])   # noqa: E731
+    grid = cl.grid
+    f = np.zeros(cl.n_dof)
+    root = (np.zeros((1,), dtype=np.int64), np.zeros((1, d), dtype=np.int64))
+    for ci in range(len(cl.cell_class)):
+        if cl.cell_class[ci] == EMPTY:
+            continue
+        cell = cl.cell_idx[ci]
+        if cl.cell_class[ci] == UNCUT:
+            fe = cell_load(grid, cfg["voids"], cell, root[0], root[1], cfg["p"], cfg["alpha"], fx,
+                           phys=np.ones((cfg["p"] + 1) ** d, dtype=bool))
+        else:
+            levels, a, ph = cl.trees[int(ci)]
+            fe = cell_load(grid, cfg["voids"], cell, levels, a, cfg["p"], cfg["alpha"], fx, phys=ph)
+        np.add.at(f, cl.dof_of_lattice[cl.enodes[ci]], fe)
+    return f
+
+
 def point_values(cfg, cl, x):
     """Receiver weights: u(x) = sum_i N_i(x) u_i with the basis of the lowest-index
     non-empty cell containing x (the evaluation point_load uses, without alpha; SURVEY
@@ -277,8 +303,10 @@ def build_system(cfg, mode="sparse", cl=None):
     else:
         sysm.K = None
         sysm.M = None
-    # load vector
-    if cfg.get("source") is not None:
+    # load vector: point load (reading C11) or the paper's Gaussian bell (Eq. eq:fx)
+    if cfg.get("source") is not None and cfg["source"].get("kind", "point") == "bell":
+        sysm.f_x = bell_load(cfg, cl)
+    elif cfg.get("source") is not None:
         sysm.f_x = point_load(cfg, cl, cfg["source"]["x"])
     else:
         sysm.f_x = np.zeros(n)

@@ -114,3 +114,43 @@ def eval_basis_at(grid, cell, x, p):
     for k in range(1, d):
         out = np.kron(vals[k], out)
     return out
+
+
+def gaussian_bell(X, xs, sigma, amp):
+    """f_x(x) = amp exp(-|x - x_s|^2 / (2 sigma^2)) (Eq. eq:fx; the paper
+    has amp = 10, sigma_s = 6e-2 m)."""
+    d = len(xs)
+    r2 = np.sum((X[:, :d] - np.asarray(xs, dtype=np.float64)[None, :]) ** 2, axis=1)
+    return amp * np.exp(-r2 / (2.0 * sigma * sigma))
+
+
+def cell_load(grid, voids, cell, levels, a, p, alpha, fx, phys=None):
+    """Element load vector f_i = int alpha f_x N_i (Eq. eq:f) with (p+1)^d Gauss
+    points per spacetree leaf (the load is Gauss-integrated in cut and uncut cells; an
+    uncut cell is the single leaf (levels [0], a [0...]) with alpha = 1).  fx(X) -> values."""
+    d = grid["dim"]
+    nodes, _ = gll_rule(p)
+    g, wg = gauss_rule(p + 1)
+    n = p + 1
+    h = [(grid["hi"][k] - grid["lo"][k]) / grid["cells"][k] for k in range(d)]
+    X = leaf_gauss_points(grid, cell, levels, a, g)
+    if phys is None:
+        phys = is_physical(X, voids)
+    a_q = np.where(phys, 1.0, alpha)
+    L = len(levels)
+    scale = 1.0 / (2.0 ** levels)
+    V, Wk = [], []
+    for k in range(d):
+        xi = -1.0 + 2.0 * (a[:, k][:, None] + (g[None, :] + 1.0) * 0.5) * scale[:, None]
+        v, _ = lagrange(nodes, xi.reshape(-1))
+        V.append(v.reshape(L, n, n))
+        Wk.append(wg[None, :] * scale[:, None] * (h[k] / 2.0))
+    if d == 1:
+        N, w = V[0].reshape(L * n, n), Wk[0].reshape(L * n)
+    elif d == 2:
+        N = np.einsum("lqj,lpi->lqpji", V[1], V[0]).reshape(L * n * n, n * n)
+        w = np.einsum("lb,la->lba", Wk[1], Wk[0]).reshape(L * n * n)
+    else:
+        N = np.einsum("lrk,lqj,lpi->lrqpkji", V[2], V[1], V[0]).reshape(L * n ** 3, n ** 3)
+        w = np.einsum("lc,lb,la->lcba", Wk[2], Wk[1], Wk[0]).reshape(L * n ** 3)
+    return N.T @ (w * a_q * fx(X))

@@ -36,7 +36,7 @@ class sc_geometry(ctypes.Structure):
 
 class sc_source(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("x", ctypes.c_double * 3), ("n_t", ctypes.c_int64),
-                ("f_t", ctypes.POINTER(ctypes.c_double))]
+                ("f_t", ctypes.POINTER(ctypes.c_double)), ("sigma", ctypes.c_double), ("amp", ctypes.c_double)]
 
 
 class sc_dist(ctypes.Structure):
@@ -157,7 +157,9 @@ class Solver:
             ft = np.ascontiguousarray(source["f_t"], dtype=np.float64)
             self._ft = ft
             src = sc_source()
-            src.kind = 1
+            src.kind = 2 if source.get("kind", "point") == "bell" else 1
+            src.sigma = float(source.get("sigma", 0.0))
+            src.amp = float(source.get("amp", 0.0))
             for k in range(3):
                 src.x[k] = source["x"][k] if k < len(source["x"]) else 0.0
             src.n_t = len(ft)
@@ -330,6 +332,9 @@ def from_config(cfg, f_t=None, stream=None, device=None, set_initial=True, rank=
             from sc_inputs import source_signal
             f_t = source_signal(cfg)
         src = {"x": cfg["source"]["x"], "f_t": f_t}
+        for k in ("kind", "sigma", "amp"):
+            if k in cfg["source"]:
+                src[k] = cfg["source"][k]
     geo = {k: cfg[k] for k in ("voids", "tree_depth", "lattice_s", "fill_eps", "rho", "c")}
     geo["integrator"] = cfg.get("integrator", "imex")
     geo["lf_m"] = cfg.get("lf_m", 1)

@@ -49,7 +49,7 @@ static void free_ctx(sc_ctx* c) {
   }
   destroy_graphs(c);
   void* ptrs[] = {c->d_voids, c->d_u[0], c->d_u[1], c->d_ntype, c->d_cell_class, c->d_dof_lat, c->d_out,
-                  c->d_ft, c->d_step, c->d_flag, c->d_irr_lat, c->d_irr_invm, c->d_irr_fx, c->d_Kref,
+                  c->d_ft, c->d_step, c->d_flag, c->d_irr_lat, c->d_irr_invm, c->d_irr_fx, c->d_load_lat, c->d_load_fxm, c->d_Kref,
                   c->d_c_lat, c->d_vc, c->d_ac, c->d_fxc, c->d_b, c->d_q, c->d_x, c->d_U,
                   c->d_celem_cell, c->d_celem_kidx, c->d_celem_cidx, c->d_Kcut, c->d_Krefp, c->d_cut_dt, c->d_Y, c->d_rhs_ptr,
                   c->d_rhs_idx, c->d_sn_c0, c->d_sn_w, c->d_sn_r, c->d_sn_aoff, c->d_sn_roff,
@@ -85,7 +85,8 @@ static void validate(const sc_grid* grid, int32_t p, double alpha, const sc_geom
   if (geom->tree_depth < 0 || geom->tree_depth > 12) throw ScError(SC_ERR_CONFIG, "tree_depth in [0, 12]");
   if (geom->lattice_s < 1 || geom->lattice_s > 16) throw ScError(SC_ERR_CONFIG, "lattice_s in [1, 16]");
   if (!(geom->rho > 0.0) || !(geom->c > 0.0)) throw ScError(SC_ERR_CONFIG, "rho and c must be positive");
-  if (src && src->kind == 1 && (src->n_t < 0 || (src->n_t > 0 && !src->f_t)))
+  if (src && (src->kind < 0 || src->kind > 2)) throw ScError(SC_ERR_CONFIG, "source kind must be 0, 1 or 2");
+  if (src && src->kind >= 1 && (src->n_t < 0 || (src->n_t > 0 && !src->f_t)))
     throw ScError(SC_ERR_CONFIG, "invalid source signal");
   for (int i = 0; i < geom->n_voids; ++i) {
     const sc_void& v = geom->voids[i];
@@ -189,9 +190,14 @@ extern "C" sc_status sc_setup(const sc_grid* grid, int32_t p, double alpha, cons
       v.b = s.b;
       c->voids.push_back(v);
     }
-    if (src && src->kind == 1) {
-      c->src_kind = 1;
+    if (src && (src->kind == 1 || src->kind == 2)) {
+      c->src_kind = src->kind;
       for (int k = 0; k < 3; ++k) c->src_x[k] = src->x[k];
+      if (src->kind == 2) {
+        if (!(src->sigma > 0.0) || !std::isfinite(src->amp)) throw ScError(SC_ERR_CONFIG, "bell source: sigma > 0");
+        c->src_sigma = src->sigma;
+        c->src_amp = src->amp;
+      }
     }
     host_reference(c);
     device_upload_reference(c);
@@ -207,7 +213,7 @@ extern "C" sc_status sc_setup(const sc_grid* grid, int32_t p, double alpha, cons
     SC_CUDA(cudaMalloc(&c->d_dof_lat, sizeof(int64_t) * std::max<int64_t>(1, c->n_dof)));
     SC_CUDA(cudaMemcpy(c->d_dof_lat, c->dof_lat.data(), sizeof(int64_t) * c->n_dof, cudaMemcpyHostToDevice));
     SC_CUDA(cudaMalloc(&c->d_out, sizeof(double) * std::max<int64_t>(1, c->n_dof)));
-    c->n_t = (src && src->kind == 1) ? src->n_t : 0;
+    c->n_t = (src && (src->kind == 1 || src->kind == 2)) ? src->n_t : 0;
     SC_CUDA(cudaMalloc(&c->d_ft, sizeof(double) * std::max<int64_t>(1, c->n_t)));
     if (c->n_t) SC_CUDA(cudaMemcpy(c->d_ft, src->f_t, sizeof(double) * c->n_t, cudaMemcpyHostToDevice));
     // algorithmic bytes per step

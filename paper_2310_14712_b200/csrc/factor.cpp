@@ -17,6 +17,7 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <map>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -333,6 +334,91 @@ void point_weights(const sc_ctx* c, const double* x, bool with_alpha,
   throw ScError(SC_ERR_CONFIG, "point lies only in empty cells");
 }
 
+// Gaussian-bell load (source kind 2, Eq. eq:fx, P:444-448 Eq. eq:f):
+// f_x,i = int alpha f_x N_i, f_x = amp exp(-|x - x_s|^2 / (2 sigma^2)), with (p+1)^d Gauss
+// points per uncut cell (alpha = 1) and per spacetree leaf of a cut cell (the leaves the device
+// built; pointwise alpha with the classifier's arithmetic, C17), accumulated in ascending cell
+// order (deterministic).  Cells farther than 40 sigma from x_s contribute exact zeros
+// (exp(-800) underflows) and are skipped.  out = (lattice index, value), ascending lattice.
+void bell_weights(const sc_ctx* c, std::vector<std::pair<int64_t, double>>& out) {
+  const GridP& g = c->g;
+  const int d = g.dim, n1 = g.p + 1, nb = c->nb;
+  const double sig = c->src_sigma, amp = c->src_amp;
+  const double rcut = 40.0 * sig;
+  std::vector<double> tq(n1);
+  for (int i = 0; i < n1; ++i) tq[i] = (c->gau_x[i] + 1.0) * 0.5;
+  std::map<int64_t, double> acc;
+  std::vector<double> fe(nb);
+  int64_t kcut = 0;   // running index into the ascending cut-cell list
+  for (int64_t cl = 0; cl < c->n_cells; ++cl) {
+    const int8_t cls = c->cell_class[cl];
+    const bool is_cut = cls == 1;
+    const int64_t my_cut = is_cut ? kcut++ : -1;
+    if (cls == 2) continue;
+    int64_t ci[3] = {cl % g.N[0], d > 1 ? (cl / g.N[0]) % g.N[1] : 0, d > 2 ? cl / ((int64_t)g.N[0] * g.N[1]) : 0};
+    // distance of the cell box to x_s
+    double dist2 = 0.0;
+    for (int k = 0; k < d; ++k) {
+      const double lo = host_lattice(g.lo[k], g.hi[k], ci[k], g.N[k]);
+      const double hi = host_lattice(g.lo[k], g.hi[k], ci[k] + 1, g.N[k]);
+      const double q = c->src_x[k] < lo ? lo - c->src_x[k] : (c->src_x[k] > hi ? c->src_x[k] - hi : 0.0);
+      dist2 += q * q;
+    }
+    if (dist2 > rcut * rcut) continue;
+    std::fill(fe.begin(), fe.end(), 0.0);
+    // leaves: the whole cell (level 0) for an uncut cell
+    std::vector<unsigned long long> one(1, 0ull);
+    const std::vector<unsigned long long>& leaves = is_cut ? c->cut_leaves[my_cut] : one;
+    for (unsigned long long lf : leaves) {
+      const int l = (int)(lf >> 48);
+      int a[3];
+      for (int k = 0; k < 3; ++k) a[k] = (int)((lf >> (16 * k)) & 0xFFFF);
+      double xlo[3] = {0, 0, 0}, span[3] = {0, 0, 0};
+      for (int k = 0; k < d; ++k) {
+        const int64_t den = (int64_t)g.N[k] * g.s << l;
+        const int64_t m0 = ((int64_t)ci[k] * g.s << l) + (int64_t)a[k] * g.s;
+        xlo[k] = host_lattice(g.lo[k], g.hi[k], m0, den);
+        span[k] = host_lattice(g.lo[k], g.hi[k], m0 + g.s, den) - xlo[k];
+      }
+      const double sc = std::ldexp(1.0, -l);
+      // basis values at the leaf's Gauss points per axis
+      double v[3][SC_MAXP1][SC_MAXP1];
+      for (int k = 0; k < 3; ++k)
+        for (int q = 0; q < n1; ++q) {
+          if (k < d) {
+            const double xi = -1.0 + (2.0 * a[k] + 1.0 + c->gau_x[q]) * sc;
+            host_lagrange(c->gll_x, xi, v[k][q], nullptr);
+          } else {
+            for (int i = 0; i < n1; ++i) v[k][q][i] = (q == 0 && i == 0) ? 1.0 : 0.0;
+          }
+        }
+      const int nq1 = d > 1 ? n1 : 1, nq2 = d > 2 ? n1 : 1;
+      for (int q2 = 0; q2 < nq2; ++q2)
+        for (int q1 = 0; q1 < nq1; ++q1)
+          for (int q0 = 0; q0 < n1; ++q0) {
+            const int qq[3] = {q0, q1, q2};
+            double x[3] = {0, 0, 0}, w = 1.0, r2 = 0.0;
+            for (int k = 0; k < d; ++k) {
+              x[k] = xlo[k] + span[k] * tq[qq[k]];
+              w *= c->gau_w[qq[k]] * 0.5 * g.h[k] * sc;
+              const double dx = x[k] - c->src_x[k];
+              r2 += dx * dx;
+            }
+            const double al = (!is_cut || host_phys(c->voids, x)) ? 1.0 : c->alpha;
+            const double f = al * w * amp * std::exp(-r2 / (2.0 * sig * sig));
+            if (f == 0.0) continue;
+            for (int loc = 0; loc < nb; ++loc) {
+              const int l0 = loc % n1, l1 = (loc / n1) % n1, l2 = loc / (n1 * n1);
+              fe[loc] += f * v[0][q0][l0] * (d > 1 ? v[1][q1][l1] : 1.0) * (d > 2 ? v[2][q2][l2] : 1.0);
+            }
+          }
+    }
+    for (int loc = 0; loc < nb; ++loc)
+      if (fe[loc] != 0.0) acc[elem_node(g, ci, loc, n1)] += fe[loc];
+  }
+  out.assign(acc.begin(), acc.end());
+}
+
 void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   Builder b;
   b.c = c;
@@ -343,10 +429,15 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   b.nb = c->nb;
   const int nb = c->nb, n1 = b.n1;
   // ---------------- source, DOF lists, irregular nodes
-  std::vector<std::pair<int64_t, double>> src;  // (lattice, f_x value)
-  if (c->src_kind == 1) point_weights(c, c->src_x, true, src);
-  for (auto& sv : src)
-    if (c->ntype[sv.first] == 1) c->ntype[sv.first] = 2;  // point-load d nodes -> irregular path
+  std::vector<std::pair<int64_t, double>> src;  // (lattice, f_x value), ascending lattice
+  if (c->src_kind == 1) {
+    point_weights(c, c->src_x, true, src);
+    for (auto& sv : src)
+      if (c->ntype[sv.first] == 1) c->ntype[sv.first] = 2;  // point-load d nodes -> irregular path
+    std::sort(src.begin(), src.end());
+  } else if (c->src_kind == 2) {
+    bell_weights(c, src);   // tensor-d nodes keep the tensor kernel; their load is added after it
+  }
   // integrator 2 (trapezoidal Newmark on all DOFs): every DOF is treated implicitly
   if (c->integrator == 2)
     for (int64_t L = 0; L < c->n_lat; ++L)
@@ -582,6 +673,33 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
         ifv.push_back(ifx[i]);
       }
     c->n_irr = (int64_t)il.size();
+    // tensor-d nodes this rank updates that carry a distributed load: f_x / M_ii with the
+    // lumped mass rho prod_k (h_k/2) wt_k (the mass the explicit kernel divides by)
+    {
+      std::vector<int32_t> ll;
+      std::vector<double> lf;
+      for (auto& sv : src) {
+        const uint8_t t = c->ntype_rank[sv.first];
+        if (t != 1 && t != 4) continue;
+        int64_t ijk[3];
+        lat_ijk(g, sv.first, ijk);
+        double m = c->rho;
+        for (int k = 0; k < g.dim; ++k) {
+          const int64_t l = ijk[k] % g.p, e = ijk[k] / g.p;
+          const double wt = l ? c->gll_w[l] : ((e > 0 ? c->gll_w[g.p] : 0.0) + (e < g.N[k] ? c->gll_w[0] : 0.0));
+          m *= 0.5 * g.h[k] * wt;
+        }
+        ll.push_back((int32_t)sv.first);
+        lf.push_back(sv.second / m);
+      }
+      c->n_load = (int64_t)ll.size();
+      if (c->n_load) {
+        SC_CUDA(cudaMalloc(&c->d_load_lat, sizeof(int32_t) * c->n_load));
+        SC_CUDA(cudaMalloc(&c->d_load_fxm, sizeof(double) * c->n_load));
+        SC_CUDA(cudaMemcpy(c->d_load_lat, ll.data(), sizeof(int32_t) * c->n_load, cudaMemcpyHostToDevice));
+        SC_CUDA(cudaMemcpy(c->d_load_fxm, lf.data(), sizeof(double) * c->n_load, cudaMemcpyHostToDevice));
+      }
+    }
     if (c->n_irr) {
       SC_CUDA(cudaMalloc(&c->d_irr_lat, sizeof(int32_t) * c->n_irr));
       SC_CUDA(cudaMalloc(&c->d_irr_invm, sizeof(double) * c->n_irr));

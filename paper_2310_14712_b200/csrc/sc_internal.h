@@ -131,6 +131,10 @@ struct sc_ctx {
   int32_t* d_irr_lat = nullptr;
   double* d_irr_invm = nullptr;
   double* d_irr_fx = nullptr;
+  // tensor-d nodes carrying a distributed load (source kind 2): lattice index, f_x / M_ii
+  int32_t* d_load_lat = nullptr;
+  double* d_load_fxm = nullptr;
+  int64_t n_load = 0;
   double* d_Kref = nullptr;
   // c state (ND order)
   int32_t* d_c_lat = nullptr;
@@ -191,6 +195,8 @@ struct sc_ctx {
   double src_x[3] = {0, 0, 0};
   std::vector<double> Kcut_host, Mcut_host;   // freed after the factorisation
   std::vector<long long> cut_cells;           // ascending cell index of each cut cell
+  std::vector<std::vector<unsigned long long>> cut_leaves;   // source kind 2: spacetree leaves per cut cell
+  double src_sigma = 0.0, src_amp = 0.0;      // source kind 2: Gaussian bell width, amplitude
   int max_w = 0;                              // widest supernode
   double* d_tmp = nullptr;
   // ---- multi-rank slab decomposition (partition.cpp; world > 1)
@@ -284,6 +290,7 @@ double elastic_energy(sc_ctx* c);
 void setup_factor(sc_ctx* c, const std::vector<double>& Mcut_host);
 void point_weights(const sc_ctx* c, const double* x, bool with_alpha,
                    std::vector<std::pair<int64_t, double>>& out);
+void bell_weights(const sc_ctx* c, std::vector<std::pair<int64_t, double>>& out);
 // step (step.cu)
 void setup_step_structures(sc_ctx* c);
 void explicit_tiling(const GridP& g, int ext[3], int tg[3]);

@@ -663,6 +663,18 @@ void setup_device_geometry(sc_ctx* c) {
     c->Mcut_host.resize(mat);
     SC_CUDA(cudaMemcpyAsync(c->Kcut_host.data(), c->d_Kcut, sizeof(double) * mat, cudaMemcpyDeviceToHost, c->stream));
     SC_CUDA(cudaMemcpyAsync(c->Mcut_host.data(), d_M, sizeof(double) * mat, cudaMemcpyDeviceToHost, c->stream));
+    // the Gaussian-bell load (source kind 2) integrates over the same leaves on the host
+    if (c->src_kind == 2) {
+      std::vector<unsigned long long> lv((size_t)n_cand * cap);
+      std::vector<int> nl(n_cand);
+      SC_CUDA(cudaMemcpy(lv.data(), d_leaves, sizeof(unsigned long long) * lv.size(), cudaMemcpyDeviceToHost));
+      SC_CUDA(cudaMemcpy(nl.data(), d_nleaves, sizeof(int) * n_cand, cudaMemcpyDeviceToHost));
+      c->cut_leaves.assign(c->n_cut, {});
+      for (int64_t k = 0; k < c->n_cut; ++k) {
+        const int sl = slots[k];
+        c->cut_leaves[k].assign(lv.begin() + (size_t)sl * cap, lv.begin() + (size_t)sl * cap + nl[sl]);
+      }
+    }
     // device copy for the step: tiled-symmetric storage (k_celem), the full matrices freed
     double* d_full = c->d_Kcut;
     c->d_Kcut = pack_sym(c, d_full, c->n_cut);

@@ -161,11 +161,27 @@ __global__ void k_irregular(const double* __restrict__ U, const double* Pv, doub
   if (!isfinite(res)) atomicExch(flag, 1);
 }
 
+// distributed load on tensor-d nodes (source kind 2): the explicit kernel has written
+// a1 u + a2 Pv - a3 (K u)/M; add a3 f_t(t_n) f_x / M (eq:CDMacc)
+__global__ void k_load_d(double* __restrict__ out, const int32_t* __restrict__ lat, const double* __restrict__ fxm,
+                         int n, const double* __restrict__ ft, long long n_t, const long long* step, double a3) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[lat[i]] += a3 * ft_at(ft, n_t, step, 0) * fxm[i];
+}
+
+static void launch_load_d(sc_ctx* c, double* out, double a3, cudaStream_t st) {
+  if (c->n_load == 0) return;
+  k_load_d<<<(unsigned)((c->n_load + 255) / 256), 256, 0, st>>>(out, c->d_load_lat, c->d_load_fxm, (int)c->n_load,
+                                                                c->d_ft, c->n_t, c->d_step, a3);
+  SC_CUDA(cudaGetLastError());
+}
+
 // ------------------------------------------------------------------ c elements
 // Element matrices K_e are symmetric: stored as the upper triangle of an nt x nt
 // grid of T x T tiles (nt T >= nb, zero padded), tiles (I, J), I <= J, in row order, each
-// row-major with stride TS doubles (TS even: 16-byte aligned); (nt+1)/(2 nt) of the full bytes
-// (60% for 3D p = 4: nt = 5, T = 25).  Built once at setup (k_pack_sym).
+// column-major with stride TS doubles; (nt+1)/(2 nt) of the full bytes (60% for 3D p = 4:
+// nt = 5, T = 25).  Built once at setup (k_pack_sym).
 __global__ void k_pack_sym(const double* __restrict__ full, double* __restrict__ packed, long long n_mat, int nb,
                            int T, int nt, int TS, long long ms) {
   const long long per = (long long)(nt * (nt + 1) / 2) * TS;
@@ -181,7 +197,7 @@ __global__ void k_pack_sym(const double* __restrict__ full, double* __restrict__
       ++I;
     }
     const int J = I + tile;
-    const int a = o / T, b = o - (o / T) * T;
+    const int b = o / T, a = o - (o / T) * T;   // column-major: o = b T + a
     const int i = I * T + a, j = J * T + b;
     double v = 0.0;
     if (o < T * T && i < nb && j < nb) v = full[(size_t)m * nb * nb + (size_t)i * nb + j];
@@ -189,42 +205,31 @@ __global__ void k_pack_sym(const double* __restrict__ full, double* __restrict__
   }
 }
 
-__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-
-// (a3)+(a4) c-element products Y[e][i] = sum_j K_e[i][j] w_j, one CTA per element.
+// (a3)+(a4) c-element products Y[e][i] = sum_j K_e[i][j] w_j, one CTA of nt T threads per
+// element, thread t = (block I = t / T, row a = t % T) owns output t.
 // mode 0 (step): w = predictor u~^c on c nodes, u^d_{n+1} (buffer B) elsewhere;
 // mode 1 (start): w = A everywhere;
 // mode 2 (leap-frog substep, integrator 4): w = u^c_k (compact, vc) on c nodes, the d values
 // A + theta (B - A) elsewhere (reading LF3: theta = k/m interpolated, 0 frozen).
-// The stored tiles stream through shared memory (cp.async, two buffers); thread t (block I =
-// t / T, row a = t % T) owns output t and adds, per tile (I0, J0): the row sum of row a when
-// I = I0 (K_IJ w_J) and the column sum of column a when I = J0 > I0 (K_JI^T w_J) - every
-// stored entry is read once from HBM and used twice; fixed order, no atomics.
+// Thread (I, a) streams row a of the stored tiles (I, J >= I) (column-major tiles: coalesced
+// across the block's threads) and column a of the tiles (J < I, I) (= row a of their
+// transposes; contiguous per thread): every stored entry is read once from HBM and used by two
+// threads; CELEM_U loads in flight per thread; fixed order, no atomics.
+#ifndef CELEM_U
+#define CELEM_U 5
+#endif
 __global__ void k_celem(int mode, const double* __restrict__ A, const double* __restrict__ B,
                         const double* __restrict__ vc, const double* __restrict__ ac, double dt,
                         const int32_t* __restrict__ ecell, const int32_t* __restrict__ ekidx,
                         const int32_t* __restrict__ ecidx, const double* __restrict__ Kp,
                         const double* __restrict__ Krefp, double* __restrict__ Y, int ne, int nb, int T, int nt,
                         int TS, long long ms, GridP g, double theta) {
-  extern __shared__ double sm[];
-  const int wlen = (nt * T + 1) & ~1;
-  double* w = sm;              // [wlen]
-  double* tb = sm + wlen;      // [2][TS]
+  extern __shared__ double w[];   // [nt T]
   const int e = blockIdx.x;
   if (e >= ne) return;
-  const int t = threadIdx.x, nthr = blockDim.x;
+  const int t = threadIdx.x, nthr = blockDim.x, wlen = nt * T;
   const int kidx = ekidx[e];
   const double* K = kidx >= 0 ? Kp + (size_t)kidx * ms : Krefp;
-  auto stage = [&](int tile, int buf) {
-    const double* src = K + (size_t)tile * TS;
-    double* dst = tb + buf * TS;
-    for (int q = t; q < TS / 2; q += nthr) cpa16(dst + 2 * q, src + 2 * q);
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-  };
-  stage(0, 0);   // the first tile streams in while w is gathered
   {
     const int n1 = g.p + 1;
     const long long cell = ecell[e];
@@ -258,38 +263,46 @@ __global__ void k_celem(int mode, const double* __restrict__ A, const double* __
       w[j] = v;
     }
   }
+  __syncthreads();
+  if (t >= wlen) return;
   const int I = t / T, a = t - (t / T) * T;
-  double acc0 = 0.0, acc1 = 0.0;
-  const int ntiles = nt * (nt + 1) / 2;
-  int tile = 0;
-  for (int I0 = 0; I0 < nt; ++I0)
-    for (int J0 = I0; J0 < nt; ++J0, ++tile) {
-      if (tile + 1 < ntiles) {
-        stage(tile + 1, (tile + 1) & 1);
-        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-      } else {
-        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-      }
-      __syncthreads();   // tile staged (and, first time, w gathered)
-      const double* tt = tb + (tile & 1) * TS;
-      if (I == I0) {   // row a of K_IJ against w_J
-        const double* row = tt + a * T;
-        const double* wj = w + J0 * T;
-        for (int b = 0; b < T; b += 2) {
-          acc0 = fma(row[b], wj[b], acc0);
-          if (b + 1 < T) acc1 = fma(row[b + 1], wj[b + 1], acc1);
-        }
-      }
-      if (I == J0 && I0 != J0) {   // column a of K_(I0,J0) (= row a of its transpose) against w_I0
-        const double* wi = w + I0 * T;
-        for (int b = 0; b < T; b += 2) {
-          acc0 = fma(tt[b * T + a], wi[b], acc0);
-          if (b + 1 < T) acc1 = fma(tt[(b + 1) * T + a], wi[b + 1], acc1);
-        }
-      }
-      __syncthreads();   // buffer free for the tile after next
+  double acc[CELEM_U];
+#pragma unroll
+  for (int k = 0; k < CELEM_U; ++k) acc[k] = 0.0;
+  // tile (I0, J0), I0 <= J0, starts at tile index I0 nt - I0 (I0 - 1) / 2 + (J0 - I0)
+  auto tile_base = [&](int I0, int J0) { return K + (size_t)(I0 * nt - I0 * (I0 - 1) / 2 + (J0 - I0)) * TS; };
+  // rows: tiles (I, J >= I), element (a, b) at b T + a
+  for (int J = I; J < nt; ++J) {
+    const double* tb = tile_base(I, J) + a;
+    const double* wj = w + J * T;
+    int b = 0;
+    for (; b + CELEM_U <= T; b += CELEM_U) {
+      double x[CELEM_U];
+#pragma unroll
+      for (int k = 0; k < CELEM_U; ++k) x[k] = __ldg(tb + (size_t)(b + k) * T);
+#pragma unroll
+      for (int k = 0; k < CELEM_U; ++k) acc[k] = fma(x[k], wj[b + k], acc[k]);
     }
-  if (t < nb) Y[(size_t)e * nb + t] = acc0 + acc1;
+    for (; b < T; ++b) acc[0] = fma(__ldg(tb + (size_t)b * T), wj[b], acc[0]);
+  }
+  // columns: tiles (J < I, I), element (b, a) at a T + b (contiguous per thread)
+  for (int J = 0; J < I; ++J) {
+    const double* tb = tile_base(J, I) + (size_t)a * T;
+    const double* wj = w + J * T;
+    int b = 0;
+    for (; b + CELEM_U <= T; b += CELEM_U) {
+      double x[CELEM_U];
+#pragma unroll
+      for (int k = 0; k < CELEM_U; ++k) x[k] = __ldg(tb + b + k);
+#pragma unroll
+      for (int k = 0; k < CELEM_U; ++k) acc[k] = fma(x[k], wj[b + k], acc[k]);
+    }
+    for (; b < T; ++b) acc[0] = fma(__ldg(tb + b), wj[b], acc[0]);
+  }
+  double sum = 0.0;
+#pragma unroll
+  for (int k = 0; k < CELEM_U; ++k) sum += acc[k];
+  if (t < nb) Y[(size_t)e * nb + t] = sum;
 }
 
 __global__ void k_crhs(double* __restrict__ b, const double* __restrict__ fxc, const int32_t* __restrict__ ptr,
@@ -570,7 +583,7 @@ static void launch_celem(sc_ctx* c, int mode, const double* A, const double* B, 
                          double theta = 0.0, const double* vc = nullptr) {
   if (c->n_celem == 0) return;
   const int nthr = ((c->ct_nt * c->ct_T + 31) / 32) * 32;
-  const size_t smem = sizeof(double) * (((c->ct_nt * c->ct_T + 1) & ~1) + 2 * (size_t)c->ct_TS);
+  const size_t smem = sizeof(double) * (size_t)c->ct_nt * c->ct_T;
   k_celem<<<(unsigned)c->n_celem, nthr, smem, st>>>(mode, A, B, vc ? vc : c->d_vc, c->d_ac, c->dt, c->d_celem_cell,
                                                      c->d_celem_kidx, c->d_celem_cidx, c->d_Kcut, c->d_Krefp, c->d_Y,
                                                      (int)c->n_celem, c->nb, c->ct_T, c->ct_nt, c->ct_TS, c->ct_ms,
@@ -583,7 +596,7 @@ void plan_sym_tiles(sc_ctx* c) {
   const int nb = c->nb;
   c->ct_nt = std::max(1, (nb + 12) / 25);   // tiles of ~25 rows: 3D p=4 -> 5 x 25, p=3 -> 3 x 22
   c->ct_T = (nb + c->ct_nt - 1) / c->ct_nt;
-  c->ct_TS = (c->ct_T * c->ct_T + 1) & ~1;
+  c->ct_TS = c->ct_T * c->ct_T;
   c->ct_ms = (long long)(c->ct_nt * (c->ct_nt + 1) / 2) * c->ct_TS;
 }
 
@@ -681,6 +694,7 @@ void enqueue_step(sc_ctx* c, int parity, cudaStream_t st) {
     // world > 1 the pack of the exchange (the next step's explicit update needs it)
     launch_explicit(c, A, B, B, 2.0, -1.0, dt * dt, 5, st);
     launch_irregular(c, A, B, B, 2.0, -1.0, dt * dt, st);
+    launch_load_d(c, B, dt * dt, st);
     enqueue_c_part(c, A, B, st);
     if (c->world > 1) enqueue_pack(c, B, st);
     return;
@@ -715,7 +729,8 @@ void build_graphs(sc_ctx* c) {
   // SC_PIPELINE=1: fork the far-d update of step n+1 against the c part of step n (one rank
   // with c DOFs); default off: measured no gain and it costs a second
   // (near-node) explicit launch
-  c->pipelined = c->n_c > 0 && c->n_d > c->n_irr && c->world == 1 && c->integrator == 0 && sc_knob("SC_PIPELINE") &&
+  c->pipelined = c->n_c > 0 && c->n_d > c->n_irr && c->world == 1 && c->integrator == 0 && c->n_load == 0 &&
+                 sc_knob("SC_PIPELINE") &&
                  atoi(sc_knob("SC_PIPELINE"));
   if (!c->s_hi) {
     int lo = 0, hi = 0;
@@ -735,7 +750,8 @@ void build_graphs(sc_ctx* c) {
     cudaGraphDestroy(gr);
   }
   // kernels per step: explicit (+ near when pipelined) + irregular + advance + c part (+ pack)
-  c->kernels_per_step = 1 + (c->pipelined && c->n_near > 0 ? 1 : 0) + (c->n_irr > 0) + 1 + (c->world > 1);
+  c->kernels_per_step = 1 + (c->pipelined && c->n_near > 0 ? 1 : 0) + (c->n_irr > 0) + (c->n_load > 0) + 1 +
+                        (c->world > 1);
   if (c->n_c > 0)
     c->kernels_per_step += c->integrator == 1   ? 3
                            : c->integrator == 4 ? 4 * c->lf_m + 1
@@ -901,6 +917,7 @@ void run_startup(sc_ctx* c, const double* u0, const double* v0) {
   const double a2 = vlat ? -dt : 0.0;
   launch_explicit(c, A, Pv, B, 1.0, a2, 0.5 * dt * dt, 5, c->stream);
   launch_irregular(c, A, Pv, B, 1.0, a2, 0.5 * dt * dt, c->stream);
+  launch_load_d(c, B, 0.5 * dt * dt, c->stream);
   if (c->n_cl > 0 && c->integrator == 1) {
     launch_celem(c, 1, A, A, c->stream);
     k_crhs<<<(unsigned)((c->n_cl + 255) / 256), 256, 0, c->stream>>>(c->d_b, c->d_fxc, c->d_rhs_ptr, c->d_rhs_idx,
