@@ -149,7 +149,8 @@ struct sc_ctx {
   double* d_Krefp = nullptr;         // the uncut reference K_e, same storage
   double* d_cut_dt = nullptr;        // [n_cut][2] cell-wise critical step (consistent, HRZ) of the cut cells
   int ct_T = 0, ct_nt = 0, ct_TS = 0;   // tiles: T rows, nt per dimension, TS doubles (stride)
-  long long ct_ms = 0;                  // doubles per stored matrix
+  long long ct_ms = 0;                  // doubles per stored matrix (even)
+  int celem_grid = 0;                   // persistent c-element CTAs
   double* d_Y = nullptr;             // n_celem x nb
   int32_t *d_rhs_ptr = nullptr, *d_rhs_idx = nullptr;   // c node -> Y entries
   // factor structure (shared by S and M^cc)
