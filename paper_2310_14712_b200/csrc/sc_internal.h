@@ -149,8 +149,7 @@ struct sc_ctx {
   double* d_Krefp = nullptr;         // the uncut reference K_e, same storage
   double* d_cut_dt = nullptr;        // [n_cut][2] cell-wise critical step (consistent, HRZ) of the cut cells
   int ct_T = 0, ct_nt = 0, ct_TS = 0;   // tiles: T rows, nt per dimension, TS doubles (stride)
-  long long ct_ms = 0;                  // doubles per stored matrix (even)
-  int celem_grid = 0;                   // persistent c-element CTAs
+  long long ct_ms = 0;                  // doubles per stored matrix
   double* d_Y = nullptr;             // n_celem x nb
   int32_t *d_rhs_ptr = nullptr, *d_rhs_idx = nullptr;   // c node -> Y entries
   // factor structure (shared by S and M^cc)
@@ -295,6 +294,7 @@ void bell_weights(const sc_ctx* c, std::vector<std::pair<int64_t, double>>& out)
 // step (step.cu)
 void setup_step_structures(sc_ctx* c);
 void explicit_tiling(const GridP& g, int ext[3], int tg[3]);
+void explicit_prepare(sc_ctx* c);
 void build_graphs(sc_ctx* c);
 void destroy_graphs(sc_ctx* c);
 void run_startup(sc_ctx* c, const double* u0, const double* v0);

@@ -16,7 +16,6 @@
 #include <vector>
 
 #include "sc_internal.h"
-#include "tma.cuh"
 
 __constant__ double c_Mh[SC_MAXP1 * SC_MAXP1];
 __constant__ double c_Kh[SC_MAXP1 * SC_MAXP1];
@@ -206,113 +205,120 @@ __global__ void k_pack_sym(const double* __restrict__ full, double* __restrict__
   }
 }
 
-// (a3)+(a4) c-element products Y[e][i] = sum_j K_e[i][j] w_j.  Persistent CTAs (one per SM)
-// of nt T (rounded to 32) threads loop over the elements; each element's stored matrix (one
-// contiguous block of ms doubles) is streamed into shared memory by ONE bulk (TMA) copy on an
-// mbarrier, double buffered (element e+1 in flight while e is computed).  Thread t = (block
-// I = t / T, row a = t % T) owns output t: row a of the tiles (I, J >= I) (column-major tiles:
-// conflict-free across the block) and column a of the tiles (J < I, I) (= row a of their
-// transposes; stride T, 2-way at most) - every stored entry read once from HBM, used twice;
-// fixed order, no atomics.
+// (a3)+(a4) c-element products Y[e][i] = sum_j K_e[i][j] w_j, one CTA of nt warps per element
+// (tiles of T = 32 rows = one warp each; T = nb <= 32: a single tile).  Warp I = output block I,
+// lane a = row a:
+//  * row tiles (I, J >= I), column-major: lane a reads element (a, b) at b T + a - coalesced;
+//  * column tiles (J < I, I) are used transposed (K_JI^T w_J): the warp reads the tile
+//    coalesced (lane l takes row l), transposes it through its own padded shared-memory
+//    buffer (__syncwarp only) and each lane then walks its column: every stored entry is read
+//    once from HBM and used by two warps; fixed order, no atomics.
 // mode 0 (step): w = predictor u~^c on c nodes, u^d_{n+1} (buffer B) elsewhere;
 // mode 1 (start): w = A everywhere;
 // mode 2 (leap-frog substep, integrator 4): w = u^c_k (compact, vc) on c nodes, the d values
 // A + theta (B - A) elsewhere (reading LF3: theta = k/m interpolated, 0 frozen).
+#ifndef CELEM_U
+#define CELEM_U 8
+#endif
 __global__ void __launch_bounds__(128) k_celem(int mode, const double* __restrict__ A, const double* __restrict__ B,
                         const double* __restrict__ vc, const double* __restrict__ ac, double dt,
                         const int32_t* __restrict__ ecell, const int32_t* __restrict__ ekidx,
                         const int32_t* __restrict__ ecidx, const double* __restrict__ Kp,
                         const double* __restrict__ Krefp, double* __restrict__ Y, int ne, int nb, int T, int nt,
                         int TS, long long ms, GridP g, double theta) {
-  extern __shared__ __align__(16) double smc[];
-  __shared__ uint64_t mbar[2];
+  extern __shared__ double smc[];
   const int wlen = nt * T;
-  double* kb[2] = {smc, smc + ms};                     // stored matrices (ms even: 16-byte blocks)
-  double* wb = smc + 2 * ms;                           // [wlen]
+  double* w = smc;                                  // [wlen]
+  const int e = blockIdx.x;
+  if (e >= ne) return;
   const int t = threadIdx.x, nthr = blockDim.x;
-  const unsigned bytes = (unsigned)(ms * sizeof(double));
-  auto src_of = [&](int e) {
-    const int kidx = ekidx[e];
-    return kidx >= 0 ? Kp + (size_t)kidx * ms : Krefp;
-  };
-  if (t == 0) {
-    tma_mbar_init(&mbar[0]);
-    tma_mbar_init(&mbar[1]);
+  const int warp = t >> 5, lane = t & 31;
+  double* tr = smc + wlen + warp * (32 * 33);       // this warp's transpose buffer [32][33]
+  const int kidx = ekidx[e];
+  const double* K = kidx >= 0 ? Kp + (size_t)kidx * ms : Krefp;
+  {
+    const int n1 = g.p + 1;
+    const long long cell = ecell[e];
+    long long ci[3];
+    long long rem = cell;
+    for (int k = 0; k < 3; ++k) {
+      if (k < g.dim) {
+        ci[k] = rem % g.N[k];
+        rem /= g.N[k];
+      } else {
+        ci[k] = 0;
+      }
+    }
+    for (int j = t; j < wlen; j += nthr) {
+      double v = 0.0;
+      if (j < nb) {
+        const int l0 = j % n1, l1 = (j / n1) % n1, l2 = j / (n1 * n1);
+        long long gl = ci[0] * g.p + l0;
+        if (g.dim > 1) gl += g.nl[0] * (ci[1] * g.p + l1);
+        if (g.dim > 2) gl += g.nl[0] * g.nl[1] * (ci[2] * g.p + l2);
+        if (mode == 1) {
+          v = A[gl];
+        } else if (mode == 2) {
+          const int cc = ecidx[(size_t)e * nb + j];
+          v = cc >= 0 ? vc[cc] : fma(theta, B[gl] - A[gl], A[gl]);
+        } else {
+          const int cc = ecidx[(size_t)e * nb + j];
+          v = cc >= 0 ? A[gl] + dt * vc[cc] + 0.25 * dt * dt * ac[cc] : B[gl];
+        }
+      }
+      w[j] = v;
+    }
   }
   __syncthreads();
-  if (t == 0 && blockIdx.x < ne) {
-    tma_mbar_expect(&mbar[0], bytes);
-    tma_bulk_g2s(kb[0], src_of(blockIdx.x), bytes, &mbar[0]);
+  if (warp >= nt) return;
+  const int I = warp, a = lane;
+  const bool act = a < T;
+  double acc[CELEM_U];
+#pragma unroll
+  for (int k = 0; k < CELEM_U; ++k) acc[k] = 0.0;
+  // tile (I0, J0), I0 <= J0, at tile index I0 nt - I0 (I0 - 1) / 2 + (J0 - I0)
+  for (int J = I; J < nt; ++J) {   // row tiles: element (a, b) at b T + a
+    const double* tb = K + (size_t)(I * nt - I * (I - 1) / 2 + (J - I)) * TS + a;
+    const double* wj = w + J * T;
+    int b = 0;
+    for (; b + CELEM_U <= T; b += CELEM_U) {
+      double x[CELEM_U];
+#pragma unroll
+      for (int k = 0; k < CELEM_U; ++k) x[k] = act ? __ldg(tb + (size_t)(b + k) * T) : 0.0;
+#pragma unroll
+      for (int k = 0; k < CELEM_U; ++k) acc[k] = fma(x[k], wj[b + k], acc[k]);
+    }
+    for (; b < T; ++b) acc[0] = fma(act ? __ldg(tb + (size_t)b * T) : 0.0, wj[b], acc[0]);
   }
-  const int n1 = g.p + 1;
-  const int I = t / T, a = t - (t / T) * T;
-  int it = 0;
-  for (int e = blockIdx.x; e < ne; e += gridDim.x, ++it) {
-    const int buf = it & 1;
-    const int en = e + gridDim.x;
-    if (t == 0 && en < ne) {   // the next element's matrix into the other buffer (freed below)
-      tma_mbar_expect(&mbar[buf ^ 1], bytes);
-      tma_bulk_g2s(kb[buf ^ 1], src_of(en), bytes, &mbar[buf ^ 1]);
+  for (int J = 0; J < I; ++J) {    // column tiles (J, I): y_I[a] += sum_r K_JI[r][a] w_J[r]
+    const double* tb = K + (size_t)(J * nt - J * (J - 1) / 2 + (I - J)) * TS;
+    // coalesced read: lane l takes element (l, c) at c T + l, stored at tr[c][l]
+    int cc = 0;
+    for (; cc + CELEM_U <= T; cc += CELEM_U) {
+      double x[CELEM_U];
+#pragma unroll
+      for (int k = 0; k < CELEM_U; ++k) x[k] = act ? __ldg(tb + (size_t)(cc + k) * T + lane) : 0.0;
+#pragma unroll
+      for (int k = 0; k < CELEM_U; ++k) tr[(cc + k) * 33 + lane] = x[k];
     }
-    // gather w of element e (overlaps the copies)
-    {
-      const long long cell = ecell[e];
-      long long ci[3];
-      long long rem = cell;
-      for (int k = 0; k < 3; ++k) {
-        if (k < g.dim) {
-          ci[k] = rem % g.N[k];
-          rem /= g.N[k];
-        } else {
-          ci[k] = 0;
-        }
+    for (; cc < T; ++cc) tr[cc * 33 + lane] = act ? __ldg(tb + (size_t)cc * T + lane) : 0.0;
+    __syncwarp();
+    const double* wj = w + J * T;
+    if (act) {
+      int r = 0;
+      for (; r + CELEM_U <= T; r += CELEM_U) {
+#pragma unroll
+        for (int k = 0; k < CELEM_U; ++k) acc[k] = fma(tr[a * 33 + r + k], wj[r + k], acc[k]);
       }
-      for (int j = t; j < wlen; j += nthr) {
-        double v = 0.0;
-        if (j < nb) {
-          const int l0 = j % n1, l1 = (j / n1) % n1, l2 = j / (n1 * n1);
-          long long gl = ci[0] * g.p + l0;
-          if (g.dim > 1) gl += g.nl[0] * (ci[1] * g.p + l1);
-          if (g.dim > 2) gl += g.nl[0] * g.nl[1] * (ci[2] * g.p + l2);
-          if (mode == 1) {
-            v = A[gl];
-          } else if (mode == 2) {
-            const int cc = ecidx[(size_t)e * nb + j];
-            v = cc >= 0 ? vc[cc] : fma(theta, B[gl] - A[gl], A[gl]);
-          } else {
-            const int cc = ecidx[(size_t)e * nb + j];
-            v = cc >= 0 ? A[gl] + dt * vc[cc] + 0.25 * dt * dt * ac[cc] : B[gl];
-          }
-        }
-        wb[j] = v;
-      }
+      for (; r < T; ++r) acc[0] = fma(tr[a * 33 + r], wj[r], acc[0]);
     }
-    __syncthreads();                          // w complete
-    tma_mbar_wait(&mbar[buf], (it >> 1) & 1);  // K_e of element e in shared memory
-    if (t < wlen) {
-      const double* K = kb[buf];
-      double acc0 = 0.0, acc1 = 0.0;
-      // tile (I0, J0), I0 <= J0, at tile index I0 nt - I0 (I0 - 1) / 2 + (J0 - I0)
-      for (int J = I; J < nt; ++J) {           // rows: element (a, b) of tile (I, J) at b T + a
-        const double* tb = K + (size_t)(I * nt - I * (I - 1) / 2 + (J - I)) * TS + a;
-        const double* wj = wb + J * T;
-        for (int b = 0; b < T; b += 2) {
-          acc0 = fma(tb[b * T], wj[b], acc0);
-          if (b + 1 < T) acc1 = fma(tb[(b + 1) * T], wj[b + 1], acc1);
-        }
-      }
-      for (int J = 0; J < I; ++J) {            // columns: element (b, a) of tile (J, I) at a T + b
-        const double* tb = K + (size_t)(J * nt - J * (J - 1) / 2 + (I - J)) * TS + (size_t)a * T;
-        const double* wj = wb + J * T;
-        for (int b = 0; b < T; b += 2) {
-          acc0 = fma(tb[b], wj[b], acc0);
-          if (b + 1 < T) acc1 = fma(tb[b + 1], wj[b + 1], acc1);
-        }
-      }
-      if (t < nb) Y[(size_t)e * nb + t] = acc0 + acc1;
-    }
-    __syncthreads();   // buffer buf and w free for the next iterations
+    __syncwarp();   // the buffer is refilled by the next column tile
   }
+  double sum = 0.0;
+#pragma unroll
+  for (int k = 0; k < CELEM_U; ++k) sum += acc[k];
+  const int o = I * T + a;
+  if (act && o < nb) Y[(size_t)e * nb + o] = sum;
 }
 
 __global__ void k_crhs(double* __restrict__ b, const double* __restrict__ fxc, const int32_t* __restrict__ ptr,
@@ -518,18 +524,40 @@ void launch_explicit_p(sc_ctx* c, const double* U, const double* Pv, double* out
   } else {
     if constexpr (P <= 6) {
       using T = Tile3<P>;
-      auto kern = k_explicit_3d<P, T::E, T::EY, T::NT, T::MINB, T::SPV>;
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::smem);
-        attr = true;
-      }
-      kern<<<grid, T::NT, T::smem, st>>>(U, Pv, out, c->d_ntype, e, c->d_flag);
+      // the shared-memory opt-in was set on this context's device at setup (explicit_prepare)
+      k_explicit_3d<P, T::E, T::EY, T::NT, T::MINB, T::SPV><<<grid, T::NT, T::smem, st>>>(U, Pv, out, c->d_ntype, e,
+                                                                                       c->d_flag);
     }
   }
 }
 
+// per-context (per-device) kernel attributes, set at setup before any graph capture: the 3D
+// explicit kernel's dynamic shared memory opt-in (~97 KB at p = 4)
+template <int P>
+void explicit_prepare_p(sc_ctx* c) {
+  if constexpr (P <= 6) {
+    using T = Tile3<P>;
+    SC_CUDA(cudaFuncSetAttribute(k_explicit_3d<P, T::E, T::EY, T::NT, T::MINB, T::SPV>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::smem));
+  }
+  (void)c;
+}
+
 }  // namespace
+
+void explicit_prepare(sc_ctx* c) {
+  if (c->g.dim != 3) return;
+  SC_CUDA(cudaSetDevice(c->device));
+  switch (c->g.p) {
+    case 1: explicit_prepare_p<1>(c); break;
+    case 2: explicit_prepare_p<2>(c); break;
+    case 3: explicit_prepare_p<3>(c); break;
+    case 4: explicit_prepare_p<4>(c); break;
+    case 5: explicit_prepare_p<5>(c); break;
+    case 6: explicit_prepare_p<6>(c); break;
+    default: break;
+  }
+}
 
 void explicit_tiling(const GridP& g, int ext[3], int tg[3]) {
   switch (g.p) {
@@ -592,9 +620,9 @@ void launch_explicit(sc_ctx* c, const double* U, const double* Pv, double* out, 
 static void launch_celem(sc_ctx* c, int mode, const double* A, const double* B, cudaStream_t st,
                          double theta = 0.0, const double* vc = nullptr) {
   if (c->n_celem == 0) return;
-  const int nthr = ((c->ct_nt * c->ct_T + 31) / 32) * 32;
-  const size_t smem = sizeof(double) * (2 * (size_t)c->ct_ms + (size_t)c->ct_nt * c->ct_T);
-  k_celem<<<(unsigned)std::min<int64_t>(c->n_celem, c->celem_grid), nthr, smem, st>>>(mode, A, B, vc ? vc : c->d_vc, c->d_ac, c->dt, c->d_celem_cell,
+  const int nthr = 32 * c->ct_nt;
+  const size_t smem = sizeof(double) * ((size_t)c->ct_nt * c->ct_T + (size_t)c->ct_nt * 32 * 33);
+  k_celem<<<(unsigned)c->n_celem, nthr, smem, st>>>(mode, A, B, vc ? vc : c->d_vc, c->d_ac, c->dt, c->d_celem_cell,
                                                      c->d_celem_kidx, c->d_celem_cidx, c->d_Kcut, c->d_Krefp, c->d_Y,
                                                      (int)c->n_celem, c->nb, c->ct_T, c->ct_nt, c->ct_TS, c->ct_ms,
                                                      c->g, theta);
@@ -604,20 +632,13 @@ static void launch_celem(sc_ctx* c, int mode, const double* A, const double* B, 
 // tiled-symmetric storage of the element matrices (k_celem): nt tiles per dimension of T rows
 void plan_sym_tiles(sc_ctx* c) {
   const int nb = c->nb;
-  c->ct_nt = std::max(1, (nb + 12) / 25);   // tiles of ~25 rows: 3D p=4 -> 5 x 25, p=3 -> 3 x 22
-  c->ct_T = (nb + c->ct_nt - 1) / c->ct_nt;
+  c->ct_T = nb <= 32 ? nb : 32;                 // tiles of one warp's rows
+  c->ct_nt = (nb + c->ct_T - 1) / c->ct_T;       // 3D p = 4: 4 x 32 (125 padded to 128)
   c->ct_TS = c->ct_T * c->ct_T;
   c->ct_ms = (long long)(c->ct_nt * (c->ct_nt + 1) / 2) * c->ct_TS;
-  c->ct_ms += c->ct_ms & 1;   // 16-byte blocks (bulk copies)
-  // persistent c-element CTAs: as many as fit (two matrices in shared memory each)
-  const size_t smem = sizeof(double) * (2 * (size_t)c->ct_ms + (size_t)c->ct_nt * c->ct_T);
-  const int nthr = ((c->ct_nt * c->ct_T + 31) / 32) * 32;
+  if (c->ct_nt > 4) throw ScError(SC_ERR_CONFIG, "(p+1)^dim > 128 not supported by the c-element kernel");
+  const size_t smem = sizeof(double) * ((size_t)c->ct_nt * c->ct_T + (size_t)c->ct_nt * 32 * 33);
   SC_CUDA(cudaFuncSetAttribute(k_celem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0, sms = 0;
-  SC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
-  SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_celem, nthr, smem));
-  if (per_sm < 1) throw ScError(SC_ERR_CONFIG, "c-element kernel does not fit an SM");
-  c->celem_grid = per_sm * sms;
 }
 
 // full row-major matrices (device) -> tiled-symmetric storage (device, allocated here)
@@ -782,6 +803,7 @@ void build_graphs(sc_ctx* c) {
 // owns nodes [ext*P*t, ext*P*(t+1)) per axis, the last tile also the final boundary node)
 void setup_step_structures(sc_ctx* c) {
   GridP& g = c->g;
+  explicit_prepare(c);
   c->n_near_tiles = c->n_far_tiles = 0;
   if (g.dim == 1) return;
   int ext[3], tg[3];
