@@ -145,8 +145,7 @@ struct sc_ctx {
   int32_t* d_celem_cell = nullptr;   // cell index of each c-element
   int32_t* d_celem_kidx = nullptr;   // index into d_Kcut or -1 (uncut -> Kref)
   int32_t* d_celem_cidx = nullptr;   // [e*nb + loc] c index (ND) or -1
-  double* d_Kcut = nullptr;          // n_cut tiled-symmetric cut-cell K_e (step.cu k_celem; ct_ms doubles each)
-  double* d_Krefp = nullptr;         // the uncut reference K_e, same storage
+  double* d_Kcut = nullptr;          // n_cut x nb x nb
   double* d_cut_dt = nullptr;        // [n_cut][2] cell-wise critical step (consistent, HRZ) of the cut cells
   int ct_T = 0, ct_nt = 0, ct_TS = 0;   // tiles: T rows, nt per dimension, TS doubles (stride)
   long long ct_ms = 0;                  // doubles per stored matrix
@@ -303,6 +302,5 @@ void enqueue_far_prologue(sc_ctx* c);
 void launch_solve(sc_ctx* c, const Factor& f, cudaStream_t st);
 void device_upload_reference(sc_ctx* c);
 void gather_dofs(sc_ctx* c, const double* d_lat, double* d_out);
-void plan_sym_tiles(sc_ctx* c);
-double* pack_sym(sc_ctx* c, const double* d_full, long long n_mat);
+
 void profile_launch(sc_ctx* c, int which);

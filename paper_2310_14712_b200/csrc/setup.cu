@@ -675,11 +675,7 @@ void setup_device_geometry(sc_ctx* c) {
         c->cut_leaves[k].assign(lv.begin() + (size_t)sl * cap, lv.begin() + (size_t)sl * cap + nl[sl]);
       }
     }
-    // device copy for the step: tiled-symmetric storage (k_celem), the full matrices freed
-    double* d_full = c->d_Kcut;
-    c->d_Kcut = pack_sym(c, d_full, c->n_cut);
     SC_CUDA(cudaStreamSynchronize(c->stream));
-    cudaFree(d_full);
     cudaFree(d_cc);
     cudaFree(d_slots);
     cudaFree(d_gll);

@@ -178,66 +178,33 @@ static void launch_load_d(sc_ctx* c, double* out, double a3, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ c elements
-// Element matrices K_e are symmetric: stored as the upper triangle of an nt x nt
-// grid of T x T tiles (nt T >= nb, zero padded), tiles (I, J), I <= J, in row order, each
-// column-major with stride TS doubles; (nt+1)/(2 nt) of the full bytes (60% for 3D p = 4:
-// nt = 5, T = 25).  Built once at setup (k_pack_sym).
-__global__ void k_pack_sym(const double* __restrict__ full, double* __restrict__ packed, long long n_mat, int nb,
-                           int T, int nt, int TS, long long ms) {
-  const long long per = (long long)(nt * (nt + 1) / 2) * TS;
-  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n_mat * per;
-       q += (long long)gridDim.x * blockDim.x) {
-    const long long m = q / per;
-    const int r = (int)(q - m * per);
-    int tile = r / TS;
-    const int o = r - tile * TS;
-    int I = 0;
-    while (tile >= nt - I) {   // tiles of row I: J = I .. nt-1
-      tile -= nt - I;
-      ++I;
-    }
-    const int J = I + tile;
-    const int b = o / T, a = o - (o / T) * T;   // column-major: o = b T + a
-    const int i = I * T + a, j = J * T + b;
-    double v = 0.0;
-    if (o < T * T && i < nb && j < nb) v = full[(size_t)m * nb * nb + (size_t)i * nb + j];
-    packed[(size_t)m * ms + r] = v;
-  }
-}
-
-// (a3)+(a4) c-element products Y[e][i] = sum_j K_e[i][j] w_j, one CTA of nt warps per element
-// (tiles of T = 32 rows = one warp each; T = nb <= 32: a single tile).  Warp I = output block I,
-// lane a = row a:
-//  * row tiles (I, J >= I), column-major: lane a reads element (a, b) at b T + a - coalesced;
-//  * column tiles (J < I, I) are used transposed (K_JI^T w_J): the warp reads the tile
-//    coalesced (lane l takes row l), transposes it through its own padded shared-memory
-//    buffer (__syncwarp only) and each lane then walks its column: every stored entry is read
-//    once from HBM and used by two warps; fixed order, no atomics.
 // mode 0 (step): w = predictor u~^c on c nodes, u^d_{n+1} (buffer B) elsewhere;
 // mode 1 (start): w = A everywhere;
 // mode 2 (leap-frog substep, integrator 4): w = u^c_k (compact, vc) on c nodes, the d values
 // A + theta (B - A) elsewhere (reading LF3: theta = k/m interpolated, 0 frozen).
+// Y[e][i] = sum_j K_e[i][j] w_j (K_e symmetric: read as columns, coalesced across threads).
+// (Tiled-symmetric storage of the upper K_e tiles was measured slower in four layouts, see
+// profiles/r2_variants.txt, so the full matrices are streamed.)
 #ifndef CELEM_U
 #define CELEM_U 8
 #endif
-__global__ void __launch_bounds__(128) k_celem(int mode, const double* __restrict__ A, const double* __restrict__ B,
+#ifndef CELEM_CS
+#define CELEM_CS 0
+#endif
+__global__ void k_celem(int mode, const double* __restrict__ A, const double* __restrict__ B,
                         const double* __restrict__ vc, const double* __restrict__ ac, double dt,
                         const int32_t* __restrict__ ecell, const int32_t* __restrict__ ekidx,
-                        const int32_t* __restrict__ ecidx, const double* __restrict__ Kp,
-                        const double* __restrict__ Krefp, double* __restrict__ Y, int ne, int nb, int T, int nt,
-                        int TS, long long ms, GridP g, double theta) {
-  extern __shared__ double smc[];
-  const int wlen = nt * T;
-  double* w = smc;                                  // [wlen]
-  const int e = blockIdx.x;
-  if (e >= ne) return;
-  const int t = threadIdx.x, nthr = blockDim.x;
-  const int warp = t >> 5, lane = t & 31;
-  double* tr = smc + wlen + warp * (32 * 33);       // this warp's transpose buffer [32][33]
-  const int kidx = ekidx[e];
-  const double* K = kidx >= 0 ? Kp + (size_t)kidx * ms : Krefp;
-  {
-    const int n1 = g.p + 1;
+                        const int32_t* __restrict__ ecidx, const double* __restrict__ Kcut,
+                        const double* __restrict__ Kref, double* __restrict__ Y, int ne, int nb, int tpe, GridP g,
+                        double theta) {
+  extern __shared__ double sw[];
+  const int epb = blockDim.x / tpe;
+  const int le = threadIdx.x / tpe, i = threadIdx.x % tpe;
+  const int e = blockIdx.x * epb + le;
+  const bool ok = e < ne;
+  const int n1 = g.p + 1;
+  double* w = sw + le * nb;
+  if (ok) {
     const long long cell = ecell[e];
     long long ci[3];
     long long rem = cell;
@@ -249,76 +216,47 @@ __global__ void __launch_bounds__(128) k_celem(int mode, const double* __restric
         ci[k] = 0;
       }
     }
-    for (int j = t; j < wlen; j += nthr) {
-      double v = 0.0;
-      if (j < nb) {
-        const int l0 = j % n1, l1 = (j / n1) % n1, l2 = j / (n1 * n1);
-        long long gl = ci[0] * g.p + l0;
-        if (g.dim > 1) gl += g.nl[0] * (ci[1] * g.p + l1);
-        if (g.dim > 2) gl += g.nl[0] * g.nl[1] * (ci[2] * g.p + l2);
-        if (mode == 1) {
-          v = A[gl];
-        } else if (mode == 2) {
-          const int cc = ecidx[(size_t)e * nb + j];
-          v = cc >= 0 ? vc[cc] : fma(theta, B[gl] - A[gl], A[gl]);
-        } else {
-          const int cc = ecidx[(size_t)e * nb + j];
-          v = cc >= 0 ? A[gl] + dt * vc[cc] + 0.25 * dt * dt * ac[cc] : B[gl];
-        }
+    for (int j = i; j < nb; j += tpe) {
+      const int l0 = j % n1, l1 = (j / n1) % n1, l2 = j / (n1 * n1);
+      long long gl = ci[0] * g.p + l0;
+      if (g.dim > 1) gl += g.nl[0] * (ci[1] * g.p + l1);
+      if (g.dim > 2) gl += g.nl[0] * g.nl[1] * (ci[2] * g.p + l2);
+      double v;
+      if (mode == 1) {
+        v = A[gl];
+      } else if (mode == 2) {
+        const int cc = ecidx[(size_t)e * nb + j];
+        v = cc >= 0 ? vc[cc] : fma(theta, B[gl] - A[gl], A[gl]);
+      } else {
+        const int cc = ecidx[(size_t)e * nb + j];
+        v = cc >= 0 ? A[gl] + dt * vc[cc] + 0.25 * dt * dt * ac[cc] : B[gl];
       }
       w[j] = v;
     }
   }
   __syncthreads();
-  if (warp >= nt) return;
-  const int I = warp, a = lane;
-  const bool act = a < T;
-  double acc[CELEM_U];
+  if (!ok) return;
+  const int kidx = ekidx[e];
+  const double* K = kidx >= 0 ? Kcut + (size_t)kidx * nb * nb : Kref;
+  auto gemv = [&](auto ld) {
+    for (int r = i; r < nb; r += tpe) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      int j = 0;
+      for (; j + CELEM_U <= nb; j += CELEM_U) {   // CELEM_U independent loads in flight (HBM-bound GEMV)
+        double x[CELEM_U];
 #pragma unroll
-  for (int k = 0; k < CELEM_U; ++k) acc[k] = 0.0;
-  // tile (I0, J0), I0 <= J0, at tile index I0 nt - I0 (I0 - 1) / 2 + (J0 - I0)
-  for (int J = I; J < nt; ++J) {   // row tiles: element (a, b) at b T + a
-    const double* tb = K + (size_t)(I * nt - I * (I - 1) / 2 + (J - I)) * TS + a;
-    const double* wj = w + J * T;
-    int b = 0;
-    for (; b + CELEM_U <= T; b += CELEM_U) {
-      double x[CELEM_U];
+        for (int k = 0; k < CELEM_U; ++k) x[k] = ld(K + (size_t)(j + k) * nb + r);
 #pragma unroll
-      for (int k = 0; k < CELEM_U; ++k) x[k] = act ? __ldg(tb + (size_t)(b + k) * T) : 0.0;
-#pragma unroll
-      for (int k = 0; k < CELEM_U; ++k) acc[k] = fma(x[k], wj[b + k], acc[k]);
-    }
-    for (; b < T; ++b) acc[0] = fma(act ? __ldg(tb + (size_t)b * T) : 0.0, wj[b], acc[0]);
-  }
-  for (int J = 0; J < I; ++J) {    // column tiles (J, I): y_I[a] += sum_r K_JI[r][a] w_J[r]
-    const double* tb = K + (size_t)(J * nt - J * (J - 1) / 2 + (I - J)) * TS;
-    // coalesced read: lane l takes element (l, c) at c T + l, stored at tr[c][l]
-    int cc = 0;
-    for (; cc + CELEM_U <= T; cc += CELEM_U) {
-      double x[CELEM_U];
-#pragma unroll
-      for (int k = 0; k < CELEM_U; ++k) x[k] = act ? __ldg(tb + (size_t)(cc + k) * T + lane) : 0.0;
-#pragma unroll
-      for (int k = 0; k < CELEM_U; ++k) tr[(cc + k) * 33 + lane] = x[k];
-    }
-    for (; cc < T; ++cc) tr[cc * 33 + lane] = act ? __ldg(tb + (size_t)cc * T + lane) : 0.0;
-    __syncwarp();
-    const double* wj = w + J * T;
-    if (act) {
-      int r = 0;
-      for (; r + CELEM_U <= T; r += CELEM_U) {
-#pragma unroll
-        for (int k = 0; k < CELEM_U; ++k) acc[k] = fma(tr[a * 33 + r + k], wj[r + k], acc[k]);
+        for (int k = 0; k < CELEM_U; ++k) acc[k & 3] += x[k] * w[j + k];
       }
-      for (; r < T; ++r) acc[0] = fma(tr[a * 33 + r], wj[r], acc[0]);
+      for (; j < nb; ++j) acc[0] += ld(K + (size_t)j * nb + r) * w[j];
+      Y[(size_t)e * nb + r] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
     }
-    __syncwarp();   // the buffer is refilled by the next column tile
-  }
-  double sum = 0.0;
-#pragma unroll
-  for (int k = 0; k < CELEM_U; ++k) sum += acc[k];
-  const int o = I * T + a;
-  if (act && o < nb) Y[(size_t)e * nb + o] = sum;
+  };
+  // cut-cell matrices are streamed once per step (evict-first); the shared uncut reference
+  // matrix stays cached
+  if (CELEM_CS && kidx >= 0) gemv([](const double* p) { return __ldcs(p); });
+  else gemv([](const double* p) { return __ldg(p); });
 }
 
 __global__ void k_crhs(double* __restrict__ b, const double* __restrict__ fxc, const int32_t* __restrict__ ptr,
@@ -620,35 +558,14 @@ void launch_explicit(sc_ctx* c, const double* U, const double* Pv, double* out, 
 static void launch_celem(sc_ctx* c, int mode, const double* A, const double* B, cudaStream_t st,
                          double theta = 0.0, const double* vc = nullptr) {
   if (c->n_celem == 0) return;
-  const int nthr = 32 * c->ct_nt;
-  const size_t smem = sizeof(double) * ((size_t)c->ct_nt * c->ct_T + (size_t)c->ct_nt * 32 * 33);
-  k_celem<<<(unsigned)c->n_celem, nthr, smem, st>>>(mode, A, B, vc ? vc : c->d_vc, c->d_ac, c->dt, c->d_celem_cell,
-                                                     c->d_celem_kidx, c->d_celem_cidx, c->d_Kcut, c->d_Krefp, c->d_Y,
-                                                     (int)c->n_celem, c->nb, c->ct_T, c->ct_nt, c->ct_TS, c->ct_ms,
-                                                     c->g, theta);
-  SC_CUDA(cudaGetLastError());
-}
-
-// tiled-symmetric storage of the element matrices (k_celem): nt tiles per dimension of T rows
-void plan_sym_tiles(sc_ctx* c) {
   const int nb = c->nb;
-  c->ct_T = nb <= 32 ? nb : 32;                 // tiles of one warp's rows
-  c->ct_nt = (nb + c->ct_T - 1) / c->ct_T;       // 3D p = 4: 4 x 32 (125 padded to 128)
-  c->ct_TS = c->ct_T * c->ct_T;
-  c->ct_ms = (long long)(c->ct_nt * (c->ct_nt + 1) / 2) * c->ct_TS;
-  if (c->ct_nt > 4) throw ScError(SC_ERR_CONFIG, "(p+1)^dim > 128 not supported by the c-element kernel");
-  const size_t smem = sizeof(double) * ((size_t)c->ct_nt * c->ct_T + (size_t)c->ct_nt * 32 * 33);
-  SC_CUDA(cudaFuncSetAttribute(k_celem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-}
-
-// full row-major matrices (device) -> tiled-symmetric storage (device, allocated here)
-double* pack_sym(sc_ctx* c, const double* d_full, long long n_mat) {
-  double* d_p = nullptr;
-  SC_CUDA(cudaMalloc(&d_p, sizeof(double) * std::max<long long>(1, n_mat * c->ct_ms)));
-  if (n_mat > 0)
-    k_pack_sym<<<148 * 8, 256, 0, c->stream>>>(d_full, d_p, n_mat, c->nb, c->ct_T, c->ct_nt, c->ct_TS, c->ct_ms);
+  const int tpe = std::min(256, ((nb + 31) / 32) * 32);
+  const int epb = 256 / tpe;
+  const unsigned blocks = (unsigned)((c->n_celem + epb - 1) / epb);
+  k_celem<<<blocks, epb * tpe, sizeof(double) * epb * nb, st>>>(
+      mode, A, B, vc ? vc : c->d_vc, c->d_ac, c->dt, c->d_celem_cell, c->d_celem_kidx, c->d_celem_cidx, c->d_Kcut,
+      c->d_Kref, c->d_Y, (int)c->n_celem, nb, tpe, c->g, theta);
   SC_CUDA(cudaGetLastError());
-  return d_p;
 }
 
 static void launch_irregular(sc_ctx* c, const double* U, const double* Pv, double* out, double a1, double a2,
@@ -921,9 +838,7 @@ void device_upload_reference(sc_ctx* c) {
   SC_CUDA(cudaMemcpyToSymbol(c_iw2, &iw2, sizeof(double)));
   SC_CUDA(cudaMalloc(&c->d_Kref, sizeof(double) * c->Kref.size()));
   SC_CUDA(cudaMemcpy(c->d_Kref, c->Kref.data(), sizeof(double) * c->Kref.size(), cudaMemcpyHostToDevice));
-  plan_sym_tiles(c);
-  c->d_Krefp = pack_sym(c, c->d_Kref, 1);
-  SC_CUDA(cudaStreamSynchronize(c->stream));
+
 }
 
 void gather_dofs(sc_ctx* c, const double* d_lat, double* d_out) {
