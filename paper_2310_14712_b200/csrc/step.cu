@@ -17,33 +17,7 @@
 
 #include "sc_internal.h"
 
-__constant__ double c_Mh[SC_MAXP1 * SC_MAXP1];
-__constant__ double c_Kh[SC_MAXP1 * SC_MAXP1];
-__constant__ double c_w[SC_MAXP1];
-__constant__ double c_iw[SC_MAXP1];   // 1 / w_l
-__constant__ double c_iw2;            // 1 / (2 w_0): interior element-boundary node
-
-enum { WANT_FAR = 1 << 1, WANT_NEAR = 1 << 4 };
-
-struct ExpP {
-  int nl[3];
-  int N[3];
-  double s[3];      // (2/h_k)^2
-  double a1, a2, coefR;  // out = a1 u + a2 P - coefR * r' / prod(wt)
-  int want;         // bit mask of the node types updated by this launch: bit 1 tensor-d far
-                    // from c nodes, bit 4 tensor-d near c nodes (WANT_FAR / WANT_NEAR)
-  int tg[2];        // tile-grid extents in x, y
-  int ntiles;       // tiles of this launch (blocks loop over them with a grid stride)
-  const int* tiles; // nullable: tile ids (x fastest) of a tile-list launch
-  const uint8_t* clean;  // nullable: per tile id, 1 = every node it owns is wanted tensor-d
-  int ezl;          // 3D: element layers per tile along z
-};
-
-// tile coordinates of the tt-th tile of the launch: from the tile list if any, else linear
-__device__ __forceinline__ int3 tile_of(const ExpP& e, int tt) {
-  const int id = e.tiles ? e.tiles[tt] : tt;
-  return make_int3(id % e.tg[0], (id / e.tg[0]) % e.tg[1], id / (e.tg[0] * e.tg[1]));
-}
+#include "explicit_common.cuh"
 
 namespace {
 
@@ -90,6 +64,7 @@ __global__ void k_explicit_1d(const double* __restrict__ U, const double* Pv, do
 }
 
 #include "explicit3d.cuh"
+#include "explicit3d_v2.cuh"
 #include "explicit2d.cuh"
 
 // ------------------------------------------------------------------ irregular d nodes
@@ -463,7 +438,7 @@ void launch_explicit_p(sc_ctx* c, const double* U, const double* Pv, double* out
     if constexpr (P <= 6) {
       using T = Tile3<P>;
       // the shared-memory opt-in was set on this context's device at setup (explicit_prepare)
-      k_explicit_3d<P, T::E, T::EY, T::NT, T::MINB, T::SPV><<<grid, T::NT, T::smem, st>>>(U, Pv, out, c->d_ntype, e,
+      v2::k_exp3<P, T::E, T::EY, T::NT, T::MINB><<<grid, T::NT, v2::smem3<P, T::E, T::EY>(), st>>>(U, Pv, out, c->d_ntype, e,
                                                                                        c->d_flag);
     }
   }
@@ -475,8 +450,8 @@ template <int P>
 void explicit_prepare_p(sc_ctx* c) {
   if constexpr (P <= 6) {
     using T = Tile3<P>;
-    SC_CUDA(cudaFuncSetAttribute(k_explicit_3d<P, T::E, T::EY, T::NT, T::MINB, T::SPV>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::smem));
+    SC_CUDA(cudaFuncSetAttribute(v2::k_exp3<P, T::E, T::EY, T::NT, T::MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)v2::smem3<P, T::E, T::EY>()));
   }
   (void)c;
 }
@@ -836,6 +811,12 @@ void device_upload_reference(sc_ctx* c) {
   const double iw2 = 1.0 / (c->gll_w[0] + c->gll_w[c->g.p]);
   SC_CUDA(cudaMemcpyToSymbol(c_iw, iw.data(), sizeof(double) * iw.size()));
   SC_CUDA(cudaMemcpyToSymbol(c_iw2, &iw2, sizeof(double)));
+  {
+    // even-odd blocks of Mhat, Khat for the 3D explicit kernel (explicit3d_v2.cuh)
+    std::vector<double> eo(4 * SC_EO_STRIDE);
+    v2::eo_blocks(c->g.p, M.data(), K.data(), eo.data());
+    SC_CUDA(cudaMemcpyToSymbol(c_EO, eo.data(), sizeof(double) * eo.size()));
+  }
   SC_CUDA(cudaMalloc(&c->d_Kref, sizeof(double) * c->Kref.size()));
   SC_CUDA(cudaMemcpy(c->d_Kref, c->Kref.data(), sizeof(double) * c->Kref.size(), cudaMemcpyHostToDevice));
 
