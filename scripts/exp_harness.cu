@@ -1,8 +1,11 @@
 // Kernel experiments for the 3D explicit step (a1)+(a2), outside the library: a synthetic
 // all-uncut lattice (random u_n, u_{n-1}), the product kernel (explicit3d.cuh) against a
 // candidate, element-wise comparison and CUDA-event timing.  Diagnostics only (not product).
+// The r1 kernel (explicit3d.cuh) is the baseline; the candidate is chosen at compile time:
+//   -DWITH_V2 (the product kernel, explicit3d_v2.cuh), -DWITH_V2 -DWITH_V2T (its TMA-staged
+//   variant, scripts/experiments/), -DWITH_XYZ (separated passes, scripts/experiments/):
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr \
-//        -o scripts/exp_harness scripts/exp_harness.cu
+//        -DWITH_V2 -o scripts/exp_harness_v2 scripts/exp_harness.cu
 //   scripts/exp_harness N [reps] [mask]   (N^3 elements of order 4; mask: random unwanted nodes)
 #include <cuda_runtime.h>
 
@@ -14,7 +17,11 @@
 #include "../paper_2310_14712_b200/csrc/explicit_common.cuh"
 #include "../paper_2310_14712_b200/csrc/explicit3d.cuh"
 #ifdef WITH_V2
+#ifdef WITH_V2T
+#include "experiments/explicit3d_v2_tma.cuh"
+#else
 #include "../paper_2310_14712_b200/csrc/explicit3d_v2.cuh"
+#endif
 #ifndef V2_EX
 #define V2_EX 6
 #endif
@@ -52,7 +59,7 @@ void launch(const double* U, double* out, const uint8_t* nt, ExpP e, int* flag, 
 #endif
 
 #ifdef WITH_XYZ
-#include "../paper_2310_14712_b200/csrc/explicit3d_xyz.cuh"
+#include "experiments/explicit3d_xyz.cuh"
 #ifndef XYZ_EX
 #define XYZ_EX 6
 #endif
@@ -110,6 +117,44 @@ void launch(const double* U, double* out, const uint8_t* nt, ExpP e, int* flag, 
 }  // namespace xyz
 #define WITH_V2
 #define CAND xyz
+#elif defined(WITH_V2T)   // v2 with TMA row staging: scripts/experiments/explicit3d_v2_tma.cuh (measured slower)
+#include <cudaTypedefs.h>
+#define WITH_V2
+namespace v2t {
+template <int P>
+void launch(const double* U, double* out, const uint8_t* nt, ExpP e, int* flag, cudaStream_t st, bool first) {
+  constexpr int EX = V2_EX, EY = V2_EY;
+  constexpr size_t sm = v2::smem3<P, EX, EY, true>();
+  auto k = v2::k_exp3t<P, EX, EY, V2_NT, V2_MINB>;
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q) != cudaSuccess || !enc)
+      exit(4);
+  }
+  CUtensorMap map;
+  const cuuint64_t dims[1] = {(cuuint64_t)e.nl[0] * e.nl[1] * e.nl[2]};
+  const cuuint64_t strides[1] = {8};
+  const cuuint32_t box[1] = {(cuuint32_t)v2::tma_row3<P, EX>()};
+  const cuuint32_t es[1] = {1};
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 1, (void*)U, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    exit(5);
+  if (first) {
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) exit(3);
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, k);
+    printf("v2t <%d,%d,%d,%d,%d>: %d regs, %zu B smem, %d B local\n", P, EX, EY, V2_NT, V2_MINB, fa.numRegs, sm,
+           (int)fa.localSizeBytes);
+  }
+  e.ezl = V2_EZL;
+  e.tg[0] = (e.N[0] + EX - 1) / EX;
+  e.tg[1] = (e.N[1] + EY - 1) / EY;
+  e.ntiles = e.tg[0] * e.tg[1] * ((e.N[2] + e.ezl - 1) / e.ezl);
+  k<<<e.ntiles, V2_NT, sm, st>>>(map, U, out, out, nt, e, flag);
+}
+}  // namespace v2t
+#define CAND v2t
 #else
 #define CAND v2
 #endif

@@ -21,9 +21,11 @@
 // Compared with the element-local kernel (explicit3d.cuh) no halo element is contracted in
 // z and y, and no node is contracted twice in z: 30% fewer FP64 operations per node.
 #pragma once
+// EXPERIMENT (not built into libsc): separated x, y, z passes; measured slower
+// (profiles/r2_variants.txt).
 #include <cuda.h>
 
-#include "explicit3d_v2.cuh"   // even-odd helpers (v2::eo_*) and c_EO
+#include "../../paper_2310_14712_b200/csrc/explicit3d_v2.cuh"   // even-odd helpers (v2::eo_*) and c_EO
 
 namespace xyz {
 
