@@ -147,7 +147,8 @@ __device__ __forceinline__ void tile3(const double* __restrict__ U, const double
   constexpr int NYI = (RX * EYH + NT - 1) / NT;   // column items per thread
   constexpr int RPW = 32 / EXH;                   // x-pass rows per warp
   constexpr int NW = NT / 32;
-  constexpr int NXI = (TY + NW * RPW - 1) / (NW * RPW);
+  constexpr int NXS = (EY + 1 + RPW - 1) / RPW * RPW + EY * (P - 1);   // x-pass row slots (row_of)
+  constexpr int NXI = (NXS + NW * RPW - 1) / (NW * RPW);
   const double* EM = c_EO;
   const double* OM = c_EO + SC_EO_STRIDE;
   const double* EK = c_EO + 2 * SC_EO_STRIDE;
@@ -177,19 +178,37 @@ __device__ __forceinline__ void tile3(const double* __restrict__ U, const double
   const int rin = lane / EXH, exl = lane - (lane / EXH) * EXH;
   const double sig0 = e.s[0] / e.s[1], sig2 = e.s[2] / e.s[1];
 
+  // stage layer ez: warp per region row, lanes along x (no index division)
   auto issue = [&](int ez, int buf) {
     double* dst = LU + buf * P1 * RC;
-    const double* base = U + (size_t)(ez * P) * pl;
-    for (int col = tid; col < RX * RY; col += NT) {
-      const int iy = col / RX, ix = col - iy * RX;
-      const int gx = xr0 + ix, gy = yr0 + iy;
-      const bool ok = INT || (gx >= 0 && gy >= 0 && gx <= gxmax && gy <= gymax);
-      const double* src = base + (ok ? gx + (size_t)nx * gy : 0);
-      double* d = dst + iy * RXP + ix;
+    const double* base = U + (size_t)(ez * P) * pl + xr0;
+    for (int iy = warp; iy < RY; iy += NW) {
+      const int gy = yr0 + iy;
+      const bool oky = INT || (gy >= 0 && gy <= gymax);
+      for (int ix = lane; ix < RX; ix += 32) {
+        const int gx = xr0 + ix;
+        const bool ok = oky && (INT || (gx >= 0 && gx <= gxmax));
+        const double* src = ok ? base + ix + (size_t)nx * gy : U;
+        double* d = dst + iy * RXP + ix;
 #pragma unroll
-      for (int k = 0; k < P1; ++k) cp_async8(d + k * RC, src + (ok ? pl * k : 0), ok);
+        for (int k = 0; k < P1; ++k) cp_async8(d + k * RC, src + (ok ? pl * k : 0), ok);
+      }
     }
     cp_async_commit();
+  };
+
+  // x-pass row of slot (warp, round q, lane group rin): the element-boundary ("vertex") rows
+  // first, padded to whole warps, then the interior rows, so that the vertex rows' extra
+  // BMP/BTP reads are warp-uniform; -1: no row
+  auto row_of = [&](int q) {
+    constexpr int NV = EY + 1, NVP = (NV + RPW - 1) / RPW * RPW, NI = EY * (P - 1);
+    const int sl = (warp + q * NW) * RPW + rin;
+    if (rin >= RPW) return -1;
+    if (sl < NV) return sl * P;
+    if (sl < NVP || P == 1) return -1;
+    const int t = sl - NVP;
+    if (t >= NI) return -1;
+    return (t / (P - 1)) * P + 1 + t % (P - 1);
   };
 
   // ---- per-thread constants of the x-pass row items (hoisted out of the plane loop)
@@ -200,8 +219,9 @@ __device__ __forceinline__ void tile3(const double* __restrict__ U, const double
   bool act[NXI], hasA[NXI];
 #pragma unroll
   for (int q = 0; q < NXI; ++q) {
-    const int oy = (warp + q * NW) * RPW + rin;
-    act[q] = rin < RPW && oy < OY && exl <= nEX && (exl > 0 || xlo);
+    const int oyr = row_of(q);
+    const int oy = oyr < 0 ? 0 : oyr;
+    act[q] = oyr >= 0 && oy < OY && exl <= nEX && (exl > 0 || xlo);
     const int qq = oy / P, ly = oy - qq * P;
     hasA[q] = oy < nEY * P;
     const bool hasP = ly == 0 && (qq > 0 || ylo);
@@ -324,16 +344,6 @@ __device__ __forceinline__ void tile3(const double* __restrict__ U, const double
         // ---- x pass (even-odd) + CDM update of plane k
         const int gz = ez * P + k;
         const double* Lk = L + k * RC;
-        double pvc[NXI][P1];
-        uint8_t ntc[NXI][P1];
-#pragma unroll
-        for (int q = 0; q < NXI; ++q)
-#pragma unroll
-          for (int l = 0; l < P1; ++l) {
-            pvc[q][l] = pv[q][l];
-            if constexpr (!CLEAN) ntc[q][l] = ntv[q][l];
-          }
-        prefetch(gz + 1);   // next plane (the next layer's plane 0 after k = P - 1)
         // lumped-mass reciprocal of plane k: interior planes compile-time, the layer's bottom
         // plane an element boundary unless on the grid's bottom face, plane P only on the top face
         const double iwzt = (k > 0 && k < P) ? c_iw[k] : (k == P ? c_iw[0] : ((ez > 0) ? c_iw2 : c_iw[0]));
@@ -372,16 +382,19 @@ __device__ __forceinline__ void tile3(const double* __restrict__ U, const double
             for (int l = 0; l < P1; ++l) {
               if (l == P && !(exl == nEX && lastx)) break;
               bool w = true;
-              if constexpr (!CLEAN) w = (e.want >> ntc[q][l]) & 1;
+              if constexpr (!CLEAN) w = (e.want >> ntv[q][l]) & 1;
               if (w) {
                 const double iwx = l == 0 ? iw0 : (l == P ? iwP : c_iw[l]);
-                const double res = fma(e.a1, urow[l], fma(e.a2, pvc[q][l], -(cyz * iwx) * r[l]));
+                const double res = fma(e.a1, urow[l], fma(e.a2, pv[q][l], -(cyz * iwx) * r[l]));
                 orow[l] = res;
                 bad |= !isfinite(res);
               }
             }
           }
         }
+        // u_{n-1} of the next plane (the next layer's plane 0 after k = P - 1), in flight
+        // during the next plane's z+y phase
+        prefetch(gz + 1);
         pp ^= 1;
       }
     }
