@@ -199,11 +199,21 @@ extern "C" sc_status sc_setup(const sc_grid* grid, int32_t p, double alpha, cons
         c->src_amp = src->amp;
       }
     }
+    // SC_SETUP_TIMES (diagnostics): setup phase times on stderr
+    auto lap = [&, tl = std::chrono::steady_clock::now()](const char* what) mutable {
+      const auto now = std::chrono::steady_clock::now();
+      if (getenv("SC_SETUP_TIMES")) fprintf(stderr, "sc_setup %-22s %8.3f s\n", what, std::chrono::duration<double>(now - tl).count());
+      tl = now;
+    };
     host_reference(c);
     device_upload_reference(c);
+    lap("reference");
     setup_device_geometry(c);
+    lap("geometry+cut matrices");
     setup_factor(c, {});
+    lap("factorisation");
     setup_step_structures(c);
+    lap("step structures");
     // state buffers
     const size_t latb = sizeof(double) * c->n_lat;
     SC_CUDA(cudaMalloc(&c->d_u[0], latb));

@@ -16,6 +16,9 @@
 // c-index maps, and the CSR that gathers element products into r^c.
 #include <omp.h>
 
+#include <chrono>
+#include <cstdio>
+
 #include <algorithm>
 #include <map>
 #include <cmath>
@@ -98,7 +101,11 @@ struct UF {
 // ---------------------------------------------------------------- dense kernels
 // Partial Cholesky of the (n x n, lower, column-major, ld) front on its first w columns,
 // then the Schur update of the trailing (n-w) block.  Returns the failing column or -1.
-int front_factor(double* F, int n, int w) {
+// The dense host kernels are compiled twice (AVX2 and baseline x86-64, selected at load time
+// by the CPU): their inner loops are independent element updates, so the vector versions give
+// the same bits (no reassociation, no contraction: -ffp-contract=off).
+#define SC_HOST_SIMD __attribute__((target_clones("avx2", "default")))
+SC_HOST_SIMD int front_factor(double* F, int n, int w) {
   for (int j = 0; j < w; ++j) {
     double* Fj = F + (size_t)j * n;
     for (int k = 0; k < j; ++k) {
@@ -133,7 +140,7 @@ int front_factor(double* F, int n, int w) {
 }
 
 // inverse of the lower-triangular w x w block L (column-major, ld n) into X (w x w, col-major)
-void tri_inverse(const double* L, int n, int w, double* X) {
+SC_HOST_SIMD void tri_inverse(const double* L, int n, int w, double* X) {
   std::fill(X, X + (size_t)w * w, 0.0);
   for (int col = 0; col < w; ++col) {
     double* x = X + (size_t)col * w;
@@ -157,7 +164,7 @@ void tri_inverse(const double* L, int n, int w, double* X) {
 int panel_wp(int w) { return (w + 1) & ~1; }
 int panel_ld(int w, int r) { return panel_wp(w) + ((r + 1) & ~1); }
 
-void make_panel(const double* F, int n, int w, double* P) {
+SC_HOST_SIMD void make_panel(const double* F, int n, int w, double* P) {
   const int r = n - w, wp = panel_wp(w), ld = panel_ld(w, r);
   std::fill(P, P + (size_t)ld * w, 0.0);
   std::vector<double> X((size_t)w * w);
@@ -420,6 +427,13 @@ void bell_weights(const sc_ctx* c, std::vector<std::pair<int64_t, double>>& out)
 }
 
 void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
+  // SC_SETUP_TIMES (diagnostics): phase times on stderr
+  auto flap = [tl = std::chrono::steady_clock::now()](const char* what) mutable {
+    const auto now = std::chrono::steady_clock::now();
+    if (getenv("SC_SETUP_TIMES"))
+      fprintf(stderr, "sc_setup   factor: %-34s %8.3f s\n", what, std::chrono::duration<double>(now - tl).count());
+    tl = now;
+  };
   Builder b;
   b.c = c;
   const GridP& g = c->g;
@@ -444,6 +458,16 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
       if (c->ntype[L] == 1 || c->ntype[L] == 2 || c->ntype[L] == 4) c->ntype[L] = 3;
   c->dof_lat.clear();
   c->n_d = c->n_c = c->n_irr = 0;
+  {
+    int64_t nd = 0, ncc = 0;
+#pragma omp parallel for reduction(+ : nd, ncc)
+    for (int64_t i = 0; i < c->n_lat; ++i) {
+      nd += c->ntype[i] != 0;
+      ncc += c->ntype[i] == 3;
+    }
+    c->dof_lat.reserve((size_t)nd);
+    b.clat.reserve((size_t)ncc);
+  }
   for (int64_t i = 0; i < c->n_lat; ++i) {
     const uint8_t t = c->ntype[i];
     if (!t) continue;
@@ -624,6 +648,7 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
     }
   };
   build_c(true);
+  flap("DOF lists, c elements, components");
   // ---------------- partition plan (world > 1; partition.cpp): component owners, regions
   const std::vector<int64_t> clat_global = b.clat;
   std::vector<int> c_owner(nc, 0);
@@ -727,6 +752,7 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   }
   c->n_cl = nc;
 
+  flap("partition plan");
   // ---------------- nested dissection -> ND order and supernodes
   std::vector<int> order;  // ND index -> canonical
   order.reserve(nc);
@@ -747,6 +773,7 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   // convert element maps to ND indices
   for (auto& v : b.celem_cidx)
     if (v >= 0) v = b.nd_of_canon[v];
+  flap("nested dissection");
   // ---------------- symbolic: R_s = (adj(cols) U struct(children)) above the supernode
   const int nsn = (int)b.sn.size();
   std::vector<int> sn_of(nc);
@@ -788,6 +815,7 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
       }
     }
   }
+  flap("symbolic");
   // ---------------- numeric multifrontal factorisation of S and M^cc
   const double beta_dt2 = 0.25 * c->dt * c->dt;
   // symmetric Jacobi scaling D A D (unit diagonal): the fictitious-region rows of S are
@@ -854,9 +882,27 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   const double* Mref = c->Mref.data();
   // (no factor for the explicit HRZ integrator: the panels stay zero and the solve never runs)
   const int n_fact = c->integrator == 1 ? 0 : (int)comps.size();
-#pragma omp parallel for schedule(dynamic, 1)
+  // tasks (component, matrix) in decreasing order of their dense work (sum of front sizes
+  // cubed): the two factorisations of a component are independent, and the largest
+  // components start first (they bound the wall time)
+  std::vector<std::pair<double, int>> tasks;
   for (int k = 0; k < n_fact; ++k) {
-    for (int which = 0; which < 2; ++which) {  // 0: S, 1: M^cc
+    double cost = 0.0;
+    for (int sn : comp_sn[k]) {
+      const double nn = (double)b.sn[sn].w + (double)b.sn[sn].R.size();
+      cost += nn * nn * nn;
+    }
+    tasks.push_back({cost, 2 * k});
+    tasks.push_back({cost, 2 * k + 1});
+  }
+  std::stable_sort(tasks.begin(), tasks.end(), [](const std::pair<double, int>& a, const std::pair<double, int>& b) {
+    return a.first > b.first;
+  });
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int tk = 0; tk < (int)tasks.size(); ++tk) {
+    const int k = tasks[tk].second / 2;
+    {
+      const int which = tasks[tk].second % 2;     // 0: S, 1: M^cc
       std::vector<std::vector<double>> upd(nsn);  // update matrices (sparse by sn id; only this comp used)
       for (int s : comp_sn[k]) {
         const SNode& S = b.sn[s];
@@ -920,6 +966,7 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
     throw ScError(SC_ERR_NUMERIC, std::string("non-positive pivot in the factorisation of ") +
                                       (fail_which == 0 ? "S" : "M^cc") + " (component " +
                                       std::to_string(fail_comp) + ", row " + std::to_string(fail_row) + ")");
+  flap("numeric");
   // ---------------- device structures
   c->n_sn = nsn;
   int H = 0;
@@ -1201,4 +1248,5 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   c->Kcut_host.shrink_to_fit();
   c->Mcut_host.clear();
   c->Mcut_host.shrink_to_fit();
+  flap("device structures");
 }

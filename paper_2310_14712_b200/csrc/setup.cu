@@ -220,7 +220,9 @@ __device__ __forceinline__ void comp_add(double& s, double& c, double x, double 
 }
 
 // Cut-cell element matrices: one CTA per CUT cell; each thread owns a 4x4 tile of both M_e
-// and K_e; quadrature points are staged in chunks of QC points in shared memory.
+// and K_e (tiles on and above the diagonal only: M_e and K_e are symmetric, the lower tiles are
+// written as mirror images); quadrature points are staged in chunks of QC points in shared
+// memory and replayed once per group of blockDim.x tiles.
 #define QC 8
 __global__ void __launch_bounds__(256) k_cut_matrices(GridP g, const DVoid* __restrict__ V, int nv, const long long* __restrict__ cells,
                                const int* __restrict__ slot, const unsigned long long* __restrict__ leaves,
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__(256) k_cut_matrices(GridP g, const DVoid* __re
   __syncthreads();
   const int nc = s_nc;
   const int T = nbp / 4;
-  const int ntiles = T * T;
+  const int ntiles = T * (T + 1) / 2;   // upper-triangular tiles (ti <= tj)
   const int npts = (d == 1) ? P1 : (d == 2 ? P1 * P1 : P1 * P1 * P1);
   const int nl = nleaves[sl];
   const long long total = (long long)nl * npts;
@@ -258,7 +260,12 @@ __global__ void __launch_bounds__(256) k_cut_matrices(GridP g, const DVoid* __re
   // tile groups: each thread owns one 4x4 tile per group; the quadrature is replayed per group
   for (int tg = 0; tg * (int)blockDim.x < ntiles; ++tg) {
   const int tile = tg * blockDim.x + threadIdx.x;
-  const int i0 = (tile % T) * 4, j0 = (tile / T) * 4;
+  int ti = 0, rem = tile;   // tile -> (ti, tj), ti <= tj, row-major over the upper triangle
+  while (ti < T && rem >= T - ti) {
+    rem -= T - ti;
+    ++ti;
+  }
+  const int i0 = ti * 4, j0 = (ti + rem) * 4;
   const bool active = tile < ntiles;
   // compensated (Neumaier + exact-product) accumulation: the quadrature sums have up to
   // (2^D)^d (p+1)^d terms with cancellation; plain accumulation loses ~sqrt(n) ulps, which
@@ -359,9 +366,12 @@ __global__ void __launch_bounds__(256) k_cut_matrices(GridP g, const DVoid* __re
     for (int a = 0; a < 4; ++a)
       for (int b = 0; b < 4; ++b) {
         const int i = i0 + a, j = j0 + b;
-        if (i < nb && j < nb) {
-          Kout[(long long)e * nb * nb + (long long)i * nb + j] = rho * c2 * (accK[a][b] + cmpK[a][b]);
-          Mout[(long long)e * nb * nb + (long long)i * nb + j] = rho * (accM[a][b] + cmpM[a][b]);
+        if (i < nb && j < nb && i <= j) {   // (i, j) and its mirror (j, i): exactly symmetric
+          const double kv = rho * c2 * (accK[a][b] + cmpK[a][b]), mv = rho * (accM[a][b] + cmpM[a][b]);
+          Kout[(long long)e * nb * nb + (long long)i * nb + j] = kv;
+          Mout[(long long)e * nb * nb + (long long)i * nb + j] = mv;
+          Kout[(long long)e * nb * nb + (long long)j * nb + i] = kv;
+          Mout[(long long)e * nb * nb + (long long)j * nb + i] = mv;
         }
       }
   }
@@ -644,7 +654,10 @@ void setup_device_geometry(sc_ctx* c) {
     SC_CUDA(cudaMalloc(&d_M, sizeof(double) * mat));
     const int nbp = ((nb + 15) / 16) * 16;
     if (nbp > 128) throw ScError(SC_ERR_CONFIG, "(p+1)^dim > 128 not supported by the cut-cell kernel");
-    const int threads = std::min(256, std::max(32, (nbp / 4) * (nbp / 4)));
+    // threads: one upper-triangular 4x4 tile each per replay of the quadrature (nbp = 128: 528
+    // tiles, 3 replays of 256; 256 threads keep the 202-register accumulators unspilled)
+    const int ntile = (nbp / 4) * (nbp / 4 + 1) / 2;
+    const int threads = std::min(256, std::max(32, (ntile + 31) / 32 * 32));
     const size_t smem = sizeof(double) * (4 * QC * nbp + 2 * QC * 3 * SC_MAXP1 + QC);
     SC_CUDA(cudaFuncSetAttribute(k_cut_matrices, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_cut_matrices<<<(unsigned)c->n_cut, threads, smem, c->stream>>>(
