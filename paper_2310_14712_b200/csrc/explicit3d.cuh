@@ -318,19 +318,19 @@ __global__ void __launch_bounds__(NT, MINB) k_explicit_3d(const double* __restri
 }
 
 // Tile shapes (EX = E along x, EY along y): the z+y phase has RX*(EY+1) column items and the
-// x phase (EY*P+1) rows of (E+1) lanes; NT is chosen so that both keep >= 84% of the threads
-// busy (one item each).  p = 4 (config 5; profiles/r1_solve_variants.txt, explicit section):
-// E = EY = 6, NT = 224, 2 CTAs/SM, u_{n-1} prefetched into registers: 3.92 ms; E = 5, NT = 160
-// at 3 CTAs/SM 4.17 ms (u_{n-1} staged in shared memory at 2 CTAs/SM: 4.53 ms); E = 4 at
-// 4 CTAs/SM 4.50 ms — the low-side halo element costs (E+1)^2/E^2 of the z+y work.
+// x phase (EY*P+1) rows of (E+1) lanes; NT is sized so both keep most threads busy (one item
+// each).  p = 4 (config 5; harness scripts/exp_harness.cu, profiles/r2_variants.txt): E = 8,
+// EY = 4, NT = 192, 2 CTAs/SM at ~160 registers without spills 2.66 ms; 6x5 2.74, 7x4 2.76, 9x3
+// 2.79; every 224-thread shape (capped at 128 registers: 6x6 3.12, 9x4 3.01, 12x3 3.10) and the
+// 3-CTA shapes (8x3 at 160 threads 2.94) are slower.
 #ifndef EXP4_E
-#define EXP4_E 6
+#define EXP4_E 8
 #endif
 #ifndef EXP4_EY
-#define EXP4_EY EXP4_E
+#define EXP4_EY 4
 #endif
 #ifndef EXP4_NT
-#define EXP4_NT 224
+#define EXP4_NT 192
 #endif
 #ifndef EXP4_MINB
 #define EXP4_MINB 2

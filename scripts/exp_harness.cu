@@ -266,7 +266,10 @@ __global__ void k_diff(const double* a, const double* b, size_t n, double* out) 
 }
 
 int main(int argc, char** argv) {
-  constexpr int P = 4;
+#ifndef HP
+#define HP 4
+#endif
+  constexpr int P = HP;   // element order (compile time: -DHP=3)
   const int Ncell = argc > 1 ? atoi(argv[1]) : 160;
   const int reps = argc > 2 ? atoi(argv[2]) : 10;
   const int mask = argc > 3 ? atoi(argv[3]) : 0;
@@ -274,7 +277,7 @@ int main(int argc, char** argv) {
   std::vector<double> gx, gw, lx, lw;
   gauss(P + 1, gx, gw);
   gll(P, lx, lw);
-  double Mh[25] = {0}, Kh[25] = {0};
+  double Mh[(P + 1) * (P + 1)] = {0}, Kh[(P + 1) * (P + 1)] = {0};
   for (int q = 0; q <= P; ++q) {
     double v[P + 1], dv[P + 1];
     lagr(lx, gx[q], v, dv);

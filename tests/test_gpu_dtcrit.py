@@ -1,4 +1,4 @@
-"""NEXT-2: device power iteration for the critical time step of the explicit
+"""NEXT-2: device Lanczos iteration for the critical time step of the explicit
 subsystem, dt = 2 / sqrt(lambda_max(K_dd, M_dd)), against the oracle's
 dense generalized eigenvalue of the same (K_dd, M_dd); and the paper's relation that the
 IMEX critical step is governed by the uncut cells (Table tab:criticaltimestepsizes)."""
@@ -42,10 +42,10 @@ def test_power_iteration_matches_dense_eigenvalue(pkg, dim, cells, p):
     cfg["dt"] = 0.9 * dt_crit_uncut(dim, p, 1.0 / max(cells))
     ref = _oracle_lambda(cfg)
     s = pkg.from_config(cfg)
-    lam, dt = s.estimate_dt(6000)
+    lam, dt = s.estimate_dt(3000)                # Lanczos (M inner product), converged well before
     s.close()
-    assert lam <= ref * (1 + 1e-12)              # the iteration approaches from below
-    assert abs(lam - ref) / ref < 1e-3, (lam, ref)
+    assert lam <= ref * (1 + 1e-12)              # Ritz values approach from below
+    assert abs(lam - ref) / ref < 1e-10, (lam, ref)
     assert abs(dt - 2.0 / np.sqrt(lam)) < 1e-15 * dt
 
 

@@ -51,7 +51,8 @@ def test_cdm_hrz_matches_oracle(pkg, dim, cells, p, void):
     ref = cdm(pr, cfg["dt"], steps, sc_inputs.source_signal(cfg, steps + 1), np.zeros(sysm.n_dof))
     err = np.linalg.norm(u - ref) / np.linalg.norm(ref)
     assert np.abs(ref).max() > 0 and err < 1e-10, err
-    assert lam_gpu <= lam * (1 + 1e-12) and abs(lam_gpu - lam) / lam < 1e-3, (lam_gpu, lam)
+    # Lanczos in the HRZ mass inner product (sc_estimate_dt): converged to rounding
+    assert lam_gpu <= lam * (1 + 1e-12) and abs(lam_gpu - lam) / lam < 1e-10, (lam_gpu, lam)
 
 
 def test_hrz_step_is_restricted_by_cut_cells(pkg):
