@@ -302,7 +302,7 @@ def main():
     # of the same workload (scripts/ncu_traffic.py), when there is one
     traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_config{cfg['id']}.json")
-    kname = {"explicit": "k_explicit_3d" if cfg["dim"] == 3 else f"k_explicit_{cfg['dim']}d",
+    kname = {"explicit": "v2::k_exp3" if cfg["dim"] == 3 else f"k_explicit_{cfg['dim']}d",
              "celem": "k_celem", "solve": "k_solve"}[dom]
     if world == 1 and os.path.exists(tpath):
         tj = json.load(open(tpath))

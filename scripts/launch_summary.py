@@ -18,7 +18,7 @@ def load(path):
         if row.get("Metric Name") != "gpu__time_duration.sum":
             continue
         name = row["Kernel Name"].split("(")[0]
-        name = re.sub(r"<unnamed>::|\(anonymous namespace\)::", "", name)
+        name = re.sub(r"<unnamed>::|\(anonymous namespace\)::|^void ", "", name)
         v = float(row["Metric Value"].replace(",", ""))
         u = row["Metric Unit"]
         v *= {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(u, 1.0)
@@ -44,7 +44,7 @@ if __name__ == "__main__":
     rows = load(sys.argv[1])
     if "--skip-setup" in sys.argv:
         # drop setup + startup: keep from the second k_explicit launch on
-        idx = [i for i, r in enumerate(rows) if r[0].startswith("k_explicit")]
+        idx = [i for i, r in enumerate(rows) if r[0].startswith(("k_explicit", "v2::k_exp3"))]
         if len(idx) > 1:
             rows = rows[idx[1]:]
     print(summary(rows))
