@@ -51,7 +51,8 @@ static void free_ctx(sc_ctx* c) {
   void* ptrs[] = {c->d_voids, c->d_u[0], c->d_u[1], c->d_ntype, c->d_cell_class, c->d_dof_lat, c->d_out,
                   c->d_ft, c->d_step, c->d_flag, c->d_irr_lat, c->d_irr_invm, c->d_irr_fx, c->d_load_lat, c->d_load_fxm, c->d_Kref,
                   c->d_c_lat, c->d_vc, c->d_ac, c->d_fxc, c->d_b, c->d_q, c->d_x, c->d_U,
-                  c->d_celem_cell, c->d_celem_kidx, c->d_celem_cidx, c->d_Kcut, c->d_cut_dt, c->d_Y, c->d_rhs_ptr,
+                  c->d_celem_cell, c->d_celem_kidx, c->d_celem_cidx, c->d_celem_cut_ids, c->d_celem_ref_ids,
+                  c->d_Kcut, c->d_cut_dt, c->d_Y, c->d_rhs_ptr,
                   c->d_rhs_idx, c->d_sn_c0, c->d_sn_w, c->d_sn_r, c->d_sn_aoff, c->d_sn_roff,
                   c->d_sn_uoff, c->d_sn_goff, c->d_R, c->d_gptr, c->d_gidx, c->d_items, c->fS.A,
                   c->fM.A, c->fS.d, c->fM.d, c->d_tmp, c->d_nitem, c->d_chptr, c->d_chidx, c->d_parent, c->d_solve_cnt,

@@ -1173,6 +1173,16 @@ void setup_factor(sc_ctx* c, const std::vector<double>& /*unused*/) {
   up32(&c->d_celem_cell, cell32);
   up32(&c->d_celem_kidx, kidx32);
   up32(&c->d_celem_cidx, b.celem_cidx);
+  // element id lists: cut elements (dense K_e streamed, k_celem) and uncut ones (the reference
+  // K_e shared by all: one batched product, k_celem_ref)
+  {
+    std::vector<int32_t> ids_cut, ids_ref;
+    for (int e = 0; e < ne; ++e) (kidx32[e] >= 0 ? ids_cut : ids_ref).push_back(e);
+    c->n_celem_cut = (int64_t)ids_cut.size();
+    c->n_celem_ref = (int64_t)ids_ref.size();
+    up32(&c->d_celem_cut_ids, ids_cut);
+    up32(&c->d_celem_ref_ids, ids_ref);
+  }
   // r^c gather CSR in ND order
   std::vector<int32_t> rptr(nc + 1, 0), ridx;
   ridx.reserve(b.node_eidx.size());

@@ -166,48 +166,54 @@ static void launch_load_d(sc_ctx* c, double* out, double a3, cudaStream_t st) {
 #ifndef CELEM_CS
 #define CELEM_CS 0
 #endif
+// local node j of c element e: its value in w_e = [u^d_{n+1}; u~^c] (mode 0: predictor for c
+// nodes), u (mode 1), or the leap-frog substep value (mode 2)
+__device__ __forceinline__ double celem_w(int mode, const double* __restrict__ A, const double* __restrict__ B,
+                                          const double* __restrict__ vc, const double* __restrict__ ac, double dt,
+                                          const int32_t* __restrict__ ecidx, int e, int nb, int j,
+                                          const long long ci[3], const GridP& g, double theta) {
+  const int n1 = g.p + 1;
+  const int l0 = j % n1, l1 = (j / n1) % n1, l2 = j / (n1 * n1);
+  long long gl = ci[0] * g.p + l0;
+  if (g.dim > 1) gl += g.nl[0] * (ci[1] * g.p + l1);
+  if (g.dim > 2) gl += g.nl[0] * g.nl[1] * (ci[2] * g.p + l2);
+  if (mode == 1) return A[gl];
+  const int cc = ecidx[(size_t)e * nb + j];
+  if (mode == 2) return cc >= 0 ? vc[cc] : fma(theta, B[gl] - A[gl], A[gl]);
+  return cc >= 0 ? A[gl] + dt * vc[cc] + 0.25 * dt * dt * ac[cc] : B[gl];
+}
+
+__device__ __forceinline__ void cell_ci(const GridP& g, long long cell, long long ci[3]) {
+  long long rem = cell;
+  for (int k = 0; k < 3; ++k) {
+    if (k < g.dim) {
+      ci[k] = rem % g.N[k];
+      rem /= g.N[k];
+    } else {
+      ci[k] = 0;
+    }
+  }
+}
+
+// ids: the c elements of this launch (the cut ones: their dense K_e is streamed once)
 __global__ void k_celem(int mode, const double* __restrict__ A, const double* __restrict__ B,
                         const double* __restrict__ vc, const double* __restrict__ ac, double dt,
                         const int32_t* __restrict__ ecell, const int32_t* __restrict__ ekidx,
                         const int32_t* __restrict__ ecidx, const double* __restrict__ Kcut,
                         const double* __restrict__ Kref, double* __restrict__ Y, int ne, int nb, int tpe, GridP g,
-                        double theta) {
+                        double theta, const int32_t* __restrict__ ids) {
   extern __shared__ double sw[];
   const int epb = blockDim.x / tpe;
   const int le = threadIdx.x / tpe, i = threadIdx.x % tpe;
-  const int e = blockIdx.x * epb + le;
-  const bool ok = e < ne;
+  const int slot = blockIdx.x * epb + le;
+  const bool ok = slot < ne;
+  const int e = ok ? ids[slot] : 0;
   const int n1 = g.p + 1;
   double* w = sw + le * nb;
   if (ok) {
-    const long long cell = ecell[e];
     long long ci[3];
-    long long rem = cell;
-    for (int k = 0; k < 3; ++k) {
-      if (k < g.dim) {
-        ci[k] = rem % g.N[k];
-        rem /= g.N[k];
-      } else {
-        ci[k] = 0;
-      }
-    }
-    for (int j = i; j < nb; j += tpe) {
-      const int l0 = j % n1, l1 = (j / n1) % n1, l2 = j / (n1 * n1);
-      long long gl = ci[0] * g.p + l0;
-      if (g.dim > 1) gl += g.nl[0] * (ci[1] * g.p + l1);
-      if (g.dim > 2) gl += g.nl[0] * g.nl[1] * (ci[2] * g.p + l2);
-      double v;
-      if (mode == 1) {
-        v = A[gl];
-      } else if (mode == 2) {
-        const int cc = ecidx[(size_t)e * nb + j];
-        v = cc >= 0 ? vc[cc] : fma(theta, B[gl] - A[gl], A[gl]);
-      } else {
-        const int cc = ecidx[(size_t)e * nb + j];
-        v = cc >= 0 ? A[gl] + dt * vc[cc] + 0.25 * dt * dt * ac[cc] : B[gl];
-      }
-      w[j] = v;
-    }
+    cell_ci(g, ecell[e], ci);
+    for (int j = i; j < nb; j += tpe) w[j] = celem_w(mode, A, B, vc, ac, dt, ecidx, e, nb, j, ci, g, theta);
   }
   __syncthreads();
   if (!ok) return;
@@ -232,6 +238,108 @@ __global__ void k_celem(int mode, const double* __restrict__ A, const double* __
   // matrix stays cached
   if (CELEM_CS && kidx >= 0) gemv([](const double* p) { return __ldcs(p); });
   else gemv([](const double* p) { return __ldg(p); });
+}
+
+// Uncut c elements all share the reference K_e (Kref, symmetric): Y_e = Kref w_e for a batch of
+// CR_EB elements is one small GEMM Kref [nb x nb] x W [nb x CR_EB].  W gathered into shared
+// memory; each thread a 4-row x 4-element register tile (lanes over rows, warps over
+// elements), Kref rows read through L1 (128 KB, cached), W broadcast from shared memory.
+#define CR_EB 32
+template <int NB>   // nodes per element (compile time: the product loop is unrolled)
+__global__ void __launch_bounds__(256) k_celem_ref(int mode, const double* __restrict__ A, const double* __restrict__ B,
+                                                   const double* __restrict__ vc, const double* __restrict__ ac,
+                                                   double dt, const int32_t* __restrict__ ecell,
+                                                   const int32_t* __restrict__ ecidx, const double* __restrict__ Kref,
+                                                   double* __restrict__ Y, int n, int /*nb*/, GridP g, double theta,
+                                                   const int32_t* __restrict__ ids) {
+  constexpr int nb = NB;
+  extern __shared__ double sW[];   // [nb][CR_EB]
+  __shared__ long long sci[CR_EB][3];
+  __shared__ int se[CR_EB];
+  const int s0 = blockIdx.x * CR_EB;
+  const int ne = min(CR_EB, n - s0);
+  if (threadIdx.x < ne) {   // cell coordinates once per element
+    const int e = ids[s0 + threadIdx.x];
+    se[threadIdx.x] = e;
+    long long ci[3];
+    cell_ci(g, ecell[e], ci);
+    for (int k = 0; k < 3; ++k) sci[threadIdx.x][k] = ci[k];
+  }
+  __syncthreads();
+  // gather W: each thread's (up to 16) entries in two passes, so that their loads are in flight
+  // together (lattice index + c index first, then the values)
+  constexpr int GU = CR_EB * 128 / 256;
+  const int n1 = g.p + 1;
+  long long glv[GU];
+  int ccv[GU];
+#pragma unroll
+  for (int u = 0; u < GU; ++u) {
+    const int t = threadIdx.x + u * 256;
+    const int b = t / nb, j = t - b * nb;
+    glv[u] = -1;
+    ccv[u] = -1;
+    if (t < CR_EB * nb && b < ne) {
+      const int l0 = j % n1, l1 = (j / n1) % n1, l2 = j / (n1 * n1);
+      long long gl = sci[b][0] * g.p + l0;
+      if (g.dim > 1) gl += g.nl[0] * (sci[b][1] * g.p + l1);
+      if (g.dim > 2) gl += g.nl[0] * g.nl[1] * (sci[b][2] * g.p + l2);
+      glv[u] = gl;
+      if (mode != 1) ccv[u] = ecidx[(size_t)se[b] * nb + j];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < GU; ++u) {
+    const int t = threadIdx.x + u * 256;
+    if (t >= CR_EB * nb) break;
+    const int b = t / nb, j = t - b * nb;
+    double v = 0.0;
+    const long long gl = glv[u];
+    const int cc = ccv[u];
+    if (gl >= 0) {
+      if (mode == 1) v = A[gl];
+      else if (mode == 2) v = cc >= 0 ? vc[cc] : fma(theta, B[gl] - A[gl], A[gl]);
+      else v = cc >= 0 ? A[gl] + dt * vc[cc] + 0.25 * dt * dt * ac[cc] : B[gl];
+    }
+    sW[j * CR_EB + b] = v;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wg = threadIdx.x >> 5;
+  const int b0 = wg * 4;   // this warp's 4 elements; lanes take rows lane + 32 a (coalesced)
+  if (b0 >= ne) return;
+  for (int rb = 0; rb < nb; rb += 128) {   // nb <= 128 in 3D p = 4: one pass
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+#pragma unroll 5
+    for (int j = 0; j < nb; ++j) {
+      double k[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int r = rb + lane + 32 * a;
+        k[a] = r < nb ? __ldg(Kref + (size_t)j * nb + r) : 0.0;   // Kref[r][j] (symmetric)
+      }
+      const double* wj = sW + j * CR_EB + b0;
+      double w[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) w[c] = wj[c];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][c] = fma(k[a], w[c], acc[a][c]);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (b0 + c >= ne) break;
+      double* y = Y + (size_t)se[b0 + c] * nb;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int r = rb + lane + 32 * a;
+        if (r < nb) y[r] = acc[a][c];
+      }
+    }
+  }
 }
 
 __global__ void k_crhs(double* __restrict__ b, const double* __restrict__ fxc, const int32_t* __restrict__ ptr,
@@ -536,11 +644,35 @@ static void launch_celem(sc_ctx* c, int mode, const double* A, const double* B, 
   const int nb = c->nb;
   const int tpe = std::min(256, ((nb + 31) / 32) * 32);
   const int epb = 256 / tpe;
-  const unsigned blocks = (unsigned)((c->n_celem + epb - 1) / epb);
-  k_celem<<<blocks, epb * tpe, sizeof(double) * epb * nb, st>>>(
-      mode, A, B, vc ? vc : c->d_vc, c->d_ac, c->dt, c->d_celem_cell, c->d_celem_kidx, c->d_celem_cidx, c->d_Kcut,
-      c->d_Kref, c->d_Y, (int)c->n_celem, nb, tpe, c->g, theta);
-  SC_CUDA(cudaGetLastError());
+  if (c->n_celem_cut > 0) {
+    const unsigned blocks = (unsigned)((c->n_celem_cut + epb - 1) / epb);
+    k_celem<<<blocks, epb * tpe, sizeof(double) * epb * nb, st>>>(
+        mode, A, B, vc ? vc : c->d_vc, c->d_ac, c->dt, c->d_celem_cell, c->d_celem_kidx, c->d_celem_cidx, c->d_Kcut,
+        c->d_Kref, c->d_Y, (int)c->n_celem_cut, nb, tpe, c->g, theta, c->d_celem_cut_ids);
+    SC_CUDA(cudaGetLastError());
+  }
+  if (c->n_celem_ref > 0) {
+    const unsigned rb = (unsigned)((c->n_celem_ref + CR_EB - 1) / CR_EB);
+    const size_t rsm = sizeof(double) * CR_EB * nb;
+    const double* vcp = vc ? vc : c->d_vc;
+    auto ref = [&](auto kern) {
+      kern<<<rb, 256, rsm, st>>>(mode, A, B, vcp, c->d_ac, c->dt, c->d_celem_cell, c->d_celem_cidx, c->d_Kref, c->d_Y,
+                                 (int)c->n_celem_ref, nb, c->g, theta, c->d_celem_ref_ids);
+    };
+    if (nb == 125) {
+      ref(k_celem_ref<125>);
+    } else if (nb == 64) {
+      ref(k_celem_ref<64>);
+    } else if (nb == 27) {
+      ref(k_celem_ref<27>);
+    } else {   // other element sizes (2D, p >= 5 in 3D): the streaming kernel
+      const unsigned blocks = (unsigned)((c->n_celem_ref + epb - 1) / epb);
+      k_celem<<<blocks, epb * tpe, sizeof(double) * epb * nb, st>>>(
+          mode, A, B, vc ? vc : c->d_vc, c->d_ac, c->dt, c->d_celem_cell, c->d_celem_kidx, c->d_celem_cidx, c->d_Kcut,
+          c->d_Kref, c->d_Y, (int)c->n_celem_ref, nb, tpe, c->g, theta, c->d_celem_ref_ids);
+    }
+    SC_CUDA(cudaGetLastError());
+  }
 }
 
 static void launch_irregular(sc_ctx* c, const double* U, const double* Pv, double* out, double a1, double a2,
