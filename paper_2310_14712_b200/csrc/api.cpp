@@ -65,6 +65,9 @@ static void free_ctx(sc_ctx* c) {
   if (c->s_hi) cudaStreamDestroy(c->s_hi);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->s_ref) cudaStreamDestroy(c->s_ref);
+  if (c->ev_ref0) cudaEventDestroy(c->ev_ref0);
+  if (c->ev_ref1) cudaEventDestroy(c->ev_ref1);
   if (cur >= 0) cudaSetDevice(cur);
   delete c;
 }

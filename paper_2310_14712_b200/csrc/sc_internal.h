@@ -185,6 +185,8 @@ struct sc_ctx {
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
   cudaStream_t s_hi = nullptr;             // high-priority stream of the c part
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t s_ref = nullptr;            // side stream of the reference-element products
+  cudaEvent_t ev_ref0 = nullptr, ev_ref1 = nullptr;
   bool far_ready = false;                  // far-d update of the current step already enqueued
   bool pipelined = false;                  // SC_PIPELINE: far-d update forked against the c part
   int far_cap = 0;                         // resident CTAs per SM of the forked far-d update (0 = no cap)

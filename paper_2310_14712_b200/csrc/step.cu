@@ -644,19 +644,26 @@ static void launch_celem(sc_ctx* c, int mode, const double* A, const double* B, 
   const int nb = c->nb;
   const int tpe = std::min(256, ((nb + 31) / 32) * 32);
   const int epb = 256 / tpe;
-  if (c->n_celem_cut > 0) {
-    const unsigned blocks = (unsigned)((c->n_celem_cut + epb - 1) / epb);
-    k_celem<<<blocks, epb * tpe, sizeof(double) * epb * nb, st>>>(
-        mode, A, B, vc ? vc : c->d_vc, c->d_ac, c->dt, c->d_celem_cell, c->d_celem_kidx, c->d_celem_cidx, c->d_Kcut,
-        c->d_Kref, c->d_Y, (int)c->n_celem_cut, nb, tpe, c->g, theta, c->d_celem_cut_ids);
-    SC_CUDA(cudaGetLastError());
+  const double* vcp = vc ? vc : c->d_vc;
+  // the reference-element products run on a side stream beside the (HBM-bound) cut-element
+  // stream: disjoint outputs, both only read the state; joined before returning
+  const bool fork = c->n_celem_cut > 0 && c->n_celem_ref > 0;
+  cudaStream_t sr = st;
+  if (fork) {
+    if (!c->s_ref) {
+      SC_CUDA(cudaStreamCreateWithFlags(&c->s_ref, cudaStreamNonBlocking));
+      SC_CUDA(cudaEventCreateWithFlags(&c->ev_ref0, cudaEventDisableTiming));
+      SC_CUDA(cudaEventCreateWithFlags(&c->ev_ref1, cudaEventDisableTiming));
+    }
+    SC_CUDA(cudaEventRecord(c->ev_ref0, st));
+    SC_CUDA(cudaStreamWaitEvent(c->s_ref, c->ev_ref0, 0));
+    sr = c->s_ref;
   }
   if (c->n_celem_ref > 0) {
     const unsigned rb = (unsigned)((c->n_celem_ref + CR_EB - 1) / CR_EB);
     const size_t rsm = sizeof(double) * CR_EB * nb;
-    const double* vcp = vc ? vc : c->d_vc;
     auto ref = [&](auto kern) {
-      kern<<<rb, 256, rsm, st>>>(mode, A, B, vcp, c->d_ac, c->dt, c->d_celem_cell, c->d_celem_cidx, c->d_Kref, c->d_Y,
+      kern<<<rb, 256, rsm, sr>>>(mode, A, B, vcp, c->d_ac, c->dt, c->d_celem_cell, c->d_celem_cidx, c->d_Kref, c->d_Y,
                                  (int)c->n_celem_ref, nb, c->g, theta, c->d_celem_ref_ids);
     };
     if (nb == 125) {
@@ -667,11 +674,22 @@ static void launch_celem(sc_ctx* c, int mode, const double* A, const double* B, 
       ref(k_celem_ref<27>);
     } else {   // other element sizes (2D, p >= 5 in 3D): the streaming kernel
       const unsigned blocks = (unsigned)((c->n_celem_ref + epb - 1) / epb);
-      k_celem<<<blocks, epb * tpe, sizeof(double) * epb * nb, st>>>(
-          mode, A, B, vc ? vc : c->d_vc, c->d_ac, c->dt, c->d_celem_cell, c->d_celem_kidx, c->d_celem_cidx, c->d_Kcut,
-          c->d_Kref, c->d_Y, (int)c->n_celem_ref, nb, tpe, c->g, theta, c->d_celem_ref_ids);
+      k_celem<<<blocks, epb * tpe, sizeof(double) * epb * nb, sr>>>(
+          mode, A, B, vcp, c->d_ac, c->dt, c->d_celem_cell, c->d_celem_kidx, c->d_celem_cidx, c->d_Kcut, c->d_Kref,
+          c->d_Y, (int)c->n_celem_ref, nb, tpe, c->g, theta, c->d_celem_ref_ids);
     }
     SC_CUDA(cudaGetLastError());
+  }
+  if (c->n_celem_cut > 0) {
+    const unsigned blocks = (unsigned)((c->n_celem_cut + epb - 1) / epb);
+    k_celem<<<blocks, epb * tpe, sizeof(double) * epb * nb, st>>>(
+        mode, A, B, vcp, c->d_ac, c->dt, c->d_celem_cell, c->d_celem_kidx, c->d_celem_cidx, c->d_Kcut, c->d_Kref,
+        c->d_Y, (int)c->n_celem_cut, nb, tpe, c->g, theta, c->d_celem_cut_ids);
+    SC_CUDA(cudaGetLastError());
+  }
+  if (fork) {
+    SC_CUDA(cudaEventRecord(c->ev_ref1, sr));
+    SC_CUDA(cudaStreamWaitEvent(st, c->ev_ref1, 0));
   }
 }
 
