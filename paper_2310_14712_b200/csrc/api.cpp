@@ -52,7 +52,7 @@ static void free_ctx(sc_ctx* c) {
                   c->d_ft, c->d_step, c->d_flag, c->d_irr_lat, c->d_irr_invm, c->d_irr_fx, c->d_load_lat, c->d_load_fxm, c->d_Kref,
                   c->d_c_lat, c->d_vc, c->d_ac, c->d_fxc, c->d_b, c->d_q, c->d_x, c->d_U,
                   c->d_celem_cell, c->d_celem_kidx, c->d_celem_cidx, c->d_celem_cut_ids, c->d_celem_ref_ids,
-                  c->d_Kcut, c->d_cut_dt, c->d_Y, c->d_rhs_ptr,
+                  c->d_Kcut, c->d_Kpk, c->d_cut_dt, c->d_Y, c->d_rhs_ptr,
                   c->d_rhs_idx, c->d_sn_c0, c->d_sn_w, c->d_sn_r, c->d_sn_aoff, c->d_sn_roff,
                   c->d_sn_uoff, c->d_sn_goff, c->d_R, c->d_gptr, c->d_gidx, c->d_items, c->fS.A,
                   c->fM.A, c->fS.d, c->fM.d, c->d_tmp, c->d_nitem, c->d_chptr, c->d_chidx, c->d_parent, c->d_solve_cnt,
@@ -235,8 +235,10 @@ extern "C" sc_status sc_setup(const sc_grid* grid, int32_t p, double alpha, cons
       const double nbd = (double)c->nb;
       // tensor-d nodes (the explicit launch, sc_profile 0): read u_n, u_{n-1}; write u_{n+1}
       const double ex = 24.0 * (double)(c->n_d - c->n_irr);
-      // c-element products: dense cut K_e once, w gathered and Y written per element node
-      const double ce = 8.0 * (double)c->n_cut * nbd * nbd + 16.0 * (double)c->n_celem * nbd;
+      // c-element products: each cut K_e once (packed lower triangle, else dense), w gathered
+      // and Y written per element node
+      const double kb = c->d_Kpk ? nbd * (nbd + 1.0) / 2.0 : nbd * nbd;
+      const double ce = 8.0 * (double)c->n_cut * kb + 16.0 * (double)c->n_celem * nbd;
       // solve: forward streams every panel [D_s; G_s], backward G_s again; b, q, x vectors
       // and the update vectors U (written once, read once)
       const double so = 8.0 * (double)(c->nnz_factor + c->nnz_G) + 32.0 * (double)c->n_cl + 16.0 * (double)c->sum_r;

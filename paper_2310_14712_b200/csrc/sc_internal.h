@@ -148,7 +148,8 @@ struct sc_ctx {
   int64_t n_celem_cut = 0, n_celem_ref = 0;
   int32_t* d_celem_cut_ids = nullptr;   // c elements with a dense cut K_e
   int32_t* d_celem_ref_ids = nullptr;   // uncut c elements (reference K_e)
-  double* d_Kcut = nullptr;          // n_cut x nb x nb
+  double* d_Kcut = nullptr;          // n_cut x nb x nb (setup; dropped once packed)
+  double* d_Kpk = nullptr;           // n_cut x nb(nb+1)/2: packed lower triangles (step)
   double* d_cut_dt = nullptr;        // [n_cut][2] cell-wise critical step (consistent, HRZ) of the cut cells
   int ct_T = 0, ct_nt = 0, ct_TS = 0;   // tiles: T rows, nt per dimension, TS doubles (stride)
   long long ct_ms = 0;                  // doubles per stored matrix

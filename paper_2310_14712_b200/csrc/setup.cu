@@ -275,24 +275,29 @@ __global__ void __launch_bounds__(256) k_cut_matrices(GridP g, const DVoid* __re
     for (int b = 0; b < 4; ++b) accM[a][b] = accK[a][b] = cmpM[a][b] = cmpK[a][b] = 0.0;
   for (long long q0 = 0; q0 < total; q0 += QC) {
     const int nq = (int)min((long long)QC, total - q0);
-    // per point, per axis: 1D basis values/derivatives; weight with alpha
-    for (int t = threadIdx.x; t < nq * 3; t += blockDim.x) {
-      const int qq = t / 3, k = t % 3;
-      const long long q = q0 + qq;
-      const unsigned long long lf = leaves[(long long)sl * cap + q / npts];
-      const int l = (int)(lf >> 48);
-      const int a = (int)((lf >> (16 * k)) & 0xFFFF);
-      int loc = (int)(q % npts);
-      int gk = (k == 0) ? loc % P1 : (k == 1 ? (loc / P1) % P1 : loc / (P1 * P1));
-      if (k < d) {
-        double xi = -1.0 + (2.0 * a + 1.0 + gx[gk]) * ldexp(1.0, -l);
-        for (int i = 0; i < P1; ++i) {
-          double dd;
-          sphi[(qq * 3 + k) * SC_MAXP1 + i] = d_lagr(gll, P1, i, xi, &dd);
-          sdph[(qq * 3 + k) * SC_MAXP1 + i] = dd * (2.0 / hk[k]);
-        }
-      }
-      if (k == 0) {
+    // per point, per axis, per basis function: the 1D value/derivative, one thread each;
+    // the alpha-weighted quadrature weight of each point on the threads after those
+    const int nbas = nq * 3 * P1;
+    for (int t = threadIdx.x; t < nbas + nq; t += blockDim.x) {
+      if (t < nbas) {
+        const int i = t % P1, qk = t / P1, qq = qk / 3, k = qk % 3;
+        if (k >= d) continue;
+        const long long q = q0 + qq;
+        const unsigned long long lf = leaves[(long long)sl * cap + q / npts];
+        const int l = (int)(lf >> 48);
+        const int a = (int)((lf >> (16 * k)) & 0xFFFF);
+        const int loc = (int)(q % npts);
+        const int gk = (k == 0) ? loc % P1 : (k == 1 ? (loc / P1) % P1 : loc / (P1 * P1));
+        const double xi = -1.0 + (2.0 * a + 1.0 + gx[gk]) * ldexp(1.0, -l);
+        double dd;
+        sphi[(qq * 3 + k) * SC_MAXP1 + i] = d_lagr(gll, P1, i, xi, &dd);
+        sdph[(qq * 3 + k) * SC_MAXP1 + i] = dd * (2.0 / hk[k]);
+      } else {
+        const int qq = t - nbas;
+        const long long q = q0 + qq;
+        const unsigned long long lf = leaves[(long long)sl * cap + q / npts];
+        const int l = (int)(lf >> 48);
+        const int loc = (int)(q % npts);
         // alpha at the physical Gauss point (same arithmetic as the classifier)
         double x[3] = {0.0, 0.0, 0.0};
         double w = 1.0;

@@ -158,14 +158,26 @@ static void launch_load_d(sc_ctx* c, double* out, double a3, cudaStream_t st) {
 // mode 2 (leap-frog substep, integrator 4): w = u^c_k (compact, vc) on c nodes, the d values
 // A + theta (B - A) elsewhere (reading LF3: theta = k/m interpolated, 0 frozen).
 // Y[e][i] = sum_j K_e[i][j] w_j (K_e symmetric: read as columns, coalesced across threads).
-// (Tiled-symmetric storage of the upper K_e tiles was measured slower in four layouts, see
-// profiles/r2_variants.txt, so the full matrices are streamed.)
+// k_celem streams a dense K_e (element sizes without a packed kernel); cut elements of the
+// common sizes use k_celem_sym on the packed lower triangle (below).
 #ifndef CELEM_U
 #define CELEM_U 8
 #endif
 #ifndef CELEM_CS
 #define CELEM_CS 0
 #endif
+#ifndef CESYM_PF
+#define CESYM_PF 0
+#endif
+#ifndef CESYM_OFF
+#define CESYM_OFF 0
+#endif
+#ifndef CESYM_G
+#define CESYM_G 8
+#endif
+__host__ __device__ constexpr int brev5(int n) {
+  return ((n & 1) << 4) | ((n & 2) << 2) | (n & 4) | ((n & 8) >> 2) | ((n & 16) >> 4);
+}
 // local node j of c element e: its value in w_e = [u^d_{n+1}; u~^c] (mode 0: predictor for c
 // nodes), u (mode 1), or the leap-frog substep value (mode 2)
 __device__ __forceinline__ double celem_w(int mode, const double* __restrict__ A, const double* __restrict__ B,
@@ -238,6 +250,142 @@ __global__ void k_celem(int mode, const double* __restrict__ A, const double* __
   // matrix stays cached
   if (CELEM_CS && kidx >= 0) gemv([](const double* p) { return __ldcs(p); });
   else gemv([](const double* p) { return __ldg(p); });
+}
+
+// Cut c elements on the PACKED lower triangle of their symmetric K_e (row i holds K[i][0..i]
+// at offset i(i+1)/2: nb(nb+1)/2 doubles, 50.4% of the dense bytes at nb = 125).  One warp
+// per element; lane l owns the columns j = l + 32c.  Row i is read coalesced (lanes over
+// j <= i) and every stored entry is used twice:
+//   row part     s_i   = sum_{j<=i} K_ij w_j   (per-lane partials, 32 rows per block, then
+//                                                one transposing butterfly: lane m gets row m)
+//   column part  t_j  += K_ij w_i  (j < i)     (lane-owned accumulators, no reduction)
+// so y = s + t.  w_i is broadcast by a shuffle from its owning lane.  The row loop is
+// unrolled at compile time (NB), so every load has an immediate offset from the element base.
+#ifndef CESYM_MINB
+#define CESYM_MINB 10
+#endif
+#if CESYM_MINB > 0
+#define CESYM_LB __launch_bounds__(128, CESYM_MINB)
+#else
+#define CESYM_LB __launch_bounds__(128)
+#endif
+// L2 prefetch of packed rows [r0, r1) of the element (lanes over 128-byte lines)
+__device__ __forceinline__ void cesym_prefetch(const double* K, int r0, int r1, int lane) {
+  const char* a = (const char*)(K + (long long)r0 * (r0 + 1) / 2);
+  const char* b = (const char*)(K + (long long)r1 * (r1 + 1) / 2);
+  const char* a0 = (const char*)((unsigned long long)a & ~127ull);
+  for (const char* q = a0 + 128 * lane; q < b; q += 128 * 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+}
+template <int NB>
+__global__ void CESYM_LB k_celem_sym(int mode, const double* __restrict__ A, const double* __restrict__ B,
+                                                   const double* __restrict__ vc, const double* __restrict__ ac,
+                                                   double dt, const int32_t* __restrict__ ecell,
+                                                   const int32_t* __restrict__ ekidx, const int32_t* __restrict__ ecidx,
+                                                   const double* __restrict__ Kpk, double* __restrict__ Y, int ne,
+                                                   GridP g, double theta, const int32_t* __restrict__ ids) {
+  constexpr int NK = (NB + 31) / 32;
+  constexpr long long NT = (long long)NB * (NB + 1) / 2;
+  const int lane = threadIdx.x & 31;
+  const int slot = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (slot >= ne) return;   // warp-uniform
+  const int e = ids[slot];
+  const double* __restrict__ K = Kpk + (long long)ekidx[e] * NT;
+#if CESYM_PF
+  // the element's whole packed triangle as one bulk L2 prefetch (16-byte granules), issued
+  // before the w gather so that the row loads below find it in L2
+  if (lane == 0) {
+    const unsigned long long a0 = (unsigned long long)K & ~15ull;
+    const unsigned long long a1 = ((unsigned long long)(K + NT) + 15ull) & ~15ull;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((unsigned)(a1 - a0)) : "memory");
+  }
+#endif
+#if CESYM_PF == 2
+  cesym_prefetch(K, 0, NB < 64 ? NB : 64, lane);
+#endif
+  long long ci[3];
+  cell_ci(g, ecell[e], ci);
+  double wr[NK], at[NK], yr[NK];
+#pragma unroll
+  for (int c = 0; c < NK; ++c) {
+    const int j = lane + 32 * c;
+    wr[c] = j < NB ? celem_w(mode, A, B, vc, ac, dt, ecidx, e, NB, j, ci, g, theta) : 0.0;
+    at[c] = 0.0;
+  }
+#pragma unroll
+  for (int b = 0; b < NK; ++b) {
+    // rows in bit-reversed order n -> m = brev5(n): the transposing butterfly (31 shuffles
+    // per 32 rows) then runs as a binary counter over the row partials -- the stage of width
+    // 16 >> lv pairs consecutive results of level lv -- so at most 5 partials stay live and
+    // the registers go to loads in flight (CESYM_G rows' loads issued before their FMAs)
+#if CESYM_PF == 2
+    if (b >= 1 && 32 * (b + 1) < NB) cesym_prefetch(K, 32 * (b + 1), 32 * (b + 2) < NB ? 32 * (b + 2) : NB, lane);
+#endif
+    double pend[5], cur = 0.0;
+#pragma unroll
+    for (int n0 = 0; n0 < 32; n0 += CESYM_G) {
+      double x[CESYM_G][NK];
+#pragma unroll
+      for (int gq = 0; gq < CESYM_G; ++gq) {
+        const int m = brev5(n0 + gq), i = 32 * b + m;
+#pragma unroll
+        for (int c = 0; c <= b; ++c) {
+          x[gq][c] = 0.0;
+          if (i < NB && (c < b || lane <= m)) x[gq][c] = __ldg(K + i * (i + 1) / 2 + lane + 32 * c);   // j <= i
+        }
+      }
+#pragma unroll
+      for (int gq = 0; gq < CESYM_G; ++gq) {
+        const int n = n0 + gq, m = brev5(n), i = 32 * b + m;
+        double p = 0.0;
+        if (i < NB) {
+          const double wi = __shfl_sync(0xffffffffu, wr[b], m);
+#pragma unroll
+          for (int c = 0; c <= b; ++c) {
+            p = fma(x[gq][c], wr[c], p);
+            if (c < b || lane < m) at[c] = fma(x[gq][c], wi, at[c]);
+          }
+        }
+        cur = p;
+#pragma unroll
+        for (int lv = 0; lv < 5; ++lv) {
+          if (((n >> lv) & 1) == 0) {
+            pend[lv] = cur;
+            break;
+          }
+          // stage of width w: each lane keeps the partner whose row bit w matches its lane bit
+          const int w = 16 >> lv;
+          const bool up = (lane & w) != 0;
+          const double lo = pend[lv], hi = cur;
+          cur = (up ? hi : lo) + __shfl_xor_sync(0xffffffffu, up ? lo : hi, w);
+        }
+      }
+    }
+    yr[b] = cur;   // n = 31 carried through all five levels: lane l holds row 32b + l
+  }
+#pragma unroll
+  for (int c = 0; c < NK; ++c) {
+    const int j = lane + 32 * c;
+    if (j < NB) Y[(size_t)e * NB + j] = yr[c] + at[c];
+  }
+}
+
+// setup: dense symmetric K_e -> packed lower triangle (one CTA per cut cell)
+__global__ void k_pack_lower(const double* __restrict__ K, double* __restrict__ P, int nb) {
+  const long long e = blockIdx.x;
+  const long long nt = (long long)nb * (nb + 1) / 2;
+  for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+    int i = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while ((long long)i * (i + 1) / 2 > t) --i;
+    while ((long long)(i + 1) * (i + 2) / 2 <= t) ++i;
+    const int j = t - i * (i + 1) / 2;
+    P[e * nt + t] = K[(e * nb + i) * nb + j];
+  }
+}
+
+// nb with a packed-symmetric cut-element kernel
+static bool celem_sym_nb(int nb) {
+  if (CESYM_OFF) return false;
+  return nb == 125 || nb == 64 || nb == 27 || nb == 25 || nb == 5;
 }
 
 // Uncut c elements all share the reference K_e (Kref, symmetric): Y_e = Kref w_e for a batch of
@@ -680,7 +828,22 @@ static void launch_celem(sc_ctx* c, int mode, const double* A, const double* B, 
     }
     SC_CUDA(cudaGetLastError());
   }
-  if (c->n_celem_cut > 0) {
+  if (c->n_celem_cut > 0 && c->d_Kpk) {
+    const unsigned blocks = (unsigned)((c->n_celem_cut + 3) / 4);
+    auto sym = [&](auto kern) {
+      kern<<<blocks, 128, 0, st>>>(mode, A, B, vcp, c->d_ac, c->dt, c->d_celem_cell, c->d_celem_kidx, c->d_celem_cidx,
+                                   c->d_Kpk, c->d_Y, (int)c->n_celem_cut, c->g, theta, c->d_celem_cut_ids);
+    };
+    switch (nb) {
+      case 125: sym(k_celem_sym<125>); break;
+      case 64: sym(k_celem_sym<64>); break;
+      case 27: sym(k_celem_sym<27>); break;
+      case 25: sym(k_celem_sym<25>); break;
+      case 5: sym(k_celem_sym<5>); break;
+      default: throw ScError(SC_ERR_CONFIG, "packed K_e without a kernel");
+    }
+    SC_CUDA(cudaGetLastError());
+  } else if (c->n_celem_cut > 0) {
     const unsigned blocks = (unsigned)((c->n_celem_cut + epb - 1) / epb);
     k_celem<<<blocks, epb * tpe, sizeof(double) * epb * nb, st>>>(
         mode, A, B, vcp, c->d_ac, c->dt, c->d_celem_cell, c->d_celem_kidx, c->d_celem_cidx, c->d_Kcut, c->d_Kref,
@@ -846,6 +1009,18 @@ void build_graphs(sc_ctx* c) {
 void setup_step_structures(sc_ctx* c) {
   GridP& g = c->g;
   explicit_prepare(c);
+  // cut K_e -> packed lower triangles (the step streams half the bytes); the dense copy is
+  // dropped once the host copy for the factorisation (setup_device_geometry) has landed
+  if (c->n_cut > 0 && c->d_Kcut && celem_sym_nb(c->nb)) {
+    const int nb = c->nb;
+    SC_CUDA(cudaStreamSynchronize(c->stream));
+    SC_CUDA(cudaMalloc(&c->d_Kpk, sizeof(double) * (size_t)c->n_cut * nb * (nb + 1) / 2));
+    k_pack_lower<<<(unsigned)c->n_cut, 256, 0, c->stream>>>(c->d_Kcut, c->d_Kpk, nb);
+    SC_CUDA(cudaGetLastError());
+    SC_CUDA(cudaStreamSynchronize(c->stream));
+    SC_CUDA(cudaFree(c->d_Kcut));
+    c->d_Kcut = nullptr;
+  }
   c->n_near_tiles = c->n_far_tiles = 0;
   if (g.dim == 1) return;
   int ext[3], tg[3];
