@@ -280,7 +280,7 @@ def main():
     # stream, sc_profile) and the roofline of the dominant one (largest time per step)
     peak, peak_kind = _peaks()
     kern = {"explicit": (0, info["bytes_explicit_per_step"], "k_explicit (a1)+(a2), tensor-d DOFs"),
-            "celem": (1, info["bytes_celem_per_step"], "k_celem (a3)+(a4) c-element products"),
+            "celem": (1, info["bytes_celem_per_step"], "k_celem_sym + k_celem_ref (a3)+(a4) c-element products"),
             "solve": (2, info["bytes_solve_per_step"], "k_solve (a5) persistent supernodal solve")}
     breakdown = {}
     for name, (which, nbytes, _) in kern.items():
