@@ -390,18 +390,28 @@ static bool celem_sym_nb(int nb) {
 
 // Uncut c elements all share the reference K_e (Kref, symmetric): Y_e = Kref w_e for a batch of
 // CR_EB elements is one small GEMM Kref [nb x nb] x W [nb x CR_EB].  W gathered into shared
-// memory; each thread a 4-row x 4-element register tile (lanes over rows, warps over
-// elements), Kref rows read through L1 (128 KB, cached), W broadcast from shared memory.
-#define CR_EB 32
+// memory; each thread a 4-row x CR_EPW-element register tile (lanes over rows, warps over
+// elements), Kref rows read through L1 (128 KB, cached), W broadcast from shared memory:
+// per j, 4 row loads + CR_EPW/2 16-byte W loads feed 4 CR_EPW FMAs (at CR_EPW = 4 the L1
+// wavefronts, not the FP64 pipe, bound the loop).  Every (row, element) sum runs over j in
+// ascending order whatever the tile, so the result does not depend on CR_EPW / CR_NW.
+#ifndef CR_EPW
+#define CR_EPW 8    // elements per warp
+#endif
+#ifndef CR_NW
+#define CR_NW 4     // warps per CTA
+#endif
+#define CR_NT (32 * CR_NW)
+#define CR_EB (CR_NW * CR_EPW)
 template <int NB>   // nodes per element (compile time: the product loop is unrolled)
-__global__ void __launch_bounds__(256) k_celem_ref(int mode, const double* __restrict__ A, const double* __restrict__ B,
+__global__ void __launch_bounds__(CR_NT) k_celem_ref(int mode, const double* __restrict__ A, const double* __restrict__ B,
                                                    const double* __restrict__ vc, const double* __restrict__ ac,
                                                    double dt, const int32_t* __restrict__ ecell,
                                                    const int32_t* __restrict__ ecidx, const double* __restrict__ Kref,
                                                    double* __restrict__ Y, int n, int /*nb*/, GridP g, double theta,
                                                    const int32_t* __restrict__ ids) {
   constexpr int nb = NB;
-  extern __shared__ double sW[];   // [nb][CR_EB]
+  extern __shared__ __align__(16) double sW[];   // [nb][CR_EB]
   __shared__ long long sci[CR_EB][3];
   __shared__ int se[CR_EB];
   const int s0 = blockIdx.x * CR_EB;
@@ -414,52 +424,56 @@ __global__ void __launch_bounds__(256) k_celem_ref(int mode, const double* __res
     for (int k = 0; k < 3; ++k) sci[threadIdx.x][k] = ci[k];
   }
   __syncthreads();
-  // gather W: each thread's (up to 16) entries in two passes, so that their loads are in flight
+  // gather W: GU entries per thread at a time in two passes, so that their loads are in flight
   // together (lattice index + c index first, then the values)
-  constexpr int GU = CR_EB * 128 / 256;
+  constexpr int GT = CR_EB * 128 / CR_NT;   // entries per thread
+  constexpr int GU = GT < 16 ? GT : 16;
+  static_assert(GT % GU == 0, "gather chunks");
   const int n1 = g.p + 1;
-  long long glv[GU];
-  int ccv[GU];
+  for (int u0 = 0; u0 < GT; u0 += GU) {
+    long long glv[GU];
+    int ccv[GU];
 #pragma unroll
-  for (int u = 0; u < GU; ++u) {
-    const int t = threadIdx.x + u * 256;
-    const int b = t / nb, j = t - b * nb;
-    glv[u] = -1;
-    ccv[u] = -1;
-    if (t < CR_EB * nb && b < ne) {
-      const int l0 = j % n1, l1 = (j / n1) % n1, l2 = j / (n1 * n1);
-      long long gl = sci[b][0] * g.p + l0;
-      if (g.dim > 1) gl += g.nl[0] * (sci[b][1] * g.p + l1);
-      if (g.dim > 2) gl += g.nl[0] * g.nl[1] * (sci[b][2] * g.p + l2);
-      glv[u] = gl;
-      if (mode != 1) ccv[u] = ecidx[(size_t)se[b] * nb + j];
+    for (int u = 0; u < GU; ++u) {
+      const int t = threadIdx.x + (u0 + u) * CR_NT;
+      const int b = t / nb, j = t - b * nb;
+      glv[u] = -1;
+      ccv[u] = -1;
+      if (t < CR_EB * nb && b < ne) {
+        const int l0 = j % n1, l1 = (j / n1) % n1, l2 = j / (n1 * n1);
+        long long gl = sci[b][0] * g.p + l0;
+        if (g.dim > 1) gl += g.nl[0] * (sci[b][1] * g.p + l1);
+        if (g.dim > 2) gl += g.nl[0] * g.nl[1] * (sci[b][2] * g.p + l2);
+        glv[u] = gl;
+        if (mode != 1) ccv[u] = ecidx[(size_t)se[b] * nb + j];
+      }
     }
-  }
 #pragma unroll
-  for (int u = 0; u < GU; ++u) {
-    const int t = threadIdx.x + u * 256;
-    if (t >= CR_EB * nb) break;
-    const int b = t / nb, j = t - b * nb;
-    double v = 0.0;
-    const long long gl = glv[u];
-    const int cc = ccv[u];
-    if (gl >= 0) {
-      if (mode == 1) v = A[gl];
-      else if (mode == 2) v = cc >= 0 ? vc[cc] : fma(theta, B[gl] - A[gl], A[gl]);
-      else v = cc >= 0 ? A[gl] + dt * vc[cc] + 0.25 * dt * dt * ac[cc] : B[gl];
+    for (int u = 0; u < GU; ++u) {
+      const int t = threadIdx.x + (u0 + u) * CR_NT;
+      if (t >= CR_EB * nb) break;
+      const int b = t / nb, j = t - b * nb;
+      double v = 0.0;
+      const long long gl = glv[u];
+      const int cc = ccv[u];
+      if (gl >= 0) {
+        if (mode == 1) v = A[gl];
+        else if (mode == 2) v = cc >= 0 ? vc[cc] : fma(theta, B[gl] - A[gl], A[gl]);
+        else v = cc >= 0 ? A[gl] + dt * vc[cc] + 0.25 * dt * dt * ac[cc] : B[gl];
+      }
+      sW[j * CR_EB + b] = v;
     }
-    sW[j * CR_EB + b] = v;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, wg = threadIdx.x >> 5;
-  const int b0 = wg * 4;   // this warp's 4 elements; lanes take rows lane + 32 a (coalesced)
+  const int b0 = wg * CR_EPW;   // this warp's elements; lanes take rows lane + 32 a (coalesced)
   if (b0 >= ne) return;
   for (int rb = 0; rb < nb; rb += 128) {   // nb <= 128 in 3D p = 4: one pass
-    double acc[4][4];
+    double acc[4][CR_EPW];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+      for (int c = 0; c < CR_EPW; ++c) acc[a][c] = 0.0;
 #pragma unroll 5
     for (int j = 0; j < nb; ++j) {
       double k[4];
@@ -469,16 +483,20 @@ __global__ void __launch_bounds__(256) k_celem_ref(int mode, const double* __res
         k[a] = r < nb ? __ldg(Kref + (size_t)j * nb + r) : 0.0;   // Kref[r][j] (symmetric)
       }
       const double* wj = sW + j * CR_EB + b0;
-      double w[4];
+      double w[CR_EPW];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) w[c] = wj[c];
+      for (int c = 0; c < CR_EPW; c += 2) {
+        const double2 w2 = *reinterpret_cast<const double2*>(wj + c);
+        w[c] = w2.x;
+        w[c + 1] = w2.y;
+      }
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) acc[a][c] = fma(k[a], w[c], acc[a][c]);
+        for (int c = 0; c < CR_EPW; ++c) acc[a][c] = fma(k[a], w[c], acc[a][c]);
     }
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < CR_EPW; ++c) {
       if (b0 + c >= ne) break;
       double* y = Y + (size_t)se[b0 + c] * nb;
 #pragma unroll
@@ -811,7 +829,7 @@ static void launch_celem(sc_ctx* c, int mode, const double* A, const double* B, 
     const unsigned rb = (unsigned)((c->n_celem_ref + CR_EB - 1) / CR_EB);
     const size_t rsm = sizeof(double) * CR_EB * nb;
     auto ref = [&](auto kern) {
-      kern<<<rb, 256, rsm, sr>>>(mode, A, B, vcp, c->d_ac, c->dt, c->d_celem_cell, c->d_celem_cidx, c->d_Kref, c->d_Y,
+      kern<<<rb, CR_NT, rsm, sr>>>(mode, A, B, vcp, c->d_ac, c->dt, c->d_celem_cell, c->d_celem_cidx, c->d_Kref, c->d_Y,
                                  (int)c->n_celem_ref, nb, c->g, theta, c->d_celem_ref_ids);
     };
     if (nb == 125) {
