@@ -392,14 +392,15 @@ static bool celem_sym_nb(int nb) {
 // CR_EB elements is one small GEMM Kref [nb x nb] x W [nb x CR_EB].  W gathered into shared
 // memory; each thread a 4-row x CR_EPW-element register tile (lanes over rows, warps over
 // elements), Kref rows read through L1 (128 KB, cached), W broadcast from shared memory:
-// per j, 4 row loads + CR_EPW/2 16-byte W loads feed 4 CR_EPW FMAs (at CR_EPW = 4 the L1
-// wavefronts, not the FP64 pipe, bound the loop).  Every (row, element) sum runs over j in
-// ascending order whatever the tile, so the result does not depend on CR_EPW / CR_NW.
+// per j, 4 row loads + CR_EPW/2 16-byte W loads feed 4 CR_EPW FMAs.  Every (row, element)
+// sum runs over j in ascending order whatever the tile, so the result does not depend on
+// CR_EPW / CR_NW (8-element tiles at 108 registers measured slower: the loop is
+// latency-bound, profiles/r2_variants.txt).
 #ifndef CR_EPW
-#define CR_EPW 8    // elements per warp
+#define CR_EPW 4    // elements per warp (8 measured slower: profiles/r2_variants.txt)
 #endif
 #ifndef CR_NW
-#define CR_NW 4     // warps per CTA
+#define CR_NW 8     // warps per CTA
 #endif
 #define CR_NT (32 * CR_NW)
 #define CR_EB (CR_NW * CR_EPW)
